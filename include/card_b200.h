@@ -1,0 +1,151 @@
+/*
+ * card_b200.h — C-ABI of the B200-native CARD query-and-correct path.
+ *
+ * Plain pointers and sizes only.  Unless stated otherwise every pointer
+ * argument is a DEVICE pointer owned by the caller, every call is
+ * asynchronous on the caller's cudaStream_t (passed as void*), and every
+ * call returns an int status (CARD_OK or a negative CARD_E_* code).  No
+ * C++ exception crosses this boundary.  Device-side protocol errors (a
+ * rejected walk, a full frontier, a bad distribution) are written to the
+ * cache's status word and read back with card_cache_status().
+ *
+ * Reference interfaces replaced (paths under /root/reference/pkg/src/specache):
+ *   operator plug-in  backend.py:42-47 get_kernels() module protocol
+ *                     {kgram_dist (_kernels.pyx:44-93), rows_topk (_kernels.pyx:96-145)}
+ *   candidate cache   cache.py:92-523 TreeCache
+ *   verification      verify.py:43-132
+ *   model plug-in     lm.py:109-196 ToyModel.next_distribution / batch_tree_forward
+ * One cache handle per request, never shared by two writers.
+ */
+#ifndef CARD_B200_H
+#define CARD_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CARD_ABI_VERSION 1
+
+/* status codes; the Python mirror maps them onto errors.py:6-45 */
+#define CARD_OK              0
+#define CARD_E_INPUT        -1   /* InputError      */
+#define CARD_E_CONFIG       -2   /* ConfigError     */
+#define CARD_E_PROTOCOL     -3   /* ProtocolError   */
+#define CARD_FRONTIER_FULL  -4   /* FrontierFull    */
+#define CARD_E_CAPACITY     -5   /* arena capacity exhausted (sizing bug) */
+#define CARD_E_CUDA         -6   /* CUDA runtime error */
+#define CARD_E_MASK         -7   /* MaskError       */
+
+int         card_abi_version(void);
+const char* card_strerror(int code);
+/* last CUDA error string recorded by a failing call (host memory, static) */
+const char* card_last_cuda_error(void);
+
+/* ------------------------------------------------------------------ *
+ * operator plug-in (backend.py:42-47)
+ * ------------------------------------------------------------------ */
+
+/* Hashed k-gram next-token distributions for n_rows contexts.
+ * tails: [n_rows, tail_len] int64 (the last `order` tokens of each context);
+ * out: [n_rows, vocab] float64.  Replaces _kernels.pyx:44-93 (bit-exact
+ * integer stream; fp64 softmax with a correctly rounded exp). */
+int card_kgram_dist(uint64_t seed, uint64_t seed2, double mix_weight,
+                    const int64_t* tails, int tail_len, int n_rows, int vocab,
+                    double sharpness, double temperature, double* out, void* stream);
+
+/* Per-row top-k by (p desc, token asc), p <= 0 excluded.  dists:
+ * [n_rows, vocab] float64; out_tok/out_p: [n_rows, k]; out_cnt: [n_rows].
+ * If status != NULL, rows are also validated as in cache.py:204-208
+ * (no NaN / negative, sum within 1e-9 of 1) and *status gets CARD_E_INPUT
+ * on failure.  Replaces _kernels.pyx:96-145. */
+int card_rows_topk(const double* dists, int n_rows, int vocab, int k,
+                   int32_t* out_tok, double* out_p, int32_t* out_cnt,
+                   int32_t* status, void* stream);
+
+/* Correctly rounded natural log / exp over n doubles (parity helpers). */
+int card_log_cr(const double* x, double* y, int n, void* stream);
+int card_exp_cr(const double* x, double* y, int n, void* stream);
+
+/* ------------------------------------------------------------------ *
+ * device candidate tree (cache.py:92-523)
+ * ------------------------------------------------------------------ */
+
+typedef struct card_cache card_cache;
+
+/* Host-visible copy of the device state word block (card_cache_state). */
+typedef struct card_cache_state {
+    int32_t n_nodes, root, n_frontier, epoch;
+    int32_t dead, status, vstatus, stamp;
+    int32_t top_layer, last_width, compacted, moved;
+    int32_t K, k, max_depth, eos;
+    int32_t capacity, hash_mask, fresh, new_root;
+    int32_t q_hit, q_len, chain_len, alive_below;
+} card_cache_state;
+
+/* Create a cache rooted at root_token (cache.py:95-105).  eos_token < 0
+ * means None.  capacity <= 0 picks a bound that covers the corrected
+ * protocol (compaction keeps the arena below ~5*K*max_depth).  This call
+ * allocates device memory and synchronises. */
+int card_cache_create(int root_token, int K, int k, int max_depth, int eos_token,
+                      int capacity, card_cache** out);
+int card_cache_destroy(card_cache* h);
+
+/* reset(root_token) (cache.py:439-444).  If d_root_token != NULL the token
+ * is read on the device (engine path), else root_token is used. */
+int card_cache_reset(card_cache* h, const int32_t* d_root_token, int root_token, void* stream);
+
+/* expand_layer(distributions) (cache.py:224-251): validate, row top-k,
+ * edge = log(p), global top-K by (-weight, token, parent id), allocate,
+ * prune dead ends.  n_rows must equal len(expansion_parents()); pass -1 to
+ * take it from the device (engine path). */
+int card_cache_expand(card_cache* h, const double* dists, int n_rows, int vocab, void* stream);
+
+/* Same, from precomputed per-row candidates (token, log-prob) — the fused
+ * lm_head top-k output.  tok/logp: [n_rows, k]; cnt: [n_rows]. */
+int card_cache_expand_topk(card_cache* h, const int32_t* tok, const double* logp,
+                           const int32_t* cnt, int n_rows, void* stream);
+
+/* Candidate pool of extension_pool() (cache.py:190-222) for the drop-in:
+ * writes P = n_rows*k slots of (token or -1, weight, parent index, edge). */
+int card_cache_pool(card_cache* h, const double* dists, int n_rows, int vocab,
+                    int32_t* out_tok, double* out_w, int32_t* out_pidx, double* out_edge,
+                    void* stream);
+
+/* query(depth) (cache.py:277-318).  Result in the state block (q_hit, q_len)
+ * and in the cache's query buffers (card_cache_query_buffers). */
+int card_cache_query(card_cache* h, int depth, void* stream);
+int card_cache_query_buffers(card_cache* h, int32_t** path, int32_t** tok, double** edge);
+
+/* correct(accepted, correction) (cache.py:355-413).  All inputs on the
+ * device: accepted[0..*n_accepted), *correction < 0 means None. */
+int card_cache_correct(card_cache* h, const int32_t* accepted, const int32_t* n_accepted,
+                       const int32_t* correction, void* stream);
+
+/* advance_root (cache.py:415-437); state.moved = 1 on success, 0 if the
+ * correction token is not cached (caller then resets). */
+int card_cache_advance_root(card_cache* h, const int32_t* accepted, const int32_t* n_accepted,
+                            const int32_t* correction, void* stream);
+
+/* alive_below_root() (cache.py:174-184) into state.alive_below. */
+int card_cache_count_alive(card_cache* h, void* stream);
+
+/* Clear the status word (stream-ordered). */
+int card_cache_clear_status(card_cache* h, void* stream);
+
+/* Synchronous host reads (parity / drop-in API).  Arrays are host buffers of
+ * at least state.n_nodes (arena) / K (frontier) entries; NULL skips one. */
+int card_cache_read_state(card_cache* h, card_cache_state* st, void* stream);
+int card_cache_snapshot(card_cache* h, int32_t* token, int32_t* parent, int32_t* layer,
+                        uint8_t* alive, double* score, double* edge, int32_t* frontier,
+                        void* stream);
+/* Device pointers of the state block and arrays (engine kernels chain on them). */
+int card_cache_device_ptrs(card_cache* h, card_cache_state** st, int32_t** token,
+                           int32_t** parent, int32_t** layer, int32_t** frontier,
+                           int32_t** remap, int32_t** chain);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CARD_B200_H */

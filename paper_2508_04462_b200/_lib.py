@@ -1,0 +1,76 @@
+"""Loader for the in-tree C-ABI library ``libcard_b200.so``.
+
+The product path has no CPU fallback: if the library (or a GPU) is
+missing, every device entry point raises ``DeviceError`` loudly.  The
+signatures below are exactly the declarations of include/card_b200.h.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from ctypes import POINTER, c_double, c_int, c_int32, c_int64, c_uint8, c_uint64, c_void_p
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libcard_b200.so")
+
+_lib = None
+
+
+class CacheState(ctypes.Structure):
+    _fields_ = [(n, c_int32) for n in (
+        "n_nodes", "root", "n_frontier", "epoch", "dead", "status", "vstatus", "stamp",
+        "top_layer", "last_width", "compacted", "moved", "K", "k", "max_depth", "eos",
+        "capacity", "hash_mask", "fresh", "new_root", "q_hit", "q_len", "chain_len", "alive_below")]
+
+
+# name -> (restype, argtypes)
+_P = c_void_p
+SIGNATURES = {
+    "card_abi_version": (c_int, []),
+    "card_strerror": (ctypes.c_char_p, [c_int]),
+    "card_last_cuda_error": (ctypes.c_char_p, []),
+    "card_kgram_dist": (c_int, [c_uint64, c_uint64, c_double, _P, c_int, c_int, c_int, c_double, c_double, _P, _P]),
+    "card_rows_topk": (c_int, [_P, c_int, c_int, c_int, _P, _P, _P, _P, _P]),
+    "card_log_cr": (c_int, [_P, _P, c_int, _P]),
+    "card_exp_cr": (c_int, [_P, _P, c_int, _P]),
+    "card_cache_create": (c_int, [c_int, c_int, c_int, c_int, c_int, c_int, POINTER(c_void_p)]),
+    "card_cache_destroy": (c_int, [_P]),
+    "card_cache_reset": (c_int, [_P, _P, c_int, _P]),
+    "card_cache_expand": (c_int, [_P, _P, c_int, c_int, _P]),
+    "card_cache_expand_topk": (c_int, [_P, _P, _P, _P, c_int, _P]),
+    "card_cache_pool": (c_int, [_P, _P, c_int, c_int, _P, _P, _P, _P, _P]),
+    "card_cache_query": (c_int, [_P, c_int, _P]),
+    "card_cache_query_buffers": (c_int, [_P, POINTER(c_void_p), POINTER(c_void_p), POINTER(c_void_p)]),
+    "card_cache_correct": (c_int, [_P, _P, _P, _P, _P]),
+    "card_cache_advance_root": (c_int, [_P, _P, _P, _P, _P]),
+    "card_cache_count_alive": (c_int, [_P, _P]),
+    "card_cache_clear_status": (c_int, [_P, _P]),
+    "card_cache_read_state": (c_int, [_P, POINTER(CacheState), _P]),
+    "card_cache_snapshot": (c_int, [_P, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "card_cache_device_ptrs": (c_int, [_P] + [POINTER(c_void_p)] * 7),
+}
+
+
+def lib():
+    """Load (once) and return the ctypes handle; raises DeviceError if absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    from .errors import DeviceError
+
+    if not os.path.exists(LIB_PATH):
+        raise DeviceError(
+            f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`"
+            " (no CPU fallback exists)")
+    handle = ctypes.CDLL(LIB_PATH, mode=ctypes.RTLD_GLOBAL)
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(handle, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = handle
+    return handle
+
+
+def exported_symbols() -> list[str]:
+    return list(SIGNATURES)
