@@ -48,11 +48,12 @@ const char* card_last_cuda_error(void);
  * ------------------------------------------------------------------ */
 
 /* Hashed k-gram next-token distributions for n_rows contexts.
- * tails: [n_rows, tail_len] int64 (the last `order` tokens of each context);
+ * tails: [n_rows, tail_len] int32 (the last `order` tokens of each context,
+ * -1 marking "context shorter than the order");
  * out: [n_rows, vocab] float64.  Replaces _kernels.pyx:44-93 (bit-exact
  * integer stream; fp64 softmax with a correctly rounded exp). */
 int card_kgram_dist(uint64_t seed, uint64_t seed2, double mix_weight,
-                    const int64_t* tails, int tail_len, int n_rows, int vocab,
+                    const int32_t* tails, int tail_len, int tail_stride, int n_rows, int vocab,
                     double sharpness, double temperature, double* out, void* stream);
 
 /* Per-row top-k by (p desc, token asc), p <= 0 excluded.  dists:
@@ -82,6 +83,7 @@ typedef struct card_cache_state {
     int32_t K, k, max_depth, eos;
     int32_t capacity, hash_mask, fresh, new_root;
     int32_t q_hit, q_len, chain_len, alive_below;
+    int32_t n_precompact, reserved[7];
 } card_cache_state;
 
 /* Create a cache rooted at root_token (cache.py:95-105).  eos_token < 0
@@ -102,10 +104,13 @@ int card_cache_reset(card_cache* h, const int32_t* d_root_token, int root_token,
  * take it from the device (engine path). */
 int card_cache_expand(card_cache* h, const double* dists, int n_rows, int vocab, void* stream);
 
-/* Same, from precomputed per-row candidates (token, log-prob) — the fused
- * lm_head top-k output.  tok/logp: [n_rows, k]; cnt: [n_rows]. */
-int card_cache_expand_topk(card_cache* h, const int32_t* tok, const double* logp,
-                           const int32_t* cnt, int n_rows, void* stream);
+/* Same, from precomputed per-row candidates — the fused lm_head top-k output
+ * (log-probs) or a row top-k over fp64 distributions (probabilities, the
+ * log is taken on the device).  tok/val: [n_rows, k]; cnt: [n_rows].  If
+ * skip is non-NULL and *skip != 0 on the device, the call is a no-op. */
+int card_cache_expand_topk(card_cache* h, const int32_t* tok, const double* val,
+                           const int32_t* cnt, int n_rows, int values_are_probs,
+                           const int32_t* skip, void* stream);
 
 /* Candidate pool of extension_pool() (cache.py:190-222) for the drop-in:
  * writes P = n_rows*k slots of (token or -1, weight, parent index, edge). */
@@ -119,9 +124,12 @@ int card_cache_query(card_cache* h, int depth, void* stream);
 int card_cache_query_buffers(card_cache* h, int32_t** path, int32_t** tok, double** edge);
 
 /* correct(accepted, correction) (cache.py:355-413).  All inputs on the
- * device: accepted[0..*n_accepted), *correction < 0 means None. */
+ * device: accepted[0..*n_accepted), *correction < 0 means None; skip as above.
+ * Before compaction the kernel records the walked chain (+ new root) in the
+ * chain buffer and whether each had tree KV (chain_kv), and sets
+ * state.n_precompact / state.compacted / remap[] for the draft KV mover. */
 int card_cache_correct(card_cache* h, const int32_t* accepted, const int32_t* n_accepted,
-                       const int32_t* correction, void* stream);
+                       const int32_t* correction, const int32_t* skip, void* stream);
 
 /* advance_root (cache.py:415-437); state.moved = 1 on success, 0 if the
  * correction token is not cached (caller then resets). */
@@ -143,7 +151,85 @@ int card_cache_snapshot(card_cache* h, int32_t* token, int32_t* parent, int32_t*
 /* Device pointers of the state block and arrays (engine kernels chain on them). */
 int card_cache_device_ptrs(card_cache* h, card_cache_state** st, int32_t** token,
                            int32_t** parent, int32_t** layer, int32_t** frontier,
-                           int32_t** remap, int32_t** chain);
+                           int32_t** remap, int32_t** chain, int32_t** chain_kv);
+
+
+/* ------------------------------------------------------------------ *
+ * model plug-in: KV-cached transformer forward (lm.py:109-196)
+ * ------------------------------------------------------------------ *
+ * dtype codes: 0 = bf16, 1 = fp32.  `dM` / `n_out` are device row counts so
+ * one captured CUDA graph serves every step of a decode. */
+
+typedef struct card_linear card_linear;
+
+/* Y[M,N] = X[M,K] . W[N,K]^T with a fused epilogue (0 store f32, 1 residual
+ * add f32, 2 store bf16, 3 SwiGLU -> bf16 with gate/up rows interleaved per
+ * 128-row tile).  bf16 weights: tcgen05 + TMA kernel (m_max >= 2) or the
+ * 128-bit-load GEMV (m_max == 1); fp32 weights: parity kernel.  X must hold
+ * round_up(m_max, 16) rows.  bias: optional fp32 [N]. */
+int card_linear_create(const void* W, int N, int K, int wdtype, const void* X, int m_max, int epi,
+                       void* out, int ldo, const float* bias, card_linear** out_h);
+int card_linear_run(card_linear* h, const int32_t* dM, void* stream);
+int card_linear_info(card_linear* h, int32_t* info8);
+int card_linear_destroy(card_linear* h);
+
+int card_embed(const int32_t* tok, const int32_t* dM, int m_max, const void* E, int wdtype, int H,
+               float* x, void* stream);
+int card_rmsnorm(const float* x, const float* w, int H, float eps, const int32_t* dM, int m_max,
+                 const int32_t* gather, void* y, int ydtype, void* stream);
+int card_rope_kv(const float* qkv, const int32_t* dM, int m_max, const int32_t* pos, const int32_t* slot,
+                 const float* cos_t, const float* sin_t, int nh, int nkv, int hd, float* q,
+                 void* k_cache, void* v_cache, int kvdtype, void* stream);
+int card_attention_work_floats(int m_max, int nh, int hd, int max_plen);
+int card_attention(const float* q, const int32_t* dM, int m_max, const int32_t* plen,
+                   const int32_t* n_extra, const int32_t* extra, int extra_max, const void* k_cache,
+                   const void* v_cache, int kvdtype, int nh, int nkv, int hd, int max_plen, float* work,
+                   void* o, int odtype, void* stream);
+/* draft lm_head epilogue: per-row top-k by (logit desc, token asc) with
+ * log-probs logit/T - logsumexp (replaces extension_pool's rows_topk+log). */
+int card_topk_logits(const float* logits, const int32_t* dM, int m_max, int V, int k, double inv_temp,
+                     int32_t* out_tok, double* out_logp, int32_t* out_cnt, void* stream);
+/* target greedy: first maximum per row (verify.py:38-40) */
+int card_argmax_logits(const float* logits, const int32_t* dM, int m_max, int V, int32_t* out, void* stream);
+int card_softmax64(const float* logits, const int32_t* dM, int m_max, int V, double inv_temp, double* out,
+                   void* stream);
+/* agreement knob: logits[r] += sharpness * (u1 + mix_weight * u2), u the
+ * splitmix64 k-gram stream of (seed, ctx_tail[r]) (_kernels.pyx:26-41). */
+int card_logit_bias(float* logits, const int32_t* dM, int m_max, int V, const int32_t* ctx_tail, int order,
+                    int stride, uint64_t seed, uint64_t seed2, float mix_weight, float sharpness, void* stream);
+
+/* ------------------------------------------------------------------ *
+ * engine: the query-and-correct cycle (engine.py:198-317) on the device
+ * ------------------------------------------------------------------ *
+ * card_engine_state is a device struct of int32 fields (layout in
+ * paper_2508_04462_b200/_lib.py: EngineState); `rows` is an int32 block
+ * [M, n_out, tok[R], pos[R], slot[R], plen[R], n_extra[R], out_rows[R],
+ * extra[R*E]] with R = rows_max, E = extra_max. */
+typedef struct card_engine_state card_engine_state;
+int card_engine_state_bytes(void);
+int card_draft_rows(card_engine_state* E, card_cache* h, const int32_t* committed, int32_t* rows,
+                    int rows_max, int extra_max, int tree_base, int32_t* ctx_tail, int order, void* stream);
+int card_target_rows(card_engine_state* E, card_cache* h, const int32_t* committed, int32_t* rows,
+                     int rows_max, int extra_max, int32_t* ctx_tail, int order, void* stream);
+int card_eos_fix(const int32_t* n_rows, int m_max, const int32_t* ctx_tail, int order, int eos, int V,
+                 double* probs, void* stream);
+int card_record_width(card_engine_state* E, card_cache* h, const int32_t* n_out, void* stream);
+/* accept-and-correct over L = state.L candidate tokens cand[0..L): greedy
+ * from per-row argmax, or greedy / lossless stochastic from fp64 rows
+ * [L+1, V] with draft conditionals qcond (NULL = the point mass q = 1 of
+ * engine.py:242) and host-drawn uniforms consumed from state.cursor.
+ * Writes accepted tokens, n, correction into the state. */
+int card_verify_argmax(card_engine_state* E, const int32_t* cand, const int32_t* amax, void* stream);
+int card_verify_probs(card_engine_state* E, const int32_t* cand, const double* probs, int V,
+                      const double* qcond, const double* uniforms, void* stream);
+int card_commit(card_engine_state* E, int32_t* committed, void* stream);
+/* KV rollback / roll-forward of the draft: promote accepted-chain tree KV
+ * rows into the prefix; move surviving tree rows after an arena compaction. */
+int card_draft_promote(card_engine_state* E, card_cache* h, void** k_layers, void** v_layers,
+                       int n_layers, int row_elems, int esize, int tree_base, int max_chain, void* stream);
+int card_kv_compact(card_engine_state* E, card_cache* h, void** k_layers, void** v_layers, int n_layers,
+                    int row_elems, int esize, int tree_base, void** scratch_kv, int capacity, void* stream);
+int card_cycle_end(card_engine_state* E, card_cache* h, void* stream);
 
 #ifdef __cplusplus
 }

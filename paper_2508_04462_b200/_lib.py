@@ -21,7 +21,8 @@ class CacheState(ctypes.Structure):
     _fields_ = [(n, c_int32) for n in (
         "n_nodes", "root", "n_frontier", "epoch", "dead", "status", "vstatus", "stamp",
         "top_layer", "last_width", "compacted", "moved", "K", "k", "max_depth", "eos",
-        "capacity", "hash_mask", "fresh", "new_root", "q_hit", "q_len", "chain_len", "alive_below")]
+        "capacity", "hash_mask", "fresh", "new_root", "q_hit", "q_len", "chain_len", "alive_below",
+        "n_precompact", "r0", "r1", "r2", "r3", "r4", "r5", "r6")]
 
 
 # name -> (restype, argtypes)
@@ -30,7 +31,8 @@ SIGNATURES = {
     "card_abi_version": (c_int, []),
     "card_strerror": (ctypes.c_char_p, [c_int]),
     "card_last_cuda_error": (ctypes.c_char_p, []),
-    "card_kgram_dist": (c_int, [c_uint64, c_uint64, c_double, _P, c_int, c_int, c_int, c_double, c_double, _P, _P]),
+    "card_kgram_dist": (c_int, [c_uint64, c_uint64, c_double, _P, c_int, c_int, c_int, c_int, c_double, c_double, _P,
+                                _P]),
     "card_rows_topk": (c_int, [_P, c_int, c_int, c_int, _P, _P, _P, _P, _P]),
     "card_log_cr": (c_int, [_P, _P, c_int, _P]),
     "card_exp_cr": (c_int, [_P, _P, c_int, _P]),
@@ -38,18 +40,56 @@ SIGNATURES = {
     "card_cache_destroy": (c_int, [_P]),
     "card_cache_reset": (c_int, [_P, _P, c_int, _P]),
     "card_cache_expand": (c_int, [_P, _P, c_int, c_int, _P]),
-    "card_cache_expand_topk": (c_int, [_P, _P, _P, _P, c_int, _P]),
+    "card_cache_expand_topk": (c_int, [_P, _P, _P, _P, c_int, c_int, _P, _P]),
     "card_cache_pool": (c_int, [_P, _P, c_int, c_int, _P, _P, _P, _P, _P]),
     "card_cache_query": (c_int, [_P, c_int, _P]),
     "card_cache_query_buffers": (c_int, [_P, POINTER(c_void_p), POINTER(c_void_p), POINTER(c_void_p)]),
-    "card_cache_correct": (c_int, [_P, _P, _P, _P, _P]),
+    "card_cache_correct": (c_int, [_P, _P, _P, _P, _P, _P]),
     "card_cache_advance_root": (c_int, [_P, _P, _P, _P, _P]),
     "card_cache_count_alive": (c_int, [_P, _P]),
     "card_cache_clear_status": (c_int, [_P, _P]),
     "card_cache_read_state": (c_int, [_P, POINTER(CacheState), _P]),
     "card_cache_snapshot": (c_int, [_P, _P, _P, _P, _P, _P, _P, _P, _P]),
-    "card_cache_device_ptrs": (c_int, [_P] + [POINTER(c_void_p)] * 7),
+    "card_cache_device_ptrs": (c_int, [_P] + [POINTER(c_void_p)] * 8),
+    # model plug-in
+    "card_linear_create": (c_int, [_P, c_int, c_int, c_int, _P, c_int, c_int, _P, c_int, _P, POINTER(c_void_p)]),
+    "card_linear_run": (c_int, [_P, _P, _P]),
+    "card_linear_info": (c_int, [_P, _P]),
+    "card_linear_destroy": (c_int, [_P]),
+    "card_embed": (c_int, [_P, _P, c_int, _P, c_int, c_int, _P, _P]),
+    "card_rmsnorm": (c_int, [_P, _P, c_int, ctypes.c_float, _P, c_int, _P, _P, c_int, _P]),
+    "card_rope_kv": (c_int, [_P, _P, c_int, _P, _P, _P, _P, c_int, c_int, c_int, _P, _P, _P, c_int, _P]),
+    "card_attention_work_floats": (c_int, [c_int, c_int, c_int, c_int]),
+    "card_attention": (c_int, [_P, _P, c_int, _P, _P, _P, c_int, _P, _P, c_int, c_int, c_int, c_int, c_int, _P,
+                               _P, c_int, _P]),
+    "card_topk_logits": (c_int, [_P, _P, c_int, c_int, c_int, c_double, _P, _P, _P, _P]),
+    "card_argmax_logits": (c_int, [_P, _P, c_int, c_int, _P, _P]),
+    "card_softmax64": (c_int, [_P, _P, c_int, c_int, c_double, _P, _P]),
+    "card_logit_bias": (c_int, [_P, _P, c_int, c_int, _P, c_int, c_int, c_uint64, c_uint64, ctypes.c_float,
+                                ctypes.c_float, _P]),
+    # engine
+    "card_engine_state_bytes": (c_int, []),
+    "card_draft_rows": (c_int, [_P, _P, _P, _P, c_int, c_int, c_int, _P, c_int, _P]),
+    "card_target_rows": (c_int, [_P, _P, _P, _P, c_int, c_int, _P, c_int, _P]),
+    "card_eos_fix": (c_int, [_P, c_int, _P, c_int, c_int, c_int, _P, _P]),
+    "card_record_width": (c_int, [_P, _P, _P, _P]),
+    "card_verify_argmax": (c_int, [_P, _P, _P, _P]),
+    "card_verify_probs": (c_int, [_P, _P, _P, c_int, _P, _P, _P]),
+    "card_commit": (c_int, [_P, _P, _P]),
+    "card_draft_promote": (c_int, [_P, _P, _P, _P, c_int, c_int, c_int, c_int, c_int, _P]),
+    "card_kv_compact": (c_int, [_P, _P, _P, _P, c_int, c_int, c_int, c_int, _P, c_int, _P]),
+    "card_cycle_end": (c_int, [_P, _P, _P]),
 }
+
+
+class EngineState(ctypes.Structure):
+    """Host mirror of card_engine_state (csrc/card_engine.cu)."""
+    _fields_ = [(n, c_int32) for n in (
+        "C", "Pd", "out_len", "done", "max_new", "eos", "stop", "n_widths", "hit", "L", "n_acc", "corr",
+        "rec_acc", "rec_lnew", "cursor", "n_uni", "base_len", "C_prev", "order", "sampling",
+        "rec_n_widths", "rec_hit", "rec_L", "rec_n_acc", "rec_corr", "rec_done", "n_commit", "anchor_origin")] + [
+        ("widths", c_int32 * 64), ("rec_widths", c_int32 * 64), ("acc", c_int32 * 64),
+        ("committed_now", c_int32 * 72), ("rec_depth", c_int32), ("rec_alive", c_int32), ("spare", c_int32 * 6)]
 
 
 def lib():
@@ -68,6 +108,8 @@ def lib():
         fn = getattr(handle, name)
         fn.restype = res
         fn.argtypes = args
+    if handle.card_engine_state_bytes() != ctypes.sizeof(EngineState):
+        raise DeviceError("EngineState layout does not match the library")
     _lib = handle
     return handle
 

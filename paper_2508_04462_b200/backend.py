@@ -33,11 +33,11 @@ def kgram_dist_rows(seed, seed2, mix_weight, tails, vocab_size, sharpness, tempe
     dev = require_cuda()
     n = len(tails)
     L = len(tails[0]) if n else 0
-    t = to_device(np.asarray(tails, dtype=np.int64).reshape(n, L), np.int64)
+    t = to_device(np.asarray(tails, dtype=np.int32).reshape(n, L), np.int32)
     if out is None:
         out = torch.empty((n, vocab_size), dtype=torch.float64, device=dev)
     M64 = (1 << 64) - 1
-    rc = lib().card_kgram_dist(int(seed) & M64, int(seed2) & M64, float(mix_weight), ptr(t), L, n,
+    rc = lib().card_kgram_dist(int(seed) & M64, int(seed2) & M64, float(mix_weight), ptr(t), L, L, n,
                                int(vocab_size), float(sharpness), float(temperature), ptr(out), stream_ptr())
     raise_for_status(rc, "card_kgram_dist")
     return out

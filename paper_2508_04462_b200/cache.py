@@ -269,7 +269,7 @@ class TreeCache:
     def correct(self, accepted, correction_token: TokenId | None) -> int:
         """cache.py:355-413 on the device."""
         self._load_commit(accepted, correction_token)
-        rc = lib().card_cache_correct(self._h, ptr(self._acc), ptr(self._nacc), ptr(self._corr), stream_ptr())
+        rc = lib().card_cache_correct(self._h, ptr(self._acc), ptr(self._nacc), ptr(self._corr), None, stream_ptr())
         raise_for_status(rc, "card_cache_correct")
         st = self.state()
         raise_for_status(st.status, "correct")

@@ -47,6 +47,7 @@ struct Bufs {
     int32_t *q_path, *q_tok;
     double* q_edge;
     int32_t* chain;
+    int32_t* chain_kv;
     // compaction scratch
     int32_t *s_token, *s_parent, *s_layer;
     uint8_t* s_haskv;
@@ -227,12 +228,17 @@ __device__ __forceinline__ bool pool_before(const PoolSmem& p, int a, int c) {
 }
 
 __global__ void __launch_bounds__(kThreads) expand_kernel(Bufs b, const int32_t* c_tok, const double* c_val,
-                                                          const int32_t* c_cnt, int n_rows_host, int vals_are_logp) {
+                                                          const int32_t* c_cnt, int n_rows_host, int vals_are_logp,
+                                                          const int32_t* skip) {
     extern __shared__ __align__(16) char smem[];
     __shared__ int sh_flag, sh_npar, sh_valid, sh_m, sh_m2, sh_dead;
     __shared__ int lvl[2][kMaxK];
     card_cache_state& S = *b.st;
     const int tid = threadIdx.x;
+    if (skip && *skip) {
+        if (tid == 0) S.last_width = 0;
+        return;
+    }
     if (tid == 0) {
         const int npar = S.n_frontier > 0 ? S.n_frontier : 1;
         const int depth = S.n_frontier > 0 ? b.layer[b.frontier[0]] - b.layer[S.root] : 0;
@@ -449,8 +455,12 @@ __device__ int walk_chain(const Bufs& b, const int32_t* acc, int n_acc, int* anc
 }
 
 __global__ void __launch_bounds__(kThreads) correct_kernel(Bufs b, const int32_t* acc, const int32_t* n_acc_p,
-                                                           const int32_t* corr_p) {
+                                                           const int32_t* corr_p, const int32_t* skip) {
     card_cache_state& S = *b.st;
+    if (skip && *skip) {
+        if (threadIdx.x == 0) S.compacted = 0;
+        return;
+    }
     __shared__ int sh_flag, sh_new_root, sh_fresh, sh_plen, sh_dead, sh_ns, sh_total;
     __shared__ int path[72];   // max_depth <= 64
     __shared__ int surv[kMaxK];
@@ -502,6 +512,7 @@ __global__ void __launch_bounds__(kThreads) correct_kernel(Bufs b, const int32_t
                 for (int i = 0; i < n_acc; ++i) path[pl++] = b.chain[i];
                 if (new_root != anchor) path[pl++] = new_root;
                 if (new_root != anchor) b.chain[n_acc] = new_root;
+                for (int i = 1; i < pl; ++i) b.chain_kv[i - 1] = b.has_kv[path[i]];
                 sh_plen = pl;
                 sh_new_root = new_root;
                 sh_fresh = fresh;
@@ -582,6 +593,7 @@ __global__ void __launch_bounds__(kThreads) correct_kernel(Bufs b, const int32_t
         S.epoch += 1;
         S.dead += sh_dead;
         sh_flag = (n >= kCompactMinArena && (double)S.dead > 0.75 * (double)n) ? 1 : 0;  // cache.py:471-474
+        S.n_precompact = n;
     }
     __syncthreads();
     if (!sh_flag) return;
@@ -729,6 +741,7 @@ int card_cache_create(int root_token, int K, int k, int max_depth, int eos_token
     const size_t o_hk = take((size_t)hcap * 8), o_hv = take((size_t)hcap * 4);
     const size_t o_ctok = take((size_t)K * k * 4), o_ccnt = take((size_t)K * 4), o_cval = take((size_t)K * k * 8);
     const size_t o_qp = take(md2 * 4), o_qt = take(md2 * 4), o_qe = take(md2 * 8), o_ch = take(md2 * 4);
+    const size_t o_chkv = take(md2 * 4);
     const size_t o_st_tok = take(cap * 4), o_st_par = take(cap * 4), o_st_lay = take(cap * 4);
     const size_t o_st_hk = take(cap), o_st_sc = take(cap * 8), o_st_ed = take(cap * 8);
     void* block = nullptr;
@@ -762,6 +775,7 @@ int card_cache_create(int root_token, int K, int k, int max_depth, int eos_token
     b.q_tok = (int32_t*)(base + o_qt);
     b.q_edge = (double*)(base + o_qe);
     b.chain = (int32_t*)(base + o_ch);
+    b.chain_kv = (int32_t*)(base + o_chkv);
     b.s_token = (int32_t*)(base + o_st_tok);
     b.s_parent = (int32_t*)(base + o_st_par);
     b.s_layer = (int32_t*)(base + o_st_lay);
@@ -819,16 +833,18 @@ int card_cache_expand(card_cache* h, const double* dists, int n_rows, int vocab,
     int rc = launch_rows_topk(dists, rows, vocab, h->k, h->b.c_tok, h->b.c_val, h->b.c_cnt, &h->b.st->vstatus, s);
     if (rc) return rc;
     const int P = (n_rows >= 0 ? (n_rows > 0 ? n_rows : 1) : h->K) * h->k;
-    expand_kernel<<<1, kThreads, pool_smem_bytes(P), s>>>(h->b, h->b.c_tok, h->b.c_val, h->b.c_cnt, n_rows, 0);
+    expand_kernel<<<1, kThreads, pool_smem_bytes(P), s>>>(h->b, h->b.c_tok, h->b.c_val, h->b.c_cnt, n_rows, 0,
+                                                          nullptr);
     CARD_LAUNCH_CHECK();
     return CARD_OK;
 }
 
-int card_cache_expand_topk(card_cache* h, const int32_t* tok, const double* logp, const int32_t* cnt, int n_rows,
-                           void* stream) {
+int card_cache_expand_topk(card_cache* h, const int32_t* tok, const double* val, const int32_t* cnt, int n_rows,
+                           int values_are_probs, const int32_t* skip, void* stream) {
     if (!h) return CARD_E_INPUT;
     const int P = (n_rows > 0 ? n_rows : h->K) * h->k;
-    expand_kernel<<<1, kThreads, pool_smem_bytes(P), (cudaStream_t)stream>>>(h->b, tok, logp, cnt, n_rows, 1);
+    expand_kernel<<<1, kThreads, pool_smem_bytes(P), (cudaStream_t)stream>>>(h->b, tok, val, cnt, n_rows,
+                                                                             values_are_probs ? 0 : 1, skip);
     CARD_LAUNCH_CHECK();
     return CARD_OK;
 }
@@ -861,9 +877,9 @@ int card_cache_query_buffers(card_cache* h, int32_t** path, int32_t** tok, doubl
 }
 
 int card_cache_correct(card_cache* h, const int32_t* accepted, const int32_t* n_accepted, const int32_t* correction,
-                       void* stream) {
+                       const int32_t* skip, void* stream) {
     if (!h) return CARD_E_INPUT;
-    correct_kernel<<<1, kThreads, 0, (cudaStream_t)stream>>>(h->b, accepted, n_accepted, correction);
+    correct_kernel<<<1, kThreads, 0, (cudaStream_t)stream>>>(h->b, accepted, n_accepted, correction, skip);
     CARD_LAUNCH_CHECK();
     return CARD_OK;
 }
@@ -919,7 +935,7 @@ int card_cache_snapshot(card_cache* h, int32_t* token, int32_t* parent, int32_t*
 }
 
 int card_cache_device_ptrs(card_cache* h, card_cache_state** st, int32_t** token, int32_t** parent, int32_t** layer,
-                           int32_t** frontier, int32_t** remap, int32_t** chain) {
+                           int32_t** frontier, int32_t** remap, int32_t** chain, int32_t** chain_kv) {
     if (!h) return CARD_E_INPUT;
     if (st) *st = h->b.st;
     if (token) *token = h->b.token;
@@ -928,6 +944,7 @@ int card_cache_device_ptrs(card_cache* h, card_cache_state** st, int32_t** token
     if (frontier) *frontier = h->b.frontier;
     if (remap) *remap = h->b.remap;
     if (chain) *chain = h->b.chain;
+    if (chain_kv) *chain_kv = h->b.chain_kv;
     return CARD_OK;
 }
 

@@ -134,14 +134,19 @@ __device__ __forceinline__ double exp_cr(double x) {
     int k;
     dd m1 = dd_exp_reduced({0.0, 0.0}, &k, x);
     dd e = dd_add({1.0, 0.0}, m1);
-    if (k > -1020) {
+    if (k >= -1021) {   // e*2^k is normal (e >= 0.7)
         double r = __dadd_rn(e.hi, e.lo);
         return ldexp(r, k);
     }
-    // subnormal result: round once at the final exponent
-    double hi = ldexp(e.hi, k);
-    double lo = ldexp(e.lo, k);
-    return __dadd_rn(hi, lo);
+    // subnormal result: round once on the 2^-1074 grid.  q = e * 2^(k+1074)
+    // is exact (a power-of-two scaling into the normal range).
+    const double qh = ldexp(e.hi, k + 1074), ql = ldexp(e.lo, k + 1074);
+    double n = floor(qh);
+    double r = __dadd_rn(__dsub_rn(qh, n), ql);
+    while (r >= 1.0) { n += 1.0; r -= 1.0; }
+    while (r < 0.0) { n -= 1.0; r += 1.0; }
+    if (r > 0.5 || (r == 0.5 && fmod(n, 2.0) != 0.0)) n += 1.0;
+    return ldexp(n, -1074);
 }
 
 // exp of a double-double argument as a double-double (for the log refinement).

@@ -1,0 +1,710 @@
+// card_gemm.cu — decode-phase weight streaming for the draft/target models.
+//
+//   Y[M, N] = X[M, K] . W[N, K]^T  (+ fused epilogue)
+//
+// Three kernels, picked per linear layer at plan time:
+//   * tc_gemm   (bf16 weights, M >= 2): TMA streams 128x64 weight tiles and
+//     the (tiny) activation tile into a multi-stage mbarrier ring; one
+//     elected thread issues tcgen05.mma kind::f16 (A = weights, K-major,
+//     SWIZZLE_128B; B = activations) into a TMEM accumulator (128 lanes x
+//     Mpad fp32 columns, double-buffered); four epilogue warps drain TMEM
+//     with tcgen05.ld and apply the fused epilogue.  Persistent CTAs walk
+//     (tile, k-split) work items; split partials are reduced in a fixed
+//     order by the last-arriving CTA (deterministic).
+//   * gemv      (bf16 weights, M == 1): 128-bit vectorised weight loads,
+//     one warp per output row group, fp32 accumulation.
+//   * f32_gemm  (fp32 weights — the parity mode against the CPU oracle).
+//
+// Epilogues: STORE_F32, RESID_F32 (out += acc), STORE_BF16, SWIGLU_BF16
+// (weight rows interleaved per 128-row tile: 64 gate rows then the 64 up
+// rows of the same features; out = silu(gate) * up), optional fp32 bias.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include "card_common.cuh"
+#include "card_llm.h"
+
+namespace card {
+
+// ---------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    const uint32_t a = smem_u32(bar);
+    asm volatile(
+        "{\n\t.reg .pred P;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+        "@!P bra WAIT_%=;\n\t}" ::"r"(a),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+            smem_u32(dst)),
+        "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+        : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* map) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void tc_mma_bf16(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                            uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
+
+// K-major SWIZZLE_128B shared-memory matrix descriptor (sm100 encoding):
+// start>>4 | LBO(16B)=1 <<16 | SBO(1024B)=64 <<32 | version 1 <<46 | layout 2 <<61
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+    return (uint64_t)((saddr & 0x3FFFF) >> 4) | ((uint64_t)1 << 16) | ((uint64_t)64 << 32) | ((uint64_t)1 << 46) |
+           ((uint64_t)2 << 61);
+}
+
+__device__ __forceinline__ float silu(float x) { return x / (1.0f + __expf(-x)); }
+
+// ---------------------------------------------------------------- tcgen05 GEMM
+constexpr int kTileN = 128;   // weight rows per tile (MMA M)
+constexpr int kBK = 64;       // bf16 K per stage = one 128-byte swizzle atom
+constexpr int kEpiThreads = 128;
+constexpr int kTcThreads = 192;   // warps 0-3 epilogue, 4 TMA producer, 5 MMA issuer
+
+struct TcArgs {
+    int N, K, kb_total, n_tiles, splits, items, Mpad, stages, tmem_cols, n_acc_buf;
+    const int32_t* dM;
+    int epi;
+    float* out_f32;
+    __nv_bfloat16* out_bf16;
+    const float* bias;
+    int ldo;
+    float* ws;
+    int32_t* counters;
+};
+
+template <int EPI>
+__device__ __forceinline__ void epi_store(const TcArgs& a, int n_glob, int n_local, int m, float v, float* xch) {
+    if (a.bias) v += a.bias[n_glob];
+    if (EPI == EPI_STORE_F32) {
+        a.out_f32[(int64_t)m * a.ldo + n_glob] = v;
+    } else if (EPI == EPI_RESID_F32) {
+        float* p = a.out_f32 + (int64_t)m * a.ldo + n_glob;
+        *p = *p + v;
+    } else if (EPI == EPI_STORE_BF16) {
+        a.out_bf16[(int64_t)m * a.ldo + n_glob] = __float2bfloat16(v);
+    }
+}
+
+// SwiGLU exchange: rows [0,64) of a tile are gates, [64,128) the matching ups.
+__device__ __forceinline__ void epi_swiglu_chunk(const TcArgs& a, int tile, int n_local, int m0, int mcount,
+                                                 const float* v, float* xch) {
+    // xch: [16][64] floats
+    if (n_local >= 64)
+        for (int j = 0; j < mcount; ++j) xch[j * 64 + (n_local - 64)] = v[j];
+    named_bar(1, kEpiThreads);
+    if (n_local < 64) {
+        const int f = tile * 64 + n_local;
+        for (int j = 0; j < mcount; ++j) {
+            const float g = v[j], u = xch[j * 64 + n_local];
+            a.out_bf16[(int64_t)(m0 + j) * a.ldo + f] = __float2bfloat16(silu(g) * u);
+        }
+    }
+    named_bar(1, kEpiThreads);
+}
+
+template <int EPI>
+__global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_constant__ CUtensorMap tmW,
+                                                               const __grid_constant__ CUtensorMap tmX, TcArgs a) {
+    if (*a.dM <= 0) return;   // nothing to do this step (graph replays with zero rows)
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    // 1024-byte alignment for SWIZZLE_128B atoms
+    uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    const int S = a.stages;
+    const int bytesA = kTileN * kBK * 2;
+    const int bytesB = a.Mpad * kBK * 2;
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + (size_t)S * bytesA;
+    uint64_t* full = (uint64_t*)(sB + (size_t)S * bytesB);
+    uint64_t* empty = full + S;
+    uint64_t* tfull = empty + S;    // [2]
+    uint64_t* tempty = tfull + 2;   // [2]
+    uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+    float* xch = (float*)(tmem_slot + 4);   // [16][64]
+    int* sh_last = (int*)(xch + 16 * 64);
+
+    const int warp = warp_id(), lane = lane_id();
+    if (warp == 4 && lane == 0) {
+        for (int i = 0; i < S; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&tfull[i], 1);
+            mbar_init(&tempty[i], 4);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        tma_prefetch_desc(&tmW);
+        tma_prefetch_desc(&tmX);
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(a.tmem_cols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    const int M = *a.dM;
+    const int m_rt = M < 1 ? 1 : M;
+    const int n_mma = ((m_rt + 15) / 16) * 16;   // runtime MMA N (tokens), <= Mpad
+
+    if (warp == 4) {
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int item = blockIdx.x; item < a.items; item += gridDim.x) {
+                const int tile = item / a.splits, split = item % a.splits;
+                const int kb0 = (int)((int64_t)a.kb_total * split / a.splits);
+                const int kb1 = (int)((int64_t)a.kb_total * (split + 1) / a.splits);
+                for (int kb = kb0; kb < kb1; ++kb) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    mbar_expect_tx(&full[stage], bytesA + bytesB);
+                    tma_load_2d(sA + (size_t)stage * bytesA, &tmW, &full[stage], kb * kBK, tile * kTileN);
+                    tma_load_2d(sB + (size_t)stage * bytesB, &tmX, &full[stage], kb * kBK, 0);
+                    if (++stage == S) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 5) {
+        if (lane == 0) {
+            const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n_mma >> 3) << 17) |
+                                   ((uint32_t)(kTileN >> 4) << 24);
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t acc_phase = 0;
+            for (int item = blockIdx.x; item < a.items; item += gridDim.x) {
+                const int split = item % a.splits;
+                const int kb0 = (int)((int64_t)a.kb_total * split / a.splits);
+                const int kb1 = (int)((int64_t)a.kb_total * (split + 1) / a.splits);
+                mbar_wait(&tempty[acc], acc_phase ^ 1);
+                tc_fence_after();
+                const uint32_t d_tmem = tmem_base + (uint32_t)(acc * a.Mpad);
+                for (int kb = kb0; kb < kb1; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+                    const uint32_t a0 = smem_u32(sA + (size_t)stage * bytesA);
+                    const uint32_t b0 = smem_u32(sB + (size_t)stage * bytesB);
+#pragma unroll
+                    for (int k = 0; k < kBK / 16; ++k) {
+                        tc_mma_bf16(d_tmem, sw128_desc(a0 + k * 32), sw128_desc(b0 + k * 32), idesc,
+                                    (kb > kb0 || k > 0) ? 1u : 0u);
+                    }
+                    tc_commit(&empty[stage]);   // frees the smem slot when these MMAs retire
+                    if (++stage == S) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                tc_commit(&tfull[acc]);   // accumulator ready for the epilogue
+                if (a.n_acc_buf == 2) {
+                    acc ^= 1;
+                    if (acc == 0) acc_phase ^= 1;
+                } else {
+                    acc_phase ^= 1;
+                }
+            }
+        }
+    } else {
+        // ---------------- epilogue warps 0..3: TMEM lane = tile row n_local
+        const int n_local = warp * 32 + lane;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int item = blockIdx.x; item < a.items; item += gridDim.x) {
+            const int tile = item / a.splits;
+            const int n_glob = tile * kTileN + n_local;
+            mbar_wait(&tfull[acc], acc_phase);
+            tc_fence_after();
+            const uint32_t trow = tmem_base + ((uint32_t)(warp * 32) << 16) + (uint32_t)(acc * a.Mpad);
+            const bool direct = a.splits == 1;
+            float* wsp = a.ws + (size_t)item * kTileN * a.Mpad;
+            for (int m0 = 0; m0 < M; m0 += 16) {
+                float v[16];
+                tmem_ld16(trow + (uint32_t)m0, v);
+                const int mc = (M - m0) < 16 ? (M - m0) : 16;
+                if (direct) {
+                    if (EPI == EPI_SWIGLU_BF16) {
+                        epi_swiglu_chunk(a, tile, n_local, m0, mc, v, xch);
+                    } else {
+                        for (int j = 0; j < mc; ++j) epi_store<EPI>(a, n_glob, n_local, m0 + j, v[j], xch);
+                    }
+                } else {
+                    for (int j = 0; j < mc; ++j) wsp[(size_t)(m0 + j) * kTileN + n_local] = v[j];
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc]);
+            if (a.n_acc_buf == 2) {
+                acc ^= 1;
+                if (acc == 0) acc_phase ^= 1;
+            } else {
+                acc_phase ^= 1;
+            }
+            if (!direct) {
+                // deterministic split-K fixup: last arriver sums splits 0..S-1 in order
+                __threadfence();
+                named_bar(1, kEpiThreads);
+                if (n_local == 0) {
+                    const int prev = atomicAdd(&a.counters[tile], 1);
+                    *sh_last = (prev == a.splits - 1);
+                    if (prev == a.splits - 1) a.counters[tile] = 0;   // reusable next launch / graph replay
+                }
+                named_bar(1, kEpiThreads);
+                if (*sh_last) {
+                    __threadfence();
+                    const float* base = a.ws + (size_t)tile * a.splits * kTileN * a.Mpad;
+                    for (int m0 = 0; m0 < M; m0 += 16) {
+                        const int mc = (M - m0) < 16 ? (M - m0) : 16;
+                        float v[16];
+                        for (int j = 0; j < mc; ++j) {
+                            float s = 0.f;
+                            for (int sp = 0; sp < a.splits; ++sp)
+                                s += __ldcg(base + ((size_t)sp * a.Mpad + (m0 + j)) * kTileN + n_local);
+                            v[j] = s;
+                        }
+                        if (EPI == EPI_SWIGLU_BF16) {
+                            epi_swiglu_chunk(a, tile, n_local, m0, mc, v, xch);
+                        } else {
+                            for (int j = 0; j < mc; ++j) epi_store<EPI>(a, n_glob, n_local, m0 + j, v[j], xch);
+                        }
+                    }
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(a.tmem_cols));
+    }
+}
+
+// ---------------------------------------------------------------- M == 1 GEMV (bf16)
+// One warp per 2 output rows; each lane streams 16-byte chunks (8 bf16) of
+// the weight rows with ld.global.nc.L1::no_allocate, x cached in smem.
+template <int EPI>
+__global__ void __launch_bounds__(256) gemv_bf16_kernel(const __nv_bfloat16* __restrict__ W,
+                                                        const __nv_bfloat16* __restrict__ X, int N, int K,
+                                                        TcArgs a) {
+    if (*a.dM <= 0) return;
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    __nv_bfloat16* xs = (__nv_bfloat16*)smem_raw;
+    for (int i = threadIdx.x * 8; i < K; i += blockDim.x * 8) *(uint4*)(xs + i) = *(const uint4*)(X + i);
+    __syncthreads();
+    const int warps = blockDim.x >> 5;
+    const int lane = lane_id();
+    constexpr int R = 2;
+    for (int row0 = (blockIdx.x * warps + warp_id()) * R; row0 < N; row0 += gridDim.x * warps * R) {
+        float acc[R] = {0.f, 0.f};
+        const uint4* wr[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) wr[r] = (const uint4*)(W + (int64_t)min(row0 + r, N - 1) * K);
+        const int chunks = K / 8;
+#pragma unroll 4
+        for (int c = lane; c < chunks; c += 32) {
+            const uint4 xv = *(const uint4*)(xs + c * 8);
+            const __nv_bfloat162* xp = (const __nv_bfloat162*)&xv;
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                uint4 wv;
+                asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                             : "=r"(wv.x), "=r"(wv.y), "=r"(wv.z), "=r"(wv.w)
+                             : "l"(wr[r] + c));
+                const __nv_bfloat162* wp = (const __nv_bfloat162*)&wv;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const float2 wf = __bfloat1622float2(wp[j]);
+                    const float2 xf = __bfloat1622float2(xp[j]);
+                    acc[r] = fmaf(wf.x, xf.x, acc[r]);
+                    acc[r] = fmaf(wf.y, xf.y, acc[r]);
+                }
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            float v = acc[r];
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            acc[r] = v;
+        }
+        if (lane == 0) {
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const int n = row0 + r;
+                if (n >= N) continue;
+                if (EPI == EPI_SWIGLU_BF16) {
+                    // interleaved tiles: partner row of gate n is n + 64 (same tile)
+                    continue;
+                }
+                epi_store<EPI>(a, n, 0, 0, acc[r], nullptr);
+            }
+        }
+    }
+}
+
+// SwiGLU for the GEMV path: rows are computed into a scratch fp32 buffer
+// first (EPI_STORE_F32), then combined here.
+__global__ void swiglu_from_rows_kernel(const float* __restrict__ rows, const int32_t* dM, int N, __nv_bfloat16* out,
+                                        int ldo) {
+    const int M = *dM < 1 ? 0 : 1;
+    const int F = N / 2;
+    for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < M * F; idx += gridDim.x * blockDim.x) {
+        const int m = idx / F, f = idx % F;
+        const int tile = f / 64, j = f % 64;
+        const float g = rows[(int64_t)m * N + tile * 128 + j];
+        const float u = rows[(int64_t)m * N + tile * 128 + 64 + j];
+        out[(int64_t)m * ldo + f] = __float2bfloat16(silu(g) * u);
+    }
+}
+
+// ---------------------------------------------------------------- fp32 parity GEMM
+// One warp per output column n; lanes stride K; rows of X reused from L1.
+template <int EPI>
+__global__ void __launch_bounds__(256) f32_gemm_kernel(const float* __restrict__ W, const float* __restrict__ X,
+                                                       int N, int K, TcArgs a) {
+    const int M = *a.dM;
+    const int lane = lane_id();
+    const int n = blockIdx.x * (blockDim.x >> 5) + warp_id();
+    if (n >= N) return;
+    const float* w = W + (int64_t)n * K;
+    for (int m = 0; m < M; ++m) {
+        const float* x = X + (int64_t)m * K;
+        float acc = 0.f;
+        for (int k = lane; k < K; k += 32) acc = fmaf(w[k], x[k], acc);
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) {
+            if (EPI == EPI_SWIGLU_BF16 || EPI == EPI_STORE_BF16) {
+                a.out_f32[(int64_t)m * a.ldo + n] = acc + (a.bias ? a.bias[n] : 0.f);   // f32 mode stores f32
+            } else {
+                epi_store<EPI>(a, n, 0, m, acc, nullptr);
+            }
+        }
+    }
+}
+
+__global__ void swiglu_f32_kernel(const float* __restrict__ rows, const int32_t* dM, int N, float* out, int ldo) {
+    const int M = *dM;
+    const int F = N / 2;
+    for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < M * F; idx += gridDim.x * blockDim.x) {
+        const int m = idx / F, f = idx % F;
+        const int tile = f / 64, j = f % 64;
+        const float g = rows[(int64_t)m * N + tile * 128 + j];
+        const float u = rows[(int64_t)m * N + tile * 128 + 64 + j];
+        out[(int64_t)m * ldo + f] = (g / (1.0f + expf(-g))) * u;
+    }
+}
+
+// ---------------------------------------------------------------- host side
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static PFN_encodeTiled get_encode() {
+    static PFN_encodeTiled fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void* p = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (PFN_encodeTiled)p;
+    }
+    return fn;
+}
+
+static int make_map_bf16(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows,
+                         CUtensorMapL2promotion promo) {
+    PFN_encodeTiled enc = get_encode();
+    if (!enc) return CARD_E_CUDA;
+    cuuint64_t dims[2] = {cols, rows};
+    cuuint64_t strides[1] = {cols * 2};
+    cuuint32_t box[2] = {(cuuint32_t)kBK, box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? CARD_OK : CARD_E_CUDA;
+}
+
+static int g_num_sms = 0;
+static int num_sms() {
+    if (!g_num_sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+        if (g_num_sms <= 0) g_num_sms = 148;
+    }
+    return g_num_sms;
+}
+
+}  // namespace card
+
+struct card_linear {
+    int kind;   // 0 tc_gemm, 1 gemv, 2 f32
+    int epi;
+    int N, K, Mpad;
+    const void* W;
+    const void* X;
+    CUtensorMap tmW, tmX;
+    card::TcArgs args;
+    int grid, smem;
+    float* scratch;   // gemv swiglu rows
+};
+
+namespace card {
+
+template <int EPI>
+static cudaError_t set_tc_attr(int smem) {
+    return cudaFuncSetAttribute(tc_gemm_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+}
+
+// Split choice: minimise (waves x k-blocks per item) + fixup traffic.
+static int choose_splits(int n_tiles, int kb_total, int Mpad, int slots) {
+    double best = 1e30;
+    int best_s = 1;
+    for (int s = 1; s <= 32 && s <= kb_total; ++s) {
+        const int items = n_tiles * s;
+        const int waves = (items + slots - 1) / slots;
+        const int kb_item = (kb_total + s - 1) / s;
+        double t = (double)waves * kb_item;   // in k-block times
+        if (s > 1) {
+            // partial write + read back: 2 * 128*Mpad*4 bytes per item vs 16 KB per k-block
+            t += (double)waves * (2.0 * kTileN * Mpad * 4) / (kTileN * kBK * 2);
+        }
+        if (t < best - 1e-9) {
+            best = t;
+            best_s = s;
+        }
+    }
+    return best_s;
+}
+
+}  // namespace card
+
+using namespace card;
+
+extern "C" {
+
+int card_linear_create(const void* W, int N, int K, int wdtype, const void* X, int m_max, int epi, void* out,
+                       int ldo, const float* bias, card_linear** out_h) {
+    if (!out_h || !W || !X || N <= 0 || K <= 0 || m_max <= 0) return CARD_E_INPUT;
+    *out_h = nullptr;
+    card_linear* h = (card_linear*)calloc(1, sizeof(card_linear));
+    h->epi = epi;
+    h->N = N;
+    h->K = K;
+    h->W = W;
+    h->X = X;
+    TcArgs& a = h->args;
+    a.N = N;
+    a.K = K;
+    a.epi = epi;
+    a.bias = bias;
+    a.ldo = ldo;
+    if (epi == EPI_STORE_BF16 || epi == EPI_SWIGLU_BF16) a.out_bf16 = (__nv_bfloat16*)out;
+    else a.out_f32 = (float*)out;
+    if (wdtype == 1) {   // fp32 parity path
+        h->kind = 2;
+        a.out_f32 = (float*)out;
+        if (epi == EPI_SWIGLU_BF16) {
+            CARD_CUDA_TRY(cudaMalloc(&h->scratch, (size_t)m_max * N * 4));
+            a.out_f32 = h->scratch;
+            a.ldo = N;
+            h->args.out_bf16 = (__nv_bfloat16*)out;   // swiglu target (f32 buffer in f32 mode)
+        }
+        h->grid = (N + 7) / 8;
+        *out_h = h;
+        return CARD_OK;
+    }
+    if (K % kBK != 0 || N % kTileN != 0) {
+        free(h);
+        return CARD_E_CONFIG;
+    }
+    if (m_max == 1) {   // decode GEMV
+        h->kind = 1;
+        if (epi == EPI_SWIGLU_BF16) {
+            CARD_CUDA_TRY(cudaMalloc(&h->scratch, (size_t)N * 4));
+            a.out_f32 = h->scratch;
+            a.ldo = N;
+            h->args.out_bf16 = (__nv_bfloat16*)out;
+        }
+        h->smem = K * 2;
+        if (h->smem > 48 * 1024) {
+            cudaFuncSetAttribute(gemv_bf16_kernel<EPI_STORE_F32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+            cudaFuncSetAttribute(gemv_bf16_kernel<EPI_RESID_F32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+            cudaFuncSetAttribute(gemv_bf16_kernel<EPI_STORE_BF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        }
+        h->grid = num_sms() * 4;
+        *out_h = h;
+        return CARD_OK;
+    }
+    h->kind = 0;
+    const int Mpad = ((m_max + 15) / 16) * 16;
+    if (Mpad > 256) {
+        free(h);
+        return CARD_E_CONFIG;
+    }
+    h->Mpad = Mpad;
+    a.Mpad = Mpad;
+    a.n_tiles = N / kTileN;
+    a.kb_total = K / kBK;
+    // TMEM: double-buffered accumulator when two of them fit in 256 columns
+    a.n_acc_buf = (2 * Mpad <= 256) ? 2 : 1;
+    int cols = 32;
+    while (cols < a.n_acc_buf * Mpad) cols <<= 1;
+    a.tmem_cols = cols;
+    const int ctas_per_sm = (cols <= 256) ? 2 : 1;
+    const int stage_bytes = kTileN * kBK * 2 + Mpad * kBK * 2;
+    const int budget = (ctas_per_sm == 2 ? 110 : 220) * 1024;
+    const int extra = 1024 + 64 * 8 + 16 * 64 * 4 + 64;
+    int stages = (budget - extra) / stage_bytes;
+    if (stages > 8) stages = 8;
+    if (stages < 2) stages = 2;
+    a.stages = stages;
+    h->smem = stages * stage_bytes + extra;
+    const int slots = num_sms() * ctas_per_sm;
+    a.splits = choose_splits(a.n_tiles, a.kb_total, Mpad, slots);
+    a.items = a.n_tiles * a.splits;
+    h->grid = a.items < slots ? a.items : slots;
+    if (a.splits > 1) {
+        CARD_CUDA_TRY(cudaMalloc(&a.ws, (size_t)a.items * kTileN * Mpad * 4));
+        CARD_CUDA_TRY(cudaMalloc(&a.counters, (size_t)a.n_tiles * 4));
+        CARD_CUDA_TRY(cudaMemset(a.counters, 0, (size_t)a.n_tiles * 4));
+    }
+    int rc = make_map_bf16(&h->tmW, W, (uint64_t)N, (uint64_t)K, kTileN, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
+    if (!rc) rc = make_map_bf16(&h->tmX, X, (uint64_t)Mpad, (uint64_t)K, (uint32_t)Mpad, CU_TENSOR_MAP_L2_PROMOTION_L2_128B);
+    if (rc) {
+        free(h);
+        return rc;
+    }
+    cudaError_t e;
+    switch (epi) {
+        case EPI_STORE_F32: e = set_tc_attr<EPI_STORE_F32>(h->smem); break;
+        case EPI_RESID_F32: e = set_tc_attr<EPI_RESID_F32>(h->smem); break;
+        case EPI_STORE_BF16: e = set_tc_attr<EPI_STORE_BF16>(h->smem); break;
+        case EPI_SWIGLU_BF16: e = set_tc_attr<EPI_SWIGLU_BF16>(h->smem); break;
+        default: free(h); return CARD_E_CONFIG;
+    }
+    if (e != cudaSuccess) {
+        set_cuda_error(e);
+        free(h);
+        return CARD_E_CUDA;
+    }
+    *out_h = h;
+    return CARD_OK;
+}
+
+int card_linear_run(card_linear* h, const int32_t* dM, void* stream) {
+    if (!h) return CARD_E_INPUT;
+    cudaStream_t s = (cudaStream_t)stream;
+    TcArgs a = h->args;
+    a.dM = dM;
+    if (h->kind == 0) {
+        switch (h->epi) {
+            case EPI_STORE_F32: tc_gemm_kernel<EPI_STORE_F32><<<h->grid, kTcThreads, h->smem, s>>>(h->tmW, h->tmX, a); break;
+            case EPI_RESID_F32: tc_gemm_kernel<EPI_RESID_F32><<<h->grid, kTcThreads, h->smem, s>>>(h->tmW, h->tmX, a); break;
+            case EPI_STORE_BF16: tc_gemm_kernel<EPI_STORE_BF16><<<h->grid, kTcThreads, h->smem, s>>>(h->tmW, h->tmX, a); break;
+            case EPI_SWIGLU_BF16: tc_gemm_kernel<EPI_SWIGLU_BF16><<<h->grid, kTcThreads, h->smem, s>>>(h->tmW, h->tmX, a); break;
+        }
+    } else if (h->kind == 1) {
+        const __nv_bfloat16* W = (const __nv_bfloat16*)h->W;
+        const __nv_bfloat16* X = (const __nv_bfloat16*)h->X;
+        switch (h->epi) {
+            case EPI_STORE_F32: gemv_bf16_kernel<EPI_STORE_F32><<<h->grid, 256, h->smem, s>>>(W, X, h->N, h->K, a); break;
+            case EPI_RESID_F32: gemv_bf16_kernel<EPI_RESID_F32><<<h->grid, 256, h->smem, s>>>(W, X, h->N, h->K, a); break;
+            case EPI_STORE_BF16: gemv_bf16_kernel<EPI_STORE_BF16><<<h->grid, 256, h->smem, s>>>(W, X, h->N, h->K, a); break;
+            case EPI_SWIGLU_BF16:
+                gemv_bf16_kernel<EPI_STORE_F32><<<h->grid, 256, h->smem, s>>>(W, X, h->N, h->K, a);
+                swiglu_from_rows_kernel<<<(h->N / 2 + 255) / 256, 256, 0, s>>>(h->scratch, dM, h->N, h->args.out_bf16,
+                                                                             h->N / 2);
+                break;
+        }
+    } else {
+        const float* W = (const float*)h->W;
+        const float* X = (const float*)h->X;
+        switch (h->epi) {
+            case EPI_STORE_F32: f32_gemm_kernel<EPI_STORE_F32><<<h->grid, 256, 0, s>>>(W, X, h->N, h->K, a); break;
+            case EPI_RESID_F32: f32_gemm_kernel<EPI_RESID_F32><<<h->grid, 256, 0, s>>>(W, X, h->N, h->K, a); break;
+            case EPI_STORE_BF16: f32_gemm_kernel<EPI_STORE_F32><<<h->grid, 256, 0, s>>>(W, X, h->N, h->K, a); break;
+            case EPI_SWIGLU_BF16:
+                f32_gemm_kernel<EPI_STORE_F32><<<h->grid, 256, 0, s>>>(W, X, h->N, h->K, a);
+                swiglu_f32_kernel<<<256, 256, 0, s>>>(h->scratch, dM, h->N, (float*)h->args.out_bf16, h->N / 2);
+                break;
+        }
+    }
+    CARD_LAUNCH_CHECK();
+    return CARD_OK;
+}
+
+int card_linear_info(card_linear* h, int32_t* info8) {
+    if (!h || !info8) return CARD_E_INPUT;
+    info8[0] = h->kind;
+    info8[1] = h->args.splits;
+    info8[2] = h->args.stages;
+    info8[3] = h->grid;
+    info8[4] = h->smem;
+    info8[5] = h->Mpad;
+    info8[6] = h->args.tmem_cols;
+    info8[7] = h->args.items;
+    return CARD_OK;
+}
+
+int card_linear_destroy(card_linear* h) {
+    if (!h) return CARD_OK;
+    if (h->args.ws) cudaFree(h->args.ws);
+    if (h->args.counters) cudaFree(h->args.counters);
+    if (h->scratch) cudaFree(h->scratch);
+    free(h);
+    return CARD_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,35 @@
+// card_llm.h — internal declarations shared by the model / engine kernels.
+#pragma once
+#include <stdint.h>
+
+#include "../../include/card_b200.h"
+
+// GEMM epilogues (card_gemm.cu)
+enum {
+    EPI_STORE_F32 = 0,
+    EPI_RESID_F32 = 1,
+    EPI_STORE_BF16 = 2,
+    EPI_SWIGLU_BF16 = 3,
+};
+
+// Per-forward row descriptors written by the row builders (card_engine.cu)
+// and consumed by the model kernels (card_llm.cu).  Device memory.
+//   tok[r]     input token of row r
+//   pos[r]     RoPE position
+//   slot[r]    KV slot the row's K/V are written to
+//   plen[r]    number of prefix KV slots [0, plen) the row attends to
+//   n_extra[r] number of extra slots (tree ancestors + self) in extra[r][..]
+//   out_rows   rows whose hidden state reaches the lm_head, in output order
+struct CardRows {
+    int32_t* M;         // [1] number of rows this forward
+    int32_t* n_out;     // [1] number of output rows
+    int32_t* tok;
+    int32_t* pos;
+    int32_t* slot;
+    int32_t* plen;
+    int32_t* n_extra;
+    int32_t* extra;     // [rows_max * extra_max]
+    int32_t* out_rows;  // [rows_max]
+    int rows_max;
+    int extra_max;
+};

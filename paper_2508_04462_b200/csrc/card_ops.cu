@@ -21,7 +21,7 @@ void set_cuda_error(cudaError_t e) {
 // fp64 work spread over the block; the softmax sum is sequential in token
 // order (as the reference) and runs on one thread — V is toy-sized here.
 __global__ void kgram_dist_kernel(uint64_t s1_seed, uint64_t s2_seed, double mix_weight,
-                                  const int64_t* __restrict__ tails, int tail_len, int vocab,
+                                  const int32_t* __restrict__ tails, int tail_len, int tail_stride, int vocab,
                                   double sharpness, double temperature, double* __restrict__ out) {
     const int row = blockIdx.x;
     __shared__ uint64_t st[2];
@@ -31,7 +31,9 @@ __global__ void kgram_dist_kernel(uint64_t s1_seed, uint64_t s2_seed, double mix
         uint64_t s = mix64(s1_seed + kSeedSalt);
         uint64_t s2 = mix64(s2_seed + kSeedSalt);
         for (int j = 0; j < tail_len; ++j) {
-            uint64_t t = (uint64_t)(tails[(int64_t)row * tail_len + j] + 1);
+            const int32_t tv = tails[(int64_t)row * tail_stride + j];
+            if (tv < 0) continue;   // context shorter than the model order (lm.py:235)
+            uint64_t t = (uint64_t)(tv + 1);
             s = mix64(s ^ mix64(t));
             s2 = mix64(s2 ^ mix64(t));
         }
@@ -190,12 +192,13 @@ const char* card_strerror(int code) {
 
 const char* card_last_cuda_error(void) { return g_cuda_err; }
 
-int card_kgram_dist(uint64_t seed, uint64_t seed2, double mix_weight, const int64_t* tails, int tail_len,
-                    int n_rows, int vocab, double sharpness, double temperature, double* out, void* stream) {
-    if (vocab < 1 || n_rows < 0 || tail_len < 0) return CARD_E_INPUT;
+int card_kgram_dist(uint64_t seed, uint64_t seed2, double mix_weight, const int32_t* tails, int tail_len,
+                    int tail_stride, int n_rows, int vocab, double sharpness, double temperature, double* out,
+                    void* stream) {
+    if (vocab < 1 || n_rows < 0 || tail_len < 0 || tail_stride < tail_len) return CARD_E_INPUT;
     if (n_rows == 0) return CARD_OK;
-    kgram_dist_kernel<<<n_rows, 128, 0, (cudaStream_t)stream>>>(seed, seed2, mix_weight, tails, tail_len, vocab,
-                                                               sharpness, temperature, out);
+    kgram_dist_kernel<<<n_rows, 128, 0, (cudaStream_t)stream>>>(seed, seed2, mix_weight, tails, tail_len,
+                                                               tail_stride, vocab, sharpness, temperature, out);
     CARD_LAUNCH_CHECK();
     return CARD_OK;
 }

@@ -1,0 +1,737 @@
+"""Query-and-correct decode loop on the device (mirrors engine.py:41-423 of
+the reference).
+
+Every protocol step is a CUDA kernel sequence on one stream:
+
+  draft step  : card_draft_rows -> model forward (k-gram stream or
+                transformer + lm_head top-k) -> card_cache_expand_topk ->
+                card_record_width                       (engine.py:198-221)
+  target step : card_cache_query -> card_target_rows -> model forward ->
+                card_verify_{argmax,probs} -> card_commit -> card_cache_correct
+                -> draft KV promote / compaction move -> card_cycle_end
+                                                         (engine.py:228-272)
+
+Two drivers share those sequences:
+
+* ``stepwise`` (parity / trace mode): the host synchronises after every
+  step, reproducing ``_run_serial`` (engine.py:290-317) event for event,
+  including ``cache_alive_nodes`` and the virtual clock;
+* ``graph`` (throughput mode): each step is a captured CUDA graph; the host
+  launches ``min(ratio, max_depth - depth)`` draft graphs and one target
+  graph per cycle and reads back one record per cycle (no other sync).
+
+``mode="concurrent"`` runs the same lockstep schedule on one GPU: greedy
+output is schedule-invariant (engine.py:11-12), the trace is the serial one.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+import time
+from dataclasses import asdict, dataclass, field
+from typing import Sequence
+
+import numpy as np
+import torch
+
+from ._device import ptr, require_cuda, stream_ptr
+from ._lib import EngineState, lib
+from .cache import CacheConfig, TreeCache
+from .errors import ConfigError, InputError, ProtocolError, raise_for_status
+from .metrics import RunMetrics, finalize
+
+TokenId = int
+MODES = ("serial_sim", "concurrent")
+PREFILL_CHUNK = 128
+
+
+def communication_ratio(target_latency: float, draft_latency: float) -> int:
+    """engine.py:41-48."""
+    if target_latency <= 0.0 or draft_latency <= 0.0:
+        raise ConfigError("latencies must be positive")
+    return max(1, math.ceil(target_latency / draft_latency - 1e-9))
+
+
+@dataclass
+class EngineConfig:
+    """engine.py:51-102 (same fields, defaults and validation)."""
+
+    K: int = 50
+    k: int = 3
+    ratio: int = 5
+    temperature: float = 0.0
+    max_new_tokens: int = 64
+    mode: str = "serial_sim"
+    correction_enabled: bool = True
+    seed: int = 0
+    query_depth: int | None = None
+    max_depth: int | None = None
+    time_scale: float = 1e-3
+
+    def __post_init__(self) -> None:
+        for name in ("K", "k", "ratio", "max_new_tokens"):
+            v = getattr(self, name)
+            if not isinstance(v, int) or isinstance(v, bool) or v < 1:
+                raise ConfigError(f"{name} must be a positive integer, got {v!r}")
+        if self.query_depth is None:
+            self.query_depth = self.ratio
+        if self.max_depth is None:
+            self.max_depth = 2 * self.ratio
+        for name in ("query_depth", "max_depth"):
+            v = getattr(self, name)
+            if not isinstance(v, int) or isinstance(v, bool) or v < 1:
+                raise ConfigError(f"{name} must be a positive integer, got {v!r}")
+        if not isinstance(self.temperature, (int, float)) or not math.isfinite(self.temperature):
+            raise ConfigError(f"temperature must be finite, got {self.temperature!r}")
+        if self.temperature < 0.0:
+            raise ConfigError(f"temperature must be >= 0, got {self.temperature!r}")
+        if self.mode not in MODES:
+            raise ConfigError(f"mode must be one of {MODES}, got {self.mode!r}")
+        if not isinstance(self.seed, int) or isinstance(self.seed, bool):
+            raise ConfigError(f"seed must be an integer, got {self.seed!r}")
+        if not isinstance(self.time_scale, (int, float)) or self.time_scale <= 0.0:
+            raise ConfigError(f"time_scale must be positive, got {self.time_scale!r}")
+        if not isinstance(self.correction_enabled, bool):
+            raise ConfigError("correction_enabled must be a bool")
+
+    @classmethod
+    def from_dict(cls, d: dict) -> "EngineConfig":
+        allowed = set(cls.__dataclass_fields__)
+        unknown = sorted(set(d) - allowed)
+        if unknown:
+            raise ConfigError(f"unknown config keys {unknown}; allowed keys are {sorted(allowed)}")
+        return cls(**d)
+
+    def to_dict(self) -> dict:
+        return asdict(self)
+
+
+@dataclass(frozen=True)
+class StepTrace:
+    step_index: int
+    sim_time: float
+    hit: bool
+    candidate_len: int
+    accepted_len: int
+    lnew: int
+    cache_alive_nodes: int
+    event: str
+
+    def to_dict(self) -> dict:
+        return asdict(self)
+
+
+@dataclass
+class RunResult:
+    output: list[TokenId]
+    metrics: RunMetrics
+    trace: list[StepTrace] = field(repr=False)
+    wall: dict = field(default_factory=dict, repr=False)
+
+
+def _check_pair(draft, target) -> None:
+    if draft.vocab.size != target.vocab.size:
+        raise ConfigError(f"draft and target vocabularies differ: {draft.vocab.size} vs {target.vocab.size}")
+    if draft.eos_token != target.eos_token:
+        raise ConfigError(f"draft and target disagree on the eos token: {draft.eos_token!r} vs {target.eos_token!r}")
+
+
+def _check_prompt(prompt: Sequence[TokenId], vocab_size: int) -> list[TokenId]:
+    toks = list(prompt)
+    if not toks:
+        raise InputError("prompt must contain at least one token")
+    for i, t in enumerate(toks):
+        if not isinstance(t, (int, np.integer)) or isinstance(t, bool) or t < 0 or t >= vocab_size:
+            raise InputError(f"prompt token {t!r} at position {i} is out of vocabulary")
+    return [int(t) for t in toks]
+
+
+# ====================================================================== adapters
+class _RowsAndTail:
+    def __init__(self, rows_max: int, extra_max: int, order: int, dev):
+        from .llama import RowBlock
+
+        self.rows = RowBlock(rows_max, extra_max, dev)
+        self.order = max(1, order)
+        self.tail = torch.full((rows_max, self.order), -1, dtype=torch.int32, device=dev)
+
+
+class _KGramAdapter:
+    """Device k-gram toy (lm.py:199-256 via card_kgram_dist)."""
+
+    def __init__(self, model, rows_max: int, k: int, dev):
+        self.m = model
+        V = model.vocab.size
+        self.V = V
+        self.rows_max = rows_max
+        self.k = k
+        self.probs = torch.zeros((rows_max, V), dtype=torch.float64, device=dev)
+        kk = min(k, V)
+        self.kk = kk
+        self.tok = torch.zeros((rows_max, k), dtype=torch.int32, device=dev)
+        self.val = torch.zeros((rows_max, k), dtype=torch.float64, device=dev)
+        self.cnt = torch.zeros(rows_max, dtype=torch.int32, device=dev)
+
+    def _dists(self, rt: _RowsAndTail, t_score: float):
+        m = self.m
+        L_ = lib()
+        M64 = (1 << 64) - 1
+        off = rt.order - m.order   # the model reads context[-order:] (lm.py:235)
+        tails = ctypes.c_void_p(rt.tail.data_ptr() + 4 * off)
+        raise_for_status(L_.card_kgram_dist(m.seed & M64, m.mix_seed & M64, m.mix_weight, tails, m.order, rt.order,
+                                            self.rows_max, self.V, m.sharpness, t_score, ptr(self.probs),
+                                            stream_ptr()), "kgram_dist")
+        if m.eos_token is not None:
+            raise_for_status(L_.card_eos_fix(ptr(rt.rows.n_out), self.rows_max, ptr(rt.tail), rt.order, m.eos_token,
+                                             self.V, ptr(self.probs), stream_ptr()), "eos_fix")
+
+    def draft(self, run):
+        self._dists(run.drt, run.t_score)
+        L_ = lib()
+        raise_for_status(L_.card_rows_topk(ptr(self.probs), self.rows_max, self.V, self.kk, ptr(self.tok),
+                                           ptr(self.val), ptr(self.cnt), None, stream_ptr()), "rows_topk")
+        return self.tok, self.val, self.cnt, 1
+
+    def target(self, run):
+        self._dists(run.trt, run.t_score)
+        raise_for_status(lib().card_verify_probs(run.E_ptr, run.q_tok_ptr, ptr(self.probs), self.V, None,
+                                                 ptr(run.uni), stream_ptr()), "verify_probs")
+
+    def prefill(self, run, tokens):
+        pass
+
+    def post_correct(self, run):
+        pass
+
+
+class _LlamaAdapter:
+    """Transformer draft/target (llama.py) with fused lm_head epilogues."""
+
+    def __init__(self, model, role: str, run, rows_max: int):
+        self.m = model
+        self.role = role
+        self.rows_max = rows_max
+        tree_slots = run.cache_capacity if role == "draft" else 0
+        budgets = {rows_max, PREFILL_CHUNK}
+        self.rt = model.runtime(run.max_ctx, tree_slots, budgets)
+        if self.rt.extra_max < run.cfg.max_depth + 1:
+            raise ConfigError("max_depth too large for the tree-attention extra-slot budget")
+        dev = run.dev
+        V = model.vocab.size
+        self.V = V
+        self.k = run.cfg.k
+        self.tok = torch.zeros((rows_max, self.k), dtype=torch.int32, device=dev)
+        self.logp = torch.zeros((rows_max, self.k), dtype=torch.float64, device=dev)
+        self.cnt = torch.zeros(rows_max, dtype=torch.int32, device=dev)
+        self.amax = torch.zeros(rows_max, dtype=torch.int32, device=dev)
+        self.probs = torch.zeros((rows_max, V), dtype=torch.float64, device=dev) if run.sampling else None
+        self.prefill_rows = None
+        if role == "draft":
+            nL = model.cfg.n_layers
+            row_bytes = self.rt.kv_row_elems() * self.rt.kv_esize()
+            self.scratch_k = torch.zeros(run.cache_capacity * nL * row_bytes // 2, dtype=torch.int16, device=dev)
+            self.scratch_v = torch.zeros_like(self.scratch_k)
+            self.scratch_ptrs = torch.tensor([self.scratch_k.data_ptr(), self.scratch_v.data_ptr()],
+                                             dtype=torch.int64, device=dev)
+
+    def _bias(self, rt_tail: _RowsAndTail):
+        b = self.m.bias
+        if b.sharpness == 0.0:
+            return
+        M64 = (1 << 64) - 1
+        tails = ctypes.c_void_p(rt_tail.tail.data_ptr() + 4 * (rt_tail.order - b.order))
+        raise_for_status(lib().card_logit_bias(ptr(self.rt.logits), ptr(rt_tail.rows.n_out), self.rows_max, self.V,
+                                               tails, b.order, rt_tail.order, b.seed & M64, b.mix_seed & M64,
+                                               float(b.mix_weight), float(b.sharpness), stream_ptr()), "logit_bias")
+
+    def prefill(self, run, tokens):
+        """Causal forward of tokens[0..n) into KV slots 0..n-1 (no outputs used)."""
+        from .llama import RowBlock
+
+        if not tokens:
+            return
+        if self.prefill_rows is None:
+            self.prefill_rows = RowBlock(PREFILL_CHUNK, 1, run.dev)
+        for s in range(0, len(tokens), PREFILL_CHUNK):
+            chunk = tokens[s:s + PREFILL_CHUNK]
+            self.prefill_rows.set_chain(chunk, s)
+            self.rt.forward(self.prefill_rows, PREFILL_CHUNK)
+
+    def draft(self, run):
+        rows = run.drt.rows
+        self.rt.forward(rows, self.rows_max)
+        self._bias(run.drt)
+        raise_for_status(lib().card_topk_logits(ptr(self.rt.logits), ptr(rows.n_out), self.rows_max, self.V, self.k,
+                                                1.0 / run.t_score, ptr(self.tok), ptr(self.logp), ptr(self.cnt),
+                                                stream_ptr()), "topk_logits")
+        return self.tok, self.logp, self.cnt, 0
+
+    def target(self, run):
+        rows = run.trt.rows
+        self.rt.forward(rows, self.rows_max)
+        self._bias(run.trt)
+        L_ = lib()
+        if run.sampling:
+            raise_for_status(L_.card_softmax64(ptr(self.rt.logits), ptr(rows.n_out), self.rows_max, self.V,
+                                               1.0 / run.t_score, ptr(self.probs), stream_ptr()), "softmax64")
+            raise_for_status(L_.card_verify_probs(run.E_ptr, run.q_tok_ptr, ptr(self.probs), self.V, None,
+                                                  ptr(run.uni), stream_ptr()), "verify_probs")
+        else:
+            raise_for_status(L_.card_argmax_logits(ptr(self.rt.logits), ptr(rows.n_out), self.rows_max, self.V,
+                                                   ptr(self.amax), stream_ptr()), "argmax")
+            raise_for_status(L_.card_verify_argmax(run.E_ptr, run.q_tok_ptr, ptr(self.amax), stream_ptr()),
+                             "verify_argmax")
+
+    def post_correct(self, run):
+        """Draft KV roll-forward: promote accepted tree KV, then follow compaction."""
+        if self.role != "draft":
+            return
+        rt = self.rt
+        L_ = lib()
+        nL = self.m.cfg.n_layers
+        raise_for_status(L_.card_draft_promote(run.E_ptr, run.cache.handle, ptr(rt.k_ptrs), ptr(rt.v_ptrs), nL,
+                                               rt.kv_row_elems(), rt.kv_esize(), rt.tree_base, run.cfg.max_depth + 2,
+                                               stream_ptr()), "draft_promote")
+        raise_for_status(L_.card_kv_compact(run.E_ptr, run.cache.handle, ptr(rt.k_ptrs), ptr(rt.v_ptrs), nL,
+                                            rt.kv_row_elems(), rt.kv_esize(), rt.tree_base, ptr(self.scratch_ptrs),
+                                            run.cache_capacity, stream_ptr()), "kv_compact")
+
+
+def _adapter(model, role, run, rows_max):
+    kind = getattr(model, "engine_kind", "host")
+    if kind == "kgram":
+        return _KGramAdapter(model, rows_max, run.cfg.k, run.dev)
+    if kind == "llama":
+        return _LlamaAdapter(model, role, run, rows_max)
+    raise ConfigError(f"model kind {kind!r} has no device adapter (host-table models run via the TreeCache API)")
+
+
+def _order_of(model) -> int:
+    if getattr(model, "engine_kind", "") == "kgram":
+        return model.order
+    if getattr(model, "engine_kind", "") == "llama":
+        return model.bias.order
+    return 1
+
+
+# ====================================================================== device run
+class DeviceRun:
+    """State of one decode on the device (engine.py:149-272)."""
+
+    def __init__(self, draft, target, prompt, config: EngineConfig, *, trace_alive: bool = True):
+        _check_pair(draft, target)
+        self.draft_model, self.target_model = draft, target
+        self.cfg = config
+        self.dev = require_cuda()
+        self.prompt = _check_prompt(prompt, target.vocab.size)
+        self.t_score = config.temperature if config.temperature > 0.0 else 1.0
+        self.sampling = config.temperature > 0.0
+        self.trace_alive = trace_alive
+        self.eos = target.eos_token
+        cfg = config
+        C0 = len(self.prompt)
+        self.max_ctx = C0 + cfg.max_new_tokens + cfg.max_depth + 8
+        if cfg.correction_enabled:
+            self.cache_capacity = 6 * cfg.K * (cfg.max_depth + 1) + 256
+        else:   # the un-steered ablation never compacts (cache.py:415-437)
+            self.cache_capacity = cfg.K * (cfg.max_new_tokens + cfg.max_depth + 2) * 2 + 256
+        self.cache = TreeCache(self.prompt[-1], CacheConfig(cfg.K, cfg.k, cfg.max_depth), eos_token=self.eos,
+                               capacity=self.cache_capacity)
+        order = max(_order_of(draft), _order_of(target))
+        self.d_rows_max = cfg.K + cfg.max_depth + 2
+        self.t_rows_max = cfg.query_depth + 1
+        self.drt = _RowsAndTail(self.d_rows_max, cfg.max_depth + 1, order, self.dev)
+        self.trt = _RowsAndTail(self.t_rows_max, 1, order, self.dev)
+        self.committed = torch.zeros(self.max_ctx + 8, dtype=torch.int32, device=self.dev)
+        self.committed[:C0] = torch.tensor(self.prompt, dtype=torch.int32)
+        rng = np.random.default_rng(cfg.seed)   # engine.py:162; the only randomness
+        n_uni = (cfg.max_new_tokens + 2) * (cfg.query_depth + 2) + 16 if self.sampling else 1
+        self.uni = torch.from_numpy(rng.random(n_uni)).to(self.dev)
+        st = EngineState()
+        st.C = C0
+        st.Pd = 0
+        st.max_new = cfg.max_new_tokens
+        st.eos = -1 if self.eos is None else int(self.eos)
+        st.order = order
+        st.sampling = int(self.sampling)
+        st.base_len = C0
+        st.anchor_origin = int(not cfg.correction_enabled)
+        st.n_uni = n_uni
+        self.E = torch.frombuffer(bytearray(bytes(st)), dtype=torch.int32).to(self.dev)
+        self.E_ptr = ptr(self.E)
+        self.q_tok_ptr = ctypes.c_void_p(self.cache._qbufs[1])
+        self._host = torch.empty(self.E.numel(), dtype=torch.int32, pin_memory=True)
+        self.da = _adapter(draft, "draft", self, self.d_rows_max)
+        self.ta = _adapter(target, "target", self, self.t_rows_max)
+        self._field = {name: getattr(EngineState, name).offset // 4 for name, _ in EngineState._fields_}
+        self.output: list[int] = []
+        self.trace: list[StepTrace] = []
+        self.graphs = None
+        self.timing = {}
+
+    # ---------------------------------------------------------------- state io
+    def _fptr(self, name: str) -> ctypes.c_void_p:
+        return ctypes.c_void_p(self.E.data_ptr() + 4 * self._field[name])
+
+    def read_state(self) -> EngineState:
+        self._host.copy_(self.E, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        return EngineState.from_buffer_copy(self._host.numpy().tobytes())
+
+    def _set_field(self, name: str, value: int):
+        self.E[self._field[name]] = int(value)
+
+    def prefill(self):
+        """Prompt KV for both models: target gets prompt[:-1] (its last token is
+        the first verify input), the draft likewise (its flat step computes the root)."""
+        body = self.prompt[:-1]
+        self.da.prefill(self, body)
+        self.ta.prefill(self, body)
+        self._set_field("Pd", len(body))
+
+    # ---------------------------------------------------------------- sequences
+    def launch_draft_step(self):
+        L_ = lib()
+        s = stream_ptr()
+        raise_for_status(L_.card_draft_rows(self.E_ptr, self.cache.handle, ptr(self.committed), ptr(self.drt.rows.block),
+                                            self.d_rows_max, self.drt.rows.extra_max,
+                                            getattr(self.da, "rt", None).tree_base if hasattr(self.da, "rt") else 0,
+                                            ptr(self.drt.tail), self.drt.order, s), "draft_rows")
+        tok, val, cnt, probs = self.da.draft(self)
+        raise_for_status(L_.card_cache_expand_topk(self.cache.handle, ptr(tok), ptr(val), ptr(cnt), -1, probs,
+                                                   self._fptr("stop"), s), "expand")
+        raise_for_status(L_.card_record_width(self.E_ptr, self.cache.handle, ptr(self.drt.rows.n_out), s), "record")
+
+    def launch_target_step(self, with_correct: bool = True, readback: bool = True):
+        L_ = lib()
+        s = stream_ptr()
+        raise_for_status(L_.card_cache_query(self.cache.handle, self.cfg.query_depth, s), "query")
+        raise_for_status(L_.card_target_rows(self.E_ptr, self.cache.handle, ptr(self.committed),
+                                             ptr(self.trt.rows.block), self.t_rows_max, 1, ptr(self.trt.tail),
+                                             self.trt.order, s), "target_rows")
+        self.ta.target(self)
+        raise_for_status(L_.card_commit(self.E_ptr, ptr(self.committed), s), "commit")
+        if with_correct:
+            self.launch_correct()
+        raise_for_status(L_.card_cycle_end(self.E_ptr, self.cache.handle, s), "cycle_end")
+        if readback:
+            self._host.copy_(self.E, non_blocking=True)
+
+    # ---------------------------------------------------------------- helpers
+    def _alive(self) -> int:
+        if not self.trace_alive:
+            return -1
+        return self.cache.alive_below_root()
+
+    def _emit(self, t, hit, cl, al, ln, ev):
+        self.trace.append(StepTrace(len(self.trace), t, bool(hit), int(cl), int(al), int(ln), self._alive(), ev))
+
+    def _check_cache_status(self):
+        st = self.cache.state()
+        if st.status not in (0, -4):
+            raise_for_status(st.status, "device cache")
+
+    # ---------------------------------------------------------------- stepwise driver
+    def draft_step_sync(self) -> int:
+        self.launch_draft_step()
+        E = self.read_state()
+        self._check_cache_status()
+        w = E.widths[E.n_widths - 1] if 0 < E.n_widths <= 64 else 0
+        self._set_field("stop", 0)
+        self._set_field("n_widths", 0)
+        return w
+
+    def target_step_sync(self):
+        self.launch_target_step(with_correct=False, readback=False)
+        E = self.read_state()
+        self._check_cache_status()
+        return E
+
+    def launch_correct(self):
+        L_ = lib()
+        s = stream_ptr()
+        raise_for_status(L_.card_cache_correct(self.cache.handle, self._fptr("acc"), self._fptr("n_acc"),
+                                               self._fptr("corr"), self._fptr("done"), s), "correct")
+        self.da.post_correct(self)
+
+    def correct_sync(self):
+        self.launch_correct()
+        torch.cuda.current_stream().synchronize()
+        self._check_cache_status()
+
+    def run_stepwise(self):
+        """_run_serial (engine.py:290-317) with one host sync per step."""
+        cfg = self.cfg
+        d_lat = self.draft_model.spec.forward_latency
+        t_lat = self.target_model.spec.forward_latency
+        self.prefill()
+        clock = 0.0
+        for _ in range(cfg.query_depth):
+            w = self.draft_step_sync()
+            if w == 0:
+                break
+            clock += d_lat
+            self._emit(clock, False, w, 0, 0, "draft_expand")
+        done = False
+        while not done:
+            start, n_exp = clock, 0
+            for _ in range(cfg.ratio):
+                w = self.draft_step_sync()
+                if w == 0:
+                    break
+                n_exp += 1
+                self._emit(start + n_exp * d_lat, False, w, 0, 0, "draft_expand")
+            E = self.target_step_sync()
+            clock = start + max(n_exp * d_lat, t_lat)
+            hit = bool(E.rec_hit)
+            self.output.extend(E.committed_now[i] for i in range(E.n_commit))
+            if cfg.correction_enabled:
+                self._emit_target(clock, hit, E)
+                done = bool(E.done)
+                if not done:
+                    self.correct_sync()
+                    self._emit(clock, hit, 0, 0, 0, "correct")
+            else:
+                done = bool(E.done)
+                self._emit_target(clock, hit, E, alive_before_update=True)
+                if not done:
+                    self._ablation_update(E)
+                    self._emit(clock, hit, 0, 0, 0, "correct")
+
+    def _emit_target(self, clock, hit, E, alive_before_update=False):
+        self._emit(clock, hit, E.rec_L if hit else 0, E.rec_acc, E.rec_lnew, "verify" if hit else "miss_step")
+
+    def _ablation_update(self, E):
+        """engine.py:269-272: advance_root, else reset to the last output."""
+        n = E.rec_n_acc
+        acc = [E.acc[i] for i in range(n)]
+        moved = self.cache.advance_root(acc, E.rec_corr)
+        if not moved:
+            self.cache.reset(self.output[-1])
+            C = len(self.prompt) + len(self.output)
+            self._set_field("base_len", C)
+
+    # ---------------------------------------------------------------- graph driver
+    def capture(self):
+        """Capture one draft step and one target step as CUDA graphs."""
+        if not self.cfg.correction_enabled:
+            raise ConfigError("graph mode needs correction_enabled=True (the ablation resets on the host)")
+        g_d, g_t = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        # state snapshot so warmup-by-capture leaves no trace: capture does not execute
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(g_d, stream=s):
+                self.launch_draft_step()
+            with torch.cuda.graph(g_t, stream=s):
+                self.launch_target_step(with_correct=True, readback=True)
+        torch.cuda.current_stream().wait_stream(s)
+        self.graphs = (g_d, g_t)
+
+    def run_graphs(self, max_cycles: int | None = None):
+        """Throughput driver: one host<->device round trip per cycle."""
+        cfg = self.cfg
+        d_lat = self.draft_model.spec.forward_latency
+        t_lat = self.target_model.spec.forward_latency
+        g_d, g_t = self.graphs
+        clock = 0.0
+        depth = 0
+        for _ in range(cfg.query_depth):   # warm-up (engine.py:295-301)
+            g_d.replay()
+        E = self.read_state()
+        for i in range(min(E.n_widths, 64)):
+            w = E.widths[i]
+            if w == 0:
+                break
+            depth += 1
+            clock += d_lat
+            self._emit(clock, False, w, 0, 0, "draft_expand")
+        self._set_field("n_widths", 0)
+        self._set_field("stop", 0)
+        done = False
+        cycles = 0
+        while not done:
+            n_exp = min(cfg.ratio, max(0, cfg.max_depth - depth))
+            for _ in range(n_exp):
+                g_d.replay()
+            g_t.replay()
+            torch.cuda.current_stream().synchronize()
+            E = EngineState.from_buffer_copy(self._host.numpy().tobytes())
+            start, k = clock, 0
+            for i in range(min(E.rec_n_widths, 64)):
+                w = E.rec_widths[i]
+                if w == 0:
+                    break
+                k += 1
+                self._emit(start + k * d_lat, False, w, 0, 0, "draft_expand")
+            clock = start + max(k * d_lat, t_lat)
+            hit = bool(E.rec_hit)
+            self.output.extend(E.committed_now[i] for i in range(E.n_commit))
+            self._emit_target(clock, hit, E)
+            done = bool(E.rec_done)
+            if not done:
+                self._emit(clock, hit, 0, 0, 0, "correct")
+            depth = E.rec_depth
+            cycles += 1
+            if max_cycles is not None and cycles >= max_cycles:
+                break
+        return cycles
+
+
+def _validate_run_config(draft, target, config):
+    if config.max_depth > 30:
+        raise ConfigError("max_depth > 30 is not supported by the device tree attention")
+    if config.query_depth > 62:
+        raise ConfigError("query_depth too large")
+
+
+def run_speculative(draft, target, prompt: Sequence[TokenId], config: EngineConfig, *,
+                    use_graphs: bool | None = None, trace_alive: bool | None = None) -> RunResult:
+    """The generate() entry point (engine.py:275-287), on the device.
+
+    ``use_graphs`` (default: True for transformer pairs with correction on)
+    selects the CUDA-graph driver; the stepwise driver reproduces the
+    reference trace exactly, including ``cache_alive_nodes``."""
+    _validate_run_config(draft, target, config)
+    kinds = {getattr(draft, "engine_kind", "host"), getattr(target, "engine_kind", "host")}
+    if "host" in kinds:
+        from .hostrun import run_host_models
+
+        return run_host_models(draft, target, prompt, config)
+    if use_graphs is None:
+        use_graphs = "llama" in kinds and config.correction_enabled
+    if trace_alive is None:
+        trace_alive = not use_graphs
+    run = DeviceRun(draft, target, prompt, config, trace_alive=trace_alive)
+    t0 = time.perf_counter()
+    if use_graphs:
+        run.prefill()
+        run.capture()
+        torch.cuda.synchronize()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record()
+        run.run_graphs()
+        ev1.record()
+        ev1.synchronize()
+        run.timing["decode_ms"] = ev0.elapsed_time(ev1)
+    else:
+        run.run_stepwise()
+    run.timing["wall_s"] = time.perf_counter() - t0
+    return RunResult(output=run.output, metrics=finalize(run.trace, target.spec, draft.spec), trace=run.trace,
+                     wall=run.timing)
+
+
+# ====================================================================== vanilla AR
+class VanillaRun:
+    """Target-only autoregressive decode (engine.py:392-423) with the same
+    kernels: one token per step, M = 1 rows (the 128-bit-load GEMV path)."""
+
+    def __init__(self, target, prompt, config: EngineConfig):
+        self.target_model = target
+        self.cfg = config
+        self.dev = require_cuda()
+        self.prompt = _check_prompt(prompt, target.vocab.size)
+        self.t_score = config.temperature if config.temperature > 0.0 else 1.0
+        self.sampling = config.temperature > 0.0
+        C0 = len(self.prompt)
+        self.max_ctx = C0 + config.max_new_tokens + 8
+        self.cache_capacity = 64
+        # a never-expanded cache: every query misses, so each step is a miss step
+        self.cache = TreeCache(self.prompt[-1], CacheConfig(1, 1, 1), eos_token=target.eos_token, capacity=64)
+        order = _order_of(target)
+        self.trt = _RowsAndTail(1, 1, order, self.dev)
+        self.committed = torch.zeros(self.max_ctx + 8, dtype=torch.int32, device=self.dev)
+        self.committed[:C0] = torch.tensor(self.prompt, dtype=torch.int32)
+        rng = np.random.default_rng(config.seed)
+        n_uni = config.max_new_tokens + 8 if self.sampling else 1
+        self.uni = torch.from_numpy(rng.random(n_uni)).to(self.dev)
+        st = EngineState()
+        st.C = C0
+        st.max_new = config.max_new_tokens
+        st.eos = -1 if target.eos_token is None else int(target.eos_token)
+        st.order = order
+        st.sampling = int(self.sampling)
+        st.base_len = C0
+        self.E = torch.frombuffer(bytearray(bytes(st)), dtype=torch.int32).to(self.dev)
+        self.E_ptr = ptr(self.E)
+        self.q_tok_ptr = ctypes.c_void_p(self.cache._qbufs[1])
+        self.ta = _adapter(target, "target", self, 1)
+        self.graph = None
+
+    def step(self):
+        L_ = lib()
+        s = stream_ptr()
+        raise_for_status(L_.card_target_rows(self.E_ptr, self.cache.handle, ptr(self.committed),
+                                             ptr(self.trt.rows.block), 1, 1, ptr(self.trt.tail), self.trt.order, s),
+                         "target_rows")
+        self.ta.target(self)
+        raise_for_status(L_.card_commit(self.E_ptr, ptr(self.committed), s), "commit")
+
+    def prefill(self):
+        self.ta.prefill(self, self.prompt[:-1])
+
+    def capture(self):
+        g = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(g, stream=s):
+                self.step()
+        torch.cuda.current_stream().wait_stream(s)
+        self.graph = g
+
+    def decode(self, use_graph: bool = True):
+        n = self.cfg.max_new_tokens
+        for _ in range(n):
+            if use_graph:
+                self.graph.replay()
+            else:
+                self.step()
+
+    def output(self) -> list[int]:
+        host = self.E.cpu().numpy().tobytes()
+        st = EngineState.from_buffer_copy(host)
+        C0 = len(self.prompt)
+        return self.committed[C0:st.C].cpu().tolist()
+
+
+def run_vanilla(target, prompt: Sequence[TokenId], config: EngineConfig, *, use_graph: bool | None = None) -> RunResult:
+    """engine.py:392-423 on the device."""
+    if getattr(target, "engine_kind", "host") == "host":
+        from .hostrun import run_vanilla_host
+
+        return run_vanilla_host(target, prompt, config)
+    run = VanillaRun(target, prompt, config)
+    if use_graph is None:
+        use_graph = getattr(target, "engine_kind", "") == "llama"
+    t0 = time.perf_counter()
+    run.prefill()
+    if use_graph:
+        run.capture()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    run.decode(use_graph)
+    ev1.record()
+    ev1.synchronize()
+    out = run.output()
+    t_lat = target.spec.forward_latency
+    trace = [StepTrace(i, (i + 1) * t_lat, False, 0, 0, 1, 0, "miss_step") for i in range(len(out))]
+    return RunResult(output=out, metrics=finalize(trace, target.spec), trace=trace,
+                     wall={"decode_ms": ev0.elapsed_time(ev1), "wall_s": time.perf_counter() - t0})
+
+
+def forward_context_logits(model, context: list[int]) -> torch.Tensor:
+    """Reference-API helper: logits of the last position of a full context
+    (prefill-style; reuses the model's runtime KV, not reentrant)."""
+    from .llama import RowBlock
+
+    rt = model.runtime(max(len(context) + 8, 64), 0, {PREFILL_CHUNK})
+    rows = RowBlock(PREFILL_CHUNK, 1, rt.dev)
+    for s in range(0, len(context), PREFILL_CHUNK):
+        chunk = context[s:s + PREFILL_CHUNK]
+        rows.set_chain(chunk, s)
+        rt.forward(rows, PREFILL_CHUNK)
+    torch.cuda.synchronize()
+    return rt.logits[0].clone()

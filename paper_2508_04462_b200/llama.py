@@ -1,0 +1,368 @@
+"""Llama-architecture draft/target models on the device.
+
+The reference's model plug-in is the ``ToyModel`` duck type
+(/root/reference/pkg/src/specache/lm.py:109-196): ``next_distribution``
+over a full context and ``batch_tree_forward`` over the newest tree layer.
+Here a model is a KV-cached forward over *rows* built on the device by the
+engine (csrc/card_engine.cu): causal chain rows (prefill, target verify,
+draft catch-up) and tree rows (one per frontier node, attending to the
+committed prefix plus its own ancestors).  Every op is a kernel of
+libcard_b200.so; the weights stream through the tcgen05/TMA GEMM.
+
+Weight layout in HBM (bf16 production / fp32 parity):
+  embed [V,H]; per layer wqkv [(nh+2nkv)*hd, H] (+ fp32 bias for Qwen2),
+  wo [H, nh*hd], wgu [2F, H] interleaved per 128-row tile (64 gate rows then
+  the 64 matching up rows), wd [H, F], fp32 norms; lm_head [V,H] (tied for
+  Llama-3.2-1B / Qwen2.5-0.5B).  KV cache per layer: K,V [slots, nkv, hd]
+  with slots = prefix positions (rounded to 64) + draft tree slots.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass, field, asdict
+
+import numpy as np
+import torch
+
+from ._device import ptr, require_cuda, stream_ptr
+from ._lib import lib
+from .errors import ConfigError, raise_for_status
+
+EPI_STORE_F32, EPI_RESID_F32, EPI_STORE_BF16, EPI_SWIGLU_BF16 = 0, 1, 2, 3
+
+
+@dataclass
+class LlamaConfig:
+    vocab_size: int
+    hidden: int
+    n_layers: int
+    n_heads: int
+    n_kv_heads: int
+    head_dim: int
+    ffn: int
+    rope_theta: float = 500000.0
+    rms_eps: float = 1e-5
+    tie_embeddings: bool = False
+    qkv_bias: bool = False
+    rope_scaling: dict | None = None
+    init_std: float = 0.02
+
+    def __post_init__(self):
+        if self.n_heads % self.n_kv_heads:
+            raise ConfigError("n_heads must be a multiple of n_kv_heads")
+        if self.head_dim % 2:
+            raise ConfigError("head_dim must be even")
+        if self.ffn % 64:
+            raise ConfigError("ffn must be a multiple of 64 (gate/up tile interleave)")
+
+    @property
+    def qkv_dim(self) -> int:
+        return (self.n_heads + 2 * self.n_kv_heads) * self.head_dim
+
+    def layer_params(self) -> int:
+        H, F = self.hidden, self.ffn
+        return H * self.qkv_dim + (self.qkv_dim if self.qkv_bias else 0) + self.n_heads * self.head_dim * H \
+            + 3 * H * F + 2 * H
+
+    def stream_params(self) -> int:
+        """Parameters streamed per forward: layers + final norm + lm_head."""
+        return self.n_layers * self.layer_params() + self.hidden + self.vocab_size * self.hidden
+
+    def total_params(self) -> int:
+        emb = self.vocab_size * self.hidden
+        return self.stream_params() + (0 if self.tie_embeddings else emb)
+
+    def to_dict(self) -> dict:
+        return asdict(self)
+
+
+_LLAMA3_SCALING_1B = dict(factor=32.0, low_freq_factor=1.0, high_freq_factor=4.0,
+                          original_max_position_embeddings=8192)
+_LLAMA3_SCALING_8B = dict(factor=8.0, low_freq_factor=1.0, high_freq_factor=4.0,
+                          original_max_position_embeddings=8192)
+
+PRESETS = {
+    # BASELINE.json configs[1]
+    "llama-3.2-1b": LlamaConfig(128256, 2048, 16, 32, 8, 64, 8192, 500000.0, 1e-5, True, False, _LLAMA3_SCALING_1B),
+    "llama-3.1-8b": LlamaConfig(128256, 4096, 32, 32, 8, 128, 14336, 500000.0, 1e-5, False, False, _LLAMA3_SCALING_8B),
+    # BASELINE.json configs[2]
+    "qwen2.5-0.5b": LlamaConfig(151936, 896, 24, 14, 2, 64, 4864, 1000000.0, 1e-6, True, True, None),
+    "qwen2.5-7b": LlamaConfig(152064, 3584, 28, 28, 4, 128, 18944, 1000000.0, 1e-6, False, True, None),
+    # BASELINE.json configs[0]: the CPU-runnable tiny pair (FFN rounded to 704)
+    "tiny-target": LlamaConfig(64, 256, 4, 4, 2, 64, 704, 10000.0, 1e-5, False, False, None),
+    "tiny-draft": LlamaConfig(64, 128, 2, 4, 2, 32, 384, 10000.0, 1e-5, False, False, None),
+    # bf16-kernel test sizes (multiples of the 128x64 weight tile)
+    "small-target": LlamaConfig(512, 512, 4, 8, 4, 64, 1536, 10000.0, 1e-5, False, False, None),
+    "small-draft": LlamaConfig(512, 256, 2, 4, 2, 64, 768, 10000.0, 1e-5, True, False, None),
+}
+
+
+def rope_tables(cfg: LlamaConfig, max_pos: int) -> tuple[torch.Tensor, torch.Tensor]:
+    """cos/sin [max_pos, hd/2] fp32, HF Llama-3 frequency scaling; computed on
+    the CPU so the device and the oracle use identical tables."""
+    hd = cfg.head_dim
+    inv = 1.0 / (cfg.rope_theta ** (torch.arange(0, hd, 2, dtype=torch.int64).float() / hd))
+    sc = cfg.rope_scaling
+    if sc:
+        factor, lo, hi, old = sc["factor"], sc["low_freq_factor"], sc["high_freq_factor"], \
+            sc["original_max_position_embeddings"]
+        low_wl, high_wl = old / lo, old / hi
+        wl = 2 * math.pi / inv
+        inv_l = torch.where(wl > low_wl, inv / factor, inv)
+        smooth = (old / wl - lo) / (hi - lo)
+        smoothed = (1 - smooth) * inv_l / factor + smooth * inv_l
+        is_med = ~(wl < high_wl) * ~(wl > low_wl)
+        inv = torch.where(is_med, smoothed, inv_l)
+    t = torch.arange(max_pos, dtype=torch.int64).float()
+    freqs = torch.outer(t, inv)
+    return freqs.cos().contiguous(), freqs.sin().contiguous()
+
+
+def init_weights(cfg: LlamaConfig, seed: int, device="cpu", dtype=torch.float32) -> dict:
+    """Canonical (HF-layout) random-init weights: Normal(0, init_std), norms 1,
+    biases 0.  Same seed + same device => identical tensors (the oracle and
+    the device model are built from one call on the CPU for parity runs)."""
+    g = torch.Generator(device=device)
+    g.manual_seed(int(seed))
+
+    def normal(*shape):
+        t = torch.empty(shape, dtype=torch.float32, device=device)
+        t.normal_(0.0, cfg.init_std, generator=g)
+        return t.to(dtype)
+
+    H, hd = cfg.hidden, cfg.head_dim
+    w = {"embed": normal(cfg.vocab_size, H)}
+    for i in range(cfg.n_layers):
+        p = f"l{i}."
+        w[p + "wq"] = normal(cfg.n_heads * hd, H)
+        w[p + "wk"] = normal(cfg.n_kv_heads * hd, H)
+        w[p + "wv"] = normal(cfg.n_kv_heads * hd, H)
+        if cfg.qkv_bias:
+            w[p + "bq"] = torch.zeros(cfg.n_heads * hd, device=device)
+            w[p + "bk"] = torch.zeros(cfg.n_kv_heads * hd, device=device)
+            w[p + "bv"] = torch.zeros(cfg.n_kv_heads * hd, device=device)
+        w[p + "wo"] = normal(H, cfg.n_heads * hd)
+        w[p + "wg"] = normal(cfg.ffn, H)
+        w[p + "wu"] = normal(cfg.ffn, H)
+        w[p + "wd"] = normal(H, cfg.ffn)
+        w[p + "attn_norm"] = torch.ones(H, device=device)
+        w[p + "mlp_norm"] = torch.ones(H, device=device)
+    w["norm"] = torch.ones(H, device=device)
+    w["lm_head"] = w["embed"] if cfg.tie_embeddings else normal(cfg.vocab_size, H)
+    return w
+
+
+def interleave_gate_up(wg: torch.Tensor, wu: torch.Tensor) -> torch.Tensor:
+    """[2F, H]: per 128-row tile, 64 gate rows then the 64 matching up rows."""
+    F, H = wg.shape
+    t = torch.stack([wg.view(F // 64, 64, H), wu.view(F // 64, 64, H)], dim=1)
+    return t.reshape(2 * F, H).contiguous()
+
+
+def pack_weights(cfg: LlamaConfig, weights: dict, dtype: str = "bf16", device=None) -> dict:
+    """Canonical weights -> the device layout (fused QKV, interleaved gate/up)."""
+    if dtype not in ("bf16", "fp32"):
+        raise ConfigError(f"dtype must be bf16 or fp32, got {dtype!r}")
+    dev = device or require_cuda()
+    wdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    to = lambda t: t.to(device=dev, dtype=wdt).contiguous()  # noqa: E731
+    f32 = lambda t: t.to(device=dev, dtype=torch.float32).contiguous()  # noqa: E731
+    out = {"dtype": dtype, "embed": to(weights["embed"]), "norm": f32(weights["norm"]), "layers": []}
+    out["lm_head"] = out["embed"] if cfg.tie_embeddings else to(weights["lm_head"])
+    for i in range(cfg.n_layers):
+        p = f"l{i}."
+        out["layers"].append({
+            "wqkv": to(torch.cat([weights[p + "wq"], weights[p + "wk"], weights[p + "wv"]], 0)),
+            "wo": to(weights[p + "wo"]),
+            "wgu": to(interleave_gate_up(weights[p + "wg"], weights[p + "wu"])),
+            "wd": to(weights[p + "wd"]),
+            "attn_norm": f32(weights[p + "attn_norm"]),
+            "mlp_norm": f32(weights[p + "mlp_norm"]),
+            "bqkv": f32(torch.cat([weights[p + "bq"], weights[p + "bk"], weights[p + "bv"]], 0))
+            if cfg.qkv_bias else None,
+        })
+    return out
+
+
+class _Linear:
+    def __init__(self, W: torch.Tensor, X: torch.Tensor, m_max: int, epi: int, out: torch.Tensor, ldo: int,
+                 bias: torch.Tensor | None = None):
+        self.keep = (W, X, out, bias)
+        h = ctypes.c_void_p()
+        wd = 0 if W.dtype == torch.bfloat16 else 1
+        rc = lib().card_linear_create(ptr(W), W.shape[0], W.shape[1], wd, ptr(X), m_max, epi, ptr(out), ldo,
+                                      ptr(bias), ctypes.byref(h))
+        raise_for_status(rc, f"card_linear_create(N={W.shape[0]}, K={W.shape[1]}, m_max={m_max})")
+        self.h = h
+        info = (ctypes.c_int32 * 8)()
+        lib().card_linear_info(h, info)
+        self.info = dict(zip(("kind", "splits", "stages", "grid", "smem", "Mpad", "tmem_cols", "items"), list(info)))
+
+    def run(self, dM: torch.Tensor):
+        rc = lib().card_linear_run(self.h, ptr(dM), stream_ptr())
+        if rc:
+            raise_for_status(rc, "card_linear_run")
+
+    def __del__(self):
+        try:
+            if self.h:
+                lib().card_linear_destroy(self.h)
+        except Exception:
+            pass
+
+
+class DeviceLlama:
+    """One draft or target model resident in HBM with its KV cache.
+
+    ``plans`` are per row-budget (e.g. 1 for AR decode, r+1 for verify,
+    K+max_depth+2 for draft tree steps, 128 for prefill chunks); each plan
+    owns the GEMM launch configurations (tensor maps, split-K workspaces)
+    bound to the shared activation buffers.
+    """
+
+    def __init__(self, cfg: LlamaConfig, packed: dict, *, max_ctx: int, tree_slots: int = 0,
+                 row_budgets=(1,), extra_max: int = 32):
+        self.dev = require_cuda()
+        dtype = packed["dtype"]
+        self.cfg = cfg
+        self.dtype = dtype
+        self.wdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+        self.code = 0 if dtype == "bf16" else 1
+        self.max_ctx = max_ctx
+        self.prefix_slots = ((max_ctx + 63) // 64) * 64
+        self.tree_base = self.prefix_slots
+        self.n_slots = self.prefix_slots + tree_slots
+        self.tree_slots = tree_slots
+        self.extra_max = extra_max
+        c = cfg
+        dev = self.dev
+        wdt = self.wdt
+        H, hd = c.hidden, c.head_dim
+        self.embed = packed["embed"]
+        self.lm_head = packed["lm_head"]
+        self.norm = packed["norm"]
+        self.layers = packed["layers"]
+        kvdt = wdt
+        self.k_cache = [torch.zeros((self.n_slots, c.n_kv_heads, hd), dtype=kvdt, device=dev) for _ in range(c.n_layers)]
+        self.v_cache = [torch.zeros((self.n_slots, c.n_kv_heads, hd), dtype=kvdt, device=dev) for _ in range(c.n_layers)]
+        cos, sin = rope_tables(c, max_ctx + 8)
+        self.cos, self.sin = cos.to(dev), sin.to(dev)
+        # activation buffers sized for the largest row budget
+        mmax = max(row_budgets)
+        self.mpad = ((mmax + 15) // 16) * 16
+        act = wdt
+        P = self.mpad
+        self.x = torch.zeros((P, H), dtype=torch.float32, device=dev)
+        self.h = torch.zeros((P, H), dtype=act, device=dev)
+        self.qkv = torch.zeros((P, c.qkv_dim), dtype=torch.float32, device=dev)
+        self.q = torch.zeros((P, c.n_heads * hd), dtype=torch.float32, device=dev)
+        self.o = torch.zeros((P, c.n_heads * hd), dtype=act, device=dev)
+        self.g = torch.zeros((P, c.ffn), dtype=act, device=dev)
+        self.hf = torch.zeros((P, H), dtype=act, device=dev)
+        self.logits = torch.zeros((P, c.vocab_size), dtype=torch.float32, device=dev)
+        nwork = lib().card_attention_work_floats(P, c.n_heads, hd, self.prefix_slots)
+        self.work = torch.zeros(nwork, dtype=torch.float32, device=dev)
+        # per-layer KV base pointer arrays for the engine's KV movers
+        self.k_ptrs = torch.tensor([t.data_ptr() for t in self.k_cache], dtype=torch.int64, device=dev)
+        self.v_ptrs = torch.tensor([t.data_ptr() for t in self.v_cache], dtype=torch.int64, device=dev)
+        self.plans = {m: self._make_plan(m) for m in sorted(set(row_budgets))}
+
+    # ------------------------------------------------------------ plans
+    def _make_plan(self, m_max: int) -> dict:
+        c = self.cfg
+        H = c.hidden
+        plan = {"m_max": m_max, "layers": []}
+        for L in self.layers:
+            plan["layers"].append({
+                "qkv": _Linear(L["wqkv"], self.h, m_max, EPI_STORE_F32, self.qkv, c.qkv_dim, L["bqkv"]),
+                "o": _Linear(L["wo"], self.o, m_max, EPI_RESID_F32, self.x, H),
+                "gu": _Linear(L["wgu"], self.h, m_max, EPI_SWIGLU_BF16, self.g, c.ffn),
+                "d": _Linear(L["wd"], self.g, m_max, EPI_RESID_F32, self.x, H),
+            })
+        plan["lm_head"] = _Linear(self.lm_head, self.hf, m_max, EPI_STORE_F32, self.logits, c.vocab_size)
+        return plan
+
+    def kv_row_elems(self) -> int:
+        return self.cfg.n_kv_heads * self.cfg.head_dim
+
+    def kv_esize(self) -> int:
+        return 2 if self.dtype == "bf16" else 4
+
+    # ------------------------------------------------------------ forward
+    def forward(self, rows: "RowBlock", m_max: int):
+        """Run the forward over the device rows; logits for the output rows
+        land in self.logits[:n_out].  Asynchronous, graph-capturable."""
+        c = self.cfg
+        L_ = lib()
+        s = stream_ptr()
+        plan = self.plans[m_max]
+        dM, dOut = rows.M, rows.n_out
+        hd = c.head_dim
+        mm = self.mpad
+        chk = raise_for_status
+        chk(L_.card_embed(ptr(rows.tok), ptr(dM), mm, ptr(self.embed), self.code, c.hidden, ptr(self.x), s), "embed")
+        for li, (L, P) in enumerate(zip(self.layers, plan["layers"])):
+            chk(L_.card_rmsnorm(ptr(self.x), ptr(L["attn_norm"]), c.hidden, c.rms_eps, ptr(dM), mm, None,
+                                ptr(self.h), self.code, s), "rmsnorm")
+            P["qkv"].run(dM)
+            chk(L_.card_rope_kv(ptr(self.qkv), ptr(dM), mm, ptr(rows.pos), ptr(rows.slot), ptr(self.cos),
+                                ptr(self.sin), c.n_heads, c.n_kv_heads, hd, ptr(self.q), ptr(self.k_cache[li]),
+                                ptr(self.v_cache[li]), self.code, s), "rope_kv")
+            chk(L_.card_attention(ptr(self.q), ptr(dM), mm, ptr(rows.plen), ptr(rows.n_extra), ptr(rows.extra),
+                                  rows.extra_max, ptr(self.k_cache[li]), ptr(self.v_cache[li]), self.code,
+                                  c.n_heads, c.n_kv_heads, hd, self.prefix_slots, ptr(self.work), ptr(self.o),
+                                  self.code, s), "attention")
+            P["o"].run(dM)
+            chk(L_.card_rmsnorm(ptr(self.x), ptr(L["mlp_norm"]), c.hidden, c.rms_eps, ptr(dM), mm, None,
+                                ptr(self.h), self.code, s), "rmsnorm")
+            P["gu"].run(dM)
+            P["d"].run(dM)
+        chk(L_.card_rmsnorm(ptr(self.x), ptr(self.norm), c.hidden, c.rms_eps, ptr(dOut), mm, ptr(rows.out_rows),
+                            ptr(self.hf), self.code, s), "final norm")
+        plan["lm_head"].run(dOut)
+
+    def launches_per_forward(self) -> int:
+        gu_extra = 0
+        return 2 + self.cfg.n_layers * (2 + 1 + 1 + 3 + 1 + 1 + 1 + gu_extra) + 2
+
+
+class RowBlock:
+    """Device row descriptors (see csrc/card_llm.h CardRows): one int32 block
+    [M, n_out, tok, pos, slot, plen, n_extra, out_rows, extra]."""
+
+    def __init__(self, rows_max: int, extra_max: int, device):
+        self.rows_max = rows_max
+        self.extra_max = extra_max
+        R = rows_max
+        self.block = torch.zeros(2 + 6 * R + R * extra_max, dtype=torch.int32, device=device)
+        b = self.block
+        self.M = b[0:1]
+        self.n_out = b[1:2]
+        self.tok = b[2:2 + R]
+        self.pos = b[2 + R:2 + 2 * R]
+        self.slot = b[2 + 2 * R:2 + 3 * R]
+        self.plen = b[2 + 3 * R:2 + 4 * R]
+        self.n_extra = b[2 + 4 * R:2 + 5 * R]
+        self.out_rows = b[2 + 5 * R:2 + 6 * R]
+        self.extra = b[2 + 6 * R:]
+
+    def set_chain(self, tokens, start_pos: int, out_last_only=True):
+        """Host helper: causal chain rows (prefill / AR decode)."""
+        n = len(tokens)
+        assert n <= self.rows_max
+        host = torch.zeros(2 + 6 * self.rows_max, dtype=torch.int32)
+        R = self.rows_max
+        host[0] = n
+        host[1] = 1 if out_last_only else n
+        host[2:2 + n] = torch.tensor(tokens, dtype=torch.int32)
+        pos = torch.arange(start_pos, start_pos + n, dtype=torch.int32)
+        host[2 + R:2 + R + n] = pos
+        host[2 + 2 * R:2 + 2 * R + n] = pos
+        host[2 + 3 * R:2 + 3 * R + n] = pos + 1
+        if out_last_only:
+            host[2 + 5 * R] = n - 1
+        else:
+            host[2 + 5 * R:2 + 5 * R + n] = torch.arange(n, dtype=torch.int32)
+        self.block[: 2 + 6 * R].copy_(host, non_blocking=False)

@@ -58,7 +58,8 @@ def test_log_exp_correctly_rounded(card):
     assert lib().card_exp_cr(ptr(e), ptr(y), e.numel(), stream_ptr()) == 0
     got = y.cpu().numpy()
     want = np.array([O.cr_exp(float(v)) for v in es])
-    assert np.array_equal(got, want)
+    bad = np.flatnonzero(got != want)
+    assert bad.size == 0, [(es[i], got[i], want[i]) for i in bad[:8]]
 
 
 # ------------------------------------------------------------ operator plug-in
@@ -218,7 +219,7 @@ def test_advance_root_and_reset(card):
     d = np.array([[0.5, 0.3, 0.2]])
     cache.expand_layer(d)
     twin.expand(d)
-    d2 = np.array([[0.6, 0.4, 0.0], [0.1, 0.1, 0.8], [0.3, 0.3, 0.4]])
+    d2 = np.array([[0.6, 0.4, 0.0], [0.1, 0.1, 0.8]])
     cache.expand_layer(d2)
     twin.expand(d2)
     assert cache.advance_root([0], 0) == twin.advance_root([0], 0)

@@ -1,0 +1,75 @@
+"""Pin the CPU transformer oracle (oracle/llama_ref.py) against HF
+transformers' LlamaForCausalLM on identical random-init weights.  CPU only."""
+
+import pytest
+import torch
+
+from oracle.llama_ref import RefLlama
+
+
+def _cfgs():
+    from paper_2508_04462_b200.llama import LlamaConfig
+
+    scaled = dict(factor=8.0, low_freq_factor=1.0, high_freq_factor=4.0, original_max_position_embeddings=64)
+    return [LlamaConfig(96, 64, 2, 4, 2, 16, 128, 10000.0, 1e-5, False, False, None),
+            LlamaConfig(96, 64, 2, 4, 1, 16, 128, 500000.0, 1e-5, True, False, scaled)]
+
+
+def _hf_model(cfg, w):
+    transformers = pytest.importorskip("transformers")
+    kw = dict(vocab_size=cfg.vocab_size, hidden_size=cfg.hidden, intermediate_size=cfg.ffn,
+              num_hidden_layers=cfg.n_layers, num_attention_heads=cfg.n_heads, num_key_value_heads=cfg.n_kv_heads,
+              head_dim=cfg.head_dim, rms_norm_eps=cfg.rms_eps, tie_word_embeddings=cfg.tie_embeddings,
+              max_position_embeddings=512)
+    rp = {"rope_type": "default", "rope_theta": cfg.rope_theta}
+    if cfg.rope_scaling:
+        rp = {"rope_type": "llama3", "rope_theta": cfg.rope_theta, **cfg.rope_scaling}
+    try:
+        hc = transformers.LlamaConfig(**kw, rope_parameters=rp)
+    except TypeError:
+        hc = transformers.LlamaConfig(**kw, rope_theta=cfg.rope_theta, rope_scaling=cfg.rope_scaling)
+    m = transformers.LlamaForCausalLM(hc).eval()
+    sd = {"model.embed_tokens.weight": w["embed"], "model.norm.weight": w["norm"], "lm_head.weight": w["lm_head"]}
+    for i in range(cfg.n_layers):
+        p, q = f"l{i}.", f"model.layers.{i}."
+        sd[q + "self_attn.q_proj.weight"] = w[p + "wq"]
+        sd[q + "self_attn.k_proj.weight"] = w[p + "wk"]
+        sd[q + "self_attn.v_proj.weight"] = w[p + "wv"]
+        sd[q + "self_attn.o_proj.weight"] = w[p + "wo"]
+        sd[q + "mlp.gate_proj.weight"] = w[p + "wg"]
+        sd[q + "mlp.up_proj.weight"] = w[p + "wu"]
+        sd[q + "mlp.down_proj.weight"] = w[p + "wd"]
+        sd[q + "input_layernorm.weight"] = w[p + "attn_norm"]
+        sd[q + "post_attention_layernorm.weight"] = w[p + "mlp_norm"]
+    m.load_state_dict(sd, strict=False)
+    return m
+
+
+@pytest.mark.parametrize("which", [0, 1])
+def test_ref_llama_matches_hf(which):
+    from paper_2508_04462_b200.llama import init_weights
+
+    cfg = _cfgs()[which]
+    w = init_weights(cfg, seed=7)
+    w = {k: (v * 20 if k[0] == "l" and k[1].isdigit() and "norm" not in k else v) for k, v in w.items()}
+    ref = RefLlama(cfg, w)
+    toks = torch.randint(0, cfg.vocab_size, (1, 150), generator=torch.Generator().manual_seed(1))
+    with torch.no_grad():
+        hf = _hf_model(cfg, w)(toks).logits[0]
+        ours = ref.full_logits(toks[0].tolist())
+    assert torch.allclose(ours, hf, rtol=1e-4, atol=1e-4), (ours - hf).abs().max()
+
+
+def test_ref_llama_incremental_equals_full():
+    from paper_2508_04462_b200.llama import init_weights
+
+    cfg = _cfgs()[0]
+    w = init_weights(cfg, seed=3)
+    ref = RefLlama(cfg, w)
+    toks = list(range(5, 45))
+    full = ref.full_logits(toks)
+    inc = RefLlama(cfg, w)
+    for n in (10, 25, 40):
+        assert torch.allclose(inc.logits_for(toks[:n]), full[n - 1], atol=1e-5)
+    branch = toks[:20] + [7, 8]
+    assert torch.allclose(inc.logits_for(branch), RefLlama(cfg, w).full_logits(branch)[-1], atol=1e-5)
