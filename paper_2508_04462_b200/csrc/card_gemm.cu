@@ -502,9 +502,12 @@ struct card_linear {
 
 namespace card {
 
+// The attribute is per kernel, not per plan: always allow the full 227 KB so
+// plans of different Mpad (hence smem) can share one template instance.
 template <int EPI>
 static cudaError_t set_tc_attr(int smem) {
-    return cudaFuncSetAttribute(tc_gemm_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    (void)smem;
+    return cudaFuncSetAttribute(tc_gemm_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
 }
 
 // Split choice: minimise (waves x k-blocks per item) + fixup traffic.
