@@ -164,9 +164,11 @@ typedef struct card_linear card_linear;
 
 /* Y[M,N] = X[M,K] . W[N,K]^T with a fused epilogue (0 store f32, 1 residual
  * add f32, 2 store bf16, 3 SwiGLU -> bf16 with gate/up rows interleaved per
- * 128-row tile).  bf16 weights: tcgen05 + TMA kernel (m_max >= 2) or the
- * 128-bit-load GEMV (m_max == 1); fp32 weights: parity kernel.  X must hold
- * round_up(m_max, 16) rows.  bias: optional fp32 [N]. */
+ * 128-row tile).  wdtype: 0 bf16 row-major (tcgen05 + tensor-map TMA for
+ * m_max >= 2, 128-bit-load GEMV for m_max == 1), 1 fp32 (parity kernel),
+ * 2 bf16 pre-tiled [N/128][K/64][128x64] blocks in SWIZZLE_128B order
+ * (card_tile_weights; one contiguous 16 KB bulk copy per pipeline stage).
+ * X must hold round_up(m_max, 16) rows.  bias: optional fp32 [N]. */
 int card_linear_create(const void* W, int N, int K, int wdtype, const void* X, int m_max, int epi,
                        void* out, int ldo, const float* bias, card_linear** out_h);
 int card_linear_run(card_linear* h, const int32_t* dM, void* stream);
@@ -187,10 +189,13 @@ int card_attention(const float* q, const int32_t* dM, int m_max, const int32_t* 
                    void* o, int odtype, void* stream);
 /* draft lm_head epilogue: per-row top-k by (logit desc, token asc) with
  * log-probs logit/T - logsumexp (replaces extension_pool's rows_topk+log). */
+int card_lmhead_work_floats(int m_max, int k);
 int card_topk_logits(const float* logits, const int32_t* dM, int m_max, int V, int k, double inv_temp,
-                     int32_t* out_tok, double* out_logp, int32_t* out_cnt, void* stream);
-/* target greedy: first maximum per row (verify.py:38-40) */
-int card_argmax_logits(const float* logits, const int32_t* dM, int m_max, int V, int32_t* out, void* stream);
+                     int32_t* out_tok, double* out_logp, int32_t* out_cnt, float* work, void* stream);
+/* target greedy: first maximum per row (verify.py:38-40); vocab split over
+ * CTAs, merged in a second launch.  work: card_lmhead_work_floats floats. */
+int card_argmax_logits(const float* logits, const int32_t* dM, int m_max, int V, int32_t* out, float* work,
+                       void* stream);
 int card_softmax64(const float* logits, const int32_t* dM, int m_max, int V, double inv_temp, double* out,
                    void* stream);
 /* agreement knob: logits[r] += sharpness * (u1 + mix_weight * u2), u the

@@ -62,8 +62,9 @@ SIGNATURES = {
     "card_attention_work_floats": (c_int, [c_int, c_int, c_int, c_int]),
     "card_attention": (c_int, [_P, _P, c_int, _P, _P, _P, c_int, _P, _P, c_int, c_int, c_int, c_int, c_int, _P,
                                _P, c_int, _P]),
-    "card_topk_logits": (c_int, [_P, _P, c_int, c_int, c_int, c_double, _P, _P, _P, _P]),
-    "card_argmax_logits": (c_int, [_P, _P, c_int, c_int, _P, _P]),
+    "card_lmhead_work_floats": (c_int, [c_int, c_int]),
+    "card_topk_logits": (c_int, [_P, _P, c_int, c_int, c_int, c_double, _P, _P, _P, _P, _P]),
+    "card_argmax_logits": (c_int, [_P, _P, c_int, c_int, _P, _P, _P]),
     "card_softmax64": (c_int, [_P, _P, c_int, c_int, c_double, _P, _P]),
     "card_logit_bias": (c_int, [_P, _P, c_int, c_int, _P, c_int, c_int, c_uint64, c_uint64, ctypes.c_float,
                                 ctypes.c_float, _P]),
@@ -92,6 +93,39 @@ class EngineState(ctypes.Structure):
         ("committed_now", c_int32 * 72), ("rec_depth", c_int32), ("rec_alive", c_int32), ("spare", c_int32 * 6)]
 
 
+# kernels launched per C-ABI call (for the bench's gpu_launches count)
+LAUNCHES = {
+    "card_kgram_dist": 1, "card_rows_topk": 1, "card_log_cr": 1, "card_exp_cr": 1,
+    "card_cache_reset": 2, "card_cache_expand": 2, "card_cache_expand_topk": 1, "card_cache_pool": 2,
+    "card_cache_query": 1, "card_cache_correct": 1, "card_cache_advance_root": 1, "card_cache_count_alive": 1,
+    "card_cache_clear_status": 1, "card_embed": 1, "card_rmsnorm": 1, "card_rope_kv": 1, "card_attention": 3,
+    "card_topk_logits": 2, "card_argmax_logits": 2, "card_softmax64": 1, "card_logit_bias": 1,
+    "card_draft_rows": 1, "card_target_rows": 1, "card_eos_fix": 1, "card_record_width": 1,
+    "card_verify_argmax": 1, "card_verify_probs": 1, "card_commit": 1, "card_draft_promote": 2,
+    "card_kv_compact": 2, "card_cycle_end": 1,
+}
+launch_count = [0]
+
+
+class _Counted:
+    """Proxy over the CDLL that tallies kernel launches per call."""
+
+    def __init__(self, handle):
+        self._h = handle
+
+    def __getattr__(self, name):
+        fn = getattr(self._h, name)
+        n = LAUNCHES.get(name)
+        if not n:
+            return fn
+
+        def call(*args):
+            launch_count[0] += n
+            return fn(*args)
+
+        return call
+
+
 def lib():
     """Load (once) and return the ctypes handle; raises DeviceError if absent."""
     global _lib
@@ -110,8 +144,14 @@ def lib():
         fn.argtypes = args
     if handle.card_engine_state_bytes() != ctypes.sizeof(EngineState):
         raise DeviceError("EngineState layout does not match the library")
-    _lib = handle
-    return handle
+    _lib = _Counted(handle)
+    return _lib
+
+
+def raw():
+    """The underlying CDLL (symbol introspection)."""
+    lib()
+    return _lib._h
 
 
 def exported_symbols() -> list[str]:

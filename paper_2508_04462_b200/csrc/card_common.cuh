@@ -172,6 +172,40 @@ __device__ __forceinline__ double log_cr(double x) {
     return __dadd_rn(y0, t);
 }
 
+// ---------------------------------------------------------------- PDL
+// Programmatic dependent launch: kernels launched with launch_pdl may start
+// (prologue, weight prefetch) while their predecessor drains; they must call
+// pdl_wait() before reading anything the predecessor wrote.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+bool pdl_enabled();
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                             Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
+#define CARD_PDL(kern, grid, block, smem, stream, ...)                        \
+    do {                                                                      \
+        cudaError_t _e = card::launch_pdl(kern, grid, block, smem, stream, __VA_ARGS__); \
+        if (_e != cudaSuccess) {                                              \
+            card::set_cuda_error(_e);                                         \
+            return CARD_E_CUDA;                                               \
+        }                                                                     \
+    } while (0)
+
 // ---------------------------------------------------------------- misc
 __device__ __forceinline__ int warp_id() { return threadIdx.x >> 5; }
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }

@@ -60,6 +60,14 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
         "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
         : "memory");
 }
+// 1-D bulk copy (TMA engine, no tensor map): weights are pre-tiled in HBM so
+// each pipeline stage is one contiguous 16 KB block already in SW128 order.
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
 __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* map) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
 }
@@ -100,6 +108,8 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
 
 __device__ __forceinline__ float silu(float x) { return x / (1.0f + __expf(-x)); }
 
+struct TcArgs;
+
 // ---------------------------------------------------------------- tcgen05 GEMM
 constexpr int kTileN = 128;   // weight rows per tile (MMA M)
 constexpr int kBK = 64;       // bf16 K per stage = one 128-byte swizzle atom
@@ -109,6 +119,7 @@ constexpr int kTcThreads = 192;   // warps 0-3 epilogue, 4 TMA producer, 5 MMA i
 struct TcArgs {
     int N, K, kb_total, n_tiles, splits, items, Mpad, stages, tmem_cols, n_acc_buf;
     const int32_t* dM;
+    const uint8_t* w_tiled;   // non-null: [n_tiles][kb_total][128 x 128 B] pre-swizzled blocks
     int epi;
     float* out_f32;
     __nv_bfloat16* out_bf16;
@@ -118,40 +129,58 @@ struct TcArgs {
     int32_t* counters;
 };
 
+// Epilogue for one 16-column chunk (tokens m0..m0+mc) of output row n_glob.
+// All loads of a chunk are issued before any store so they overlap.
 template <int EPI>
-__device__ __forceinline__ void epi_store(const TcArgs& a, int n_glob, int n_local, int m, float v, float* xch) {
-    if (a.bias) v += a.bias[n_glob];
-    if (EPI == EPI_STORE_F32) {
-        a.out_f32[(int64_t)m * a.ldo + n_glob] = v;
-    } else if (EPI == EPI_RESID_F32) {
-        float* p = a.out_f32 + (int64_t)m * a.ldo + n_glob;
-        *p = *p + v;
-    } else if (EPI == EPI_STORE_BF16) {
-        a.out_bf16[(int64_t)m * a.ldo + n_glob] = __float2bfloat16(v);
+__device__ __forceinline__ void epi_chunk(const TcArgs& a, int tile, int n_glob, int n_local, int m0, int mc,
+                                          float* v, float* xch) {
+    const float b = a.bias ? a.bias[n_glob] : 0.f;
+    if (EPI == EPI_SWIGLU_BF16) {
+        // rows [0,64) of a tile are gates, [64,128) the matching ups (xch: [16][64])
+        if (n_local >= 64)
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+                if (j < mc) xch[j * 64 + (n_local - 64)] = v[j] + b;
+        named_bar(1, kEpiThreads);
+        if (n_local < 64) {
+            const int f = tile * 64 + n_local;
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+                if (j < mc) {
+                    const float g = v[j] + b, u = xch[j * 64 + n_local];
+                    a.out_bf16[(int64_t)(m0 + j) * a.ldo + f] = __float2bfloat16(silu(g) * u);
+                }
+        }
+        named_bar(1, kEpiThreads);
+        return;
+    }
+    if (EPI == EPI_RESID_F32) {
+        float old[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) old[j] = j < mc ? a.out_f32[(int64_t)(m0 + j) * a.ldo + n_glob] : 0.f;
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+            if (j < mc) a.out_f32[(int64_t)(m0 + j) * a.ldo + n_glob] = old[j] + (v[j] + b);
+        return;
+    }
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        if (j >= mc) break;
+        if (EPI == EPI_STORE_F32) a.out_f32[(int64_t)(m0 + j) * a.ldo + n_glob] = v[j] + b;
+        else a.out_bf16[(int64_t)(m0 + j) * a.ldo + n_glob] = __float2bfloat16(v[j] + b);
     }
 }
 
-// SwiGLU exchange: rows [0,64) of a tile are gates, [64,128) the matching ups.
-__device__ __forceinline__ void epi_swiglu_chunk(const TcArgs& a, int tile, int n_local, int m0, int mcount,
-                                                 const float* v, float* xch) {
-    // xch: [16][64] floats
-    if (n_local >= 64)
-        for (int j = 0; j < mcount; ++j) xch[j * 64 + (n_local - 64)] = v[j];
-    named_bar(1, kEpiThreads);
-    if (n_local < 64) {
-        const int f = tile * 64 + n_local;
-        for (int j = 0; j < mcount; ++j) {
-            const float g = v[j], u = xch[j * 64 + n_local];
-            a.out_bf16[(int64_t)(m0 + j) * a.ldo + f] = __float2bfloat16(silu(g) * u);
-        }
-    }
-    named_bar(1, kEpiThreads);
+// gpu-scope release/acquire add on the per-tile split counter
+__device__ __forceinline__ int atom_add_acq_rel(int* p, int v) {
+    int old;
+    asm volatile("atom.add.acq_rel.gpu.global.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
 }
 
 template <int EPI>
 __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_constant__ CUtensorMap tmW,
                                                                const __grid_constant__ CUtensorMap tmX, TcArgs a) {
-    if (*a.dM <= 0) return;   // nothing to do this step (graph replays with zero rows)
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1024-byte alignment for SWIZZLE_128B atoms
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -191,28 +220,68 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    // Weights do not depend on the previous kernel: the producer streams the
+    // first pipeline stages of weights before waiting on the grid dependency.
+    int pre = 0;
+    if (warp == 4 && lane == 0 && a.w_tiled) {
+        const int item = blockIdx.x;
+        if (item < a.items) {
+            const int tile = item / a.splits, split = item % a.splits;
+            const int kb0 = (int)((int64_t)a.kb_total * split / a.splits);
+            const int kb1 = (int)((int64_t)a.kb_total * (split + 1) / a.splits);
+            pre = (kb1 - kb0) < a.stages ? (kb1 - kb0) : a.stages;
+            for (int i = 0; i < pre; ++i) {
+                mbar_expect_tx(&full[i], bytesA + bytesB);
+                bulk_load(sA + (size_t)i * bytesA, a.w_tiled + ((size_t)tile * a.kb_total + kb0 + i) * (size_t)bytesA,
+                          bytesA, &full[i]);
+            }
+        }
+    }
+    pdl_wait();
+    pdl_trigger();
     const int M = *a.dM;
     const int m_rt = M < 1 ? 1 : M;
     const int n_mma = ((m_rt + 15) / 16) * 16;   // runtime MMA N (tokens), <= Mpad
 
-    if (warp == 4) {
+    if (M <= 0) {
+        // zero-row replay: drain the prefetched stages, then leave
+        if (warp == 4 && lane == 0)
+            for (int i = 0; i < pre; ++i) {
+                tma_load_2d(sB + (size_t)i * bytesB, &tmX, &full[i], 0, 0);
+                mbar_wait(&full[i], 0);
+            }
+    } else if (warp == 4) {
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
+            bool first = true;
             for (int item = blockIdx.x; item < a.items; item += gridDim.x) {
                 const int tile = item / a.splits, split = item % a.splits;
                 const int kb0 = (int)((int64_t)a.kb_total * split / a.splits);
                 const int kb1 = (int)((int64_t)a.kb_total * (split + 1) / a.splits);
                 for (int kb = kb0; kb < kb1; ++kb) {
+                    if (first && kb - kb0 < pre) {   // weights already in flight
+                        tma_load_2d(sB + (size_t)stage * bytesB, &tmX, &full[stage], kb * kBK, 0);
+                        if (++stage == S) {
+                            stage = 0;
+                            phase ^= 1;
+                        }
+                        continue;
+                    }
                     mbar_wait(&empty[stage], phase ^ 1);
                     mbar_expect_tx(&full[stage], bytesA + bytesB);
-                    tma_load_2d(sA + (size_t)stage * bytesA, &tmW, &full[stage], kb * kBK, tile * kTileN);
+                    if (a.w_tiled)
+                        bulk_load(sA + (size_t)stage * bytesA,
+                                  a.w_tiled + ((size_t)tile * a.kb_total + kb) * (size_t)bytesA, bytesA, &full[stage]);
+                    else
+                        tma_load_2d(sA + (size_t)stage * bytesA, &tmW, &full[stage], kb * kBK, tile * kTileN);
                     tma_load_2d(sB + (size_t)stage * bytesB, &tmX, &full[stage], kb * kBK, 0);
                     if (++stage == S) {
                         stage = 0;
                         phase ^= 1;
                     }
                 }
+                first = false;
             }
         }
     } else if (warp == 5) {
@@ -263,7 +332,20 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
         for (int item = blockIdx.x; item < a.items; item += gridDim.x) {
             const int tile = item / a.splits;
             const int n_glob = tile * kTileN + n_local;
-            mbar_wait(&tfull[acc], acc_phase);
+            // epilogue warps poll politely: they must not steal issue slots
+            // from the producer / MMA threads of this SM
+            while (true) {
+                uint32_t ok;
+                asm volatile(
+                    "{\n\t.reg .pred P;\n\t"
+                    "mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n\t"
+                    "selp.u32 %0, 1, 0, P;\n\t}"
+                    : "=r"(ok)
+                    : "r"(smem_u32(&tfull[acc])), "r"(acc_phase)
+                    : "memory");
+                if (ok) break;
+                __nanosleep(128);
+            }
             tc_fence_after();
             const uint32_t trow = tmem_base + ((uint32_t)(warp * 32) << 16) + (uint32_t)(acc * a.Mpad);
             const bool direct = a.splits == 1;
@@ -273,13 +355,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
                 tmem_ld16(trow + (uint32_t)m0, v);
                 const int mc = (M - m0) < 16 ? (M - m0) : 16;
                 if (direct) {
-                    if (EPI == EPI_SWIGLU_BF16) {
-                        epi_swiglu_chunk(a, tile, n_local, m0, mc, v, xch);
-                    } else {
-                        for (int j = 0; j < mc; ++j) epi_store<EPI>(a, n_glob, n_local, m0 + j, v[j], xch);
-                    }
+                    epi_chunk<EPI>(a, tile, n_glob, n_local, m0, mc, v, xch);
                 } else {
-                    for (int j = 0; j < mc; ++j) wsp[(size_t)(m0 + j) * kTileN + n_local] = v[j];
+#pragma unroll
+                    for (int j = 0; j < 16; ++j)
+                        if (j < mc) __stcg(wsp + (size_t)(m0 + j) * kTileN + n_local, v[j]);
                 }
             }
             tc_fence_before();
@@ -292,32 +372,31 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
                 acc_phase ^= 1;
             }
             if (!direct) {
-                // deterministic split-K fixup: last arriver sums splits 0..S-1 in order
-                __threadfence();
+                // deterministic split-K fixup: the last arriver sums splits 0..S-1 in order.
+                // bar.sync orders this CTA's partial stores before thread 0's release.
                 named_bar(1, kEpiThreads);
                 if (n_local == 0) {
-                    const int prev = atomicAdd(&a.counters[tile], 1);
+                    const int prev = atom_add_acq_rel(&a.counters[tile], 1);
                     *sh_last = (prev == a.splits - 1);
                     if (prev == a.splits - 1) a.counters[tile] = 0;   // reusable next launch / graph replay
                 }
                 named_bar(1, kEpiThreads);
                 if (*sh_last) {
-                    __threadfence();
                     const float* base = a.ws + (size_t)tile * a.splits * kTileN * a.Mpad;
                     for (int m0 = 0; m0 < M; m0 += 16) {
                         const int mc = (M - m0) < 16 ? (M - m0) : 16;
                         float v[16];
-                        for (int j = 0; j < mc; ++j) {
-                            float s = 0.f;
-                            for (int sp = 0; sp < a.splits; ++sp)
-                                s += __ldcg(base + ((size_t)sp * a.Mpad + (m0 + j)) * kTileN + n_local);
-                            v[j] = s;
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) v[j] = 0.f;
+                        for (int sp = 0; sp < a.splits; ++sp) {
+                            const float* p = base + ((size_t)sp * a.Mpad + m0) * kTileN + n_local;
+                            float t[16];
+#pragma unroll
+                            for (int j = 0; j < 16; ++j) t[j] = j < mc ? __ldcg(p + (size_t)j * kTileN) : 0.f;
+#pragma unroll
+                            for (int j = 0; j < 16; ++j) v[j] += t[j];
                         }
-                        if (EPI == EPI_SWIGLU_BF16) {
-                            epi_swiglu_chunk(a, tile, n_local, m0, mc, v, xch);
-                        } else {
-                            for (int j = 0; j < mc; ++j) epi_store<EPI>(a, n_glob, n_local, m0 + j, v[j], xch);
-                        }
+                        epi_chunk<EPI>(a, tile, n_glob, n_local, m0, mc, v, xch);
                     }
                 }
             }
@@ -331,6 +410,19 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
     }
 }
 
+template <int EPI>
+__device__ __forceinline__ void epi_store(const TcArgs& a, int n_glob, int n_local, int m, float v, float* xch) {
+    if (a.bias) v += a.bias[n_glob];
+    if (EPI == EPI_STORE_F32) {
+        a.out_f32[(int64_t)m * a.ldo + n_glob] = v;
+    } else if (EPI == EPI_RESID_F32) {
+        float* p = a.out_f32 + (int64_t)m * a.ldo + n_glob;
+        *p = *p + v;
+    } else if (EPI == EPI_STORE_BF16) {
+        a.out_bf16[(int64_t)m * a.ldo + n_glob] = __float2bfloat16(v);
+    }
+}
+
 // ---------------------------------------------------------------- M == 1 GEMV (bf16)
 // One warp per 2 output rows; each lane streams 16-byte chunks (8 bf16) of
 // the weight rows with ld.global.nc.L1::no_allocate, x cached in smem.
@@ -338,6 +430,8 @@ template <int EPI>
 __global__ void __launch_bounds__(256) gemv_bf16_kernel(const __nv_bfloat16* __restrict__ W,
                                                         const __nv_bfloat16* __restrict__ X, int N, int K,
                                                         TcArgs a) {
+    pdl_wait();     // predecessor outputs visible from here
+    pdl_trigger();  // let the next kernel start its prologue
     if (*a.dM <= 0) return;
     extern __shared__ __align__(16) uint8_t smem_raw[];
     __nv_bfloat16* xs = (__nv_bfloat16*)smem_raw;
@@ -397,6 +491,8 @@ __global__ void __launch_bounds__(256) gemv_bf16_kernel(const __nv_bfloat16* __r
 // first (EPI_STORE_F32), then combined here.
 __global__ void swiglu_from_rows_kernel(const float* __restrict__ rows, const int32_t* dM, int N, __nv_bfloat16* out,
                                         int ldo) {
+    pdl_wait();     // predecessor outputs visible from here
+    pdl_trigger();  // let the next kernel start its prologue
     const int M = *dM < 1 ? 0 : 1;
     const int F = N / 2;
     for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < M * F; idx += gridDim.x * blockDim.x) {
@@ -413,6 +509,8 @@ __global__ void swiglu_from_rows_kernel(const float* __restrict__ rows, const in
 template <int EPI>
 __global__ void __launch_bounds__(256) f32_gemm_kernel(const float* __restrict__ W, const float* __restrict__ X,
                                                        int N, int K, TcArgs a) {
+    pdl_wait();     // predecessor outputs visible from here
+    pdl_trigger();  // let the next kernel start its prologue
     const int M = *a.dM;
     const int lane = lane_id();
     const int n = blockIdx.x * (blockDim.x >> 5) + warp_id();
@@ -434,6 +532,8 @@ __global__ void __launch_bounds__(256) f32_gemm_kernel(const float* __restrict__
 }
 
 __global__ void swiglu_f32_kernel(const float* __restrict__ rows, const int32_t* dM, int N, float* out, int ldo) {
+    pdl_wait();     // predecessor outputs visible from here
+    pdl_trigger();  // let the next kernel start its prologue
     const int M = *dM;
     const int F = N / 2;
     for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < M * F; idx += gridDim.x * blockDim.x) {
@@ -510,25 +610,18 @@ static cudaError_t set_tc_attr(int smem) {
     return cudaFuncSetAttribute(tc_gemm_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
 }
 
-// Split choice: minimise (waves x k-blocks per item) + fixup traffic.
+// Split choice (calibrated on B200 with tools/split_sweep.sh): a work item
+// carries a large fixed cost (~9 us: pipeline ramp, TMEM drain, fixup), so
+// items should be long — just enough of them to cover ~80% of the resident
+// CTA slots — and the split partial traffic (write + read, 2*128*Mpad*4 B
+// per split) must stay <= 1/4 of the tile's weight bytes (128*K*2 B).
 static int choose_splits(int n_tiles, int kb_total, int Mpad, int slots) {
-    double best = 1e30;
-    int best_s = 1;
-    for (int s = 1; s <= 32 && s <= kb_total; ++s) {
-        const int items = n_tiles * s;
-        const int waves = (items + slots - 1) / slots;
-        const int kb_item = (kb_total + s - 1) / s;
-        double t = (double)waves * kb_item;   // in k-block times
-        if (s > 1) {
-            // partial write + read back: 2 * 128*Mpad*4 bytes per item vs 16 KB per k-block
-            t += (double)waves * (2.0 * kTileN * Mpad * 4) / (kTileN * kBK * 2);
-        }
-        if (t < best - 1e-9) {
-            best = t;
-            best_s = s;
-        }
-    }
-    return best_s;
+    int s = (int)(0.8 * slots / n_tiles + 0.5);
+    int max_s = (kb_total * kBK) / (16 * Mpad);
+    if (s > max_s) s = max_s;
+    if (s > kb_total) s = kb_total;
+    if (s > 32) s = 32;
+    return s < 1 ? 1 : s;
 }
 
 }  // namespace card
@@ -555,6 +648,8 @@ int card_linear_create(const void* W, int N, int K, int wdtype, const void* X, i
     a.ldo = ldo;
     if (epi == EPI_STORE_BF16 || epi == EPI_SWIGLU_BF16) a.out_bf16 = (__nv_bfloat16*)out;
     else a.out_f32 = (float*)out;
+    const bool tiled = (wdtype == 2);
+    if (tiled) a.w_tiled = (const uint8_t*)W;
     if (wdtype == 1) {   // fp32 parity path
         h->kind = 2;
         a.out_f32 = (float*)out;
@@ -572,7 +667,7 @@ int card_linear_create(const void* W, int N, int K, int wdtype, const void* X, i
         free(h);
         return CARD_E_CONFIG;
     }
-    if (m_max == 1) {   // decode GEMV
+    if (m_max == 1 && !tiled) {   // decode GEMV over row-major weights
         h->kind = 1;
         if (epi == EPI_SWIGLU_BF16) {
             CARD_CUDA_TRY(cudaMalloc(&h->scratch, (size_t)N * 4));
@@ -605,7 +700,8 @@ int card_linear_create(const void* W, int N, int K, int wdtype, const void* X, i
     int cols = 32;
     while (cols < a.n_acc_buf * Mpad) cols <<= 1;
     a.tmem_cols = cols;
-    const int ctas_per_sm = (cols <= 256) ? 2 : 1;
+    int ctas_per_sm = (cols <= 256) ? 2 : 1;
+    if (getenv("CARD_CTAS_PER_SM")) ctas_per_sm = atoi(getenv("CARD_CTAS_PER_SM"));   // tuning knob
     const int stage_bytes = kTileN * kBK * 2 + Mpad * kBK * 2;
     const int budget = (ctas_per_sm == 2 ? 110 : 220) * 1024;
     const int extra = 1024 + 64 * 8 + 16 * 64 * 4 + 64;
@@ -616,6 +712,7 @@ int card_linear_create(const void* W, int N, int K, int wdtype, const void* X, i
     h->smem = stages * stage_bytes + extra;
     const int slots = num_sms() * ctas_per_sm;
     a.splits = choose_splits(a.n_tiles, a.kb_total, Mpad, slots);
+    if (getenv("CARD_SPLITS")) a.splits = atoi(getenv("CARD_SPLITS"));   // tuning knob
     a.items = a.n_tiles * a.splits;
     h->grid = a.items < slots ? a.items : slots;
     if (a.splits > 1) {
@@ -623,7 +720,7 @@ int card_linear_create(const void* W, int N, int K, int wdtype, const void* X, i
         CARD_CUDA_TRY(cudaMalloc(&a.counters, (size_t)a.n_tiles * 4));
         CARD_CUDA_TRY(cudaMemset(a.counters, 0, (size_t)a.n_tiles * 4));
     }
-    int rc = make_map_bf16(&h->tmW, W, (uint64_t)N, (uint64_t)K, kTileN, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
+    int rc = tiled ? CARD_OK : make_map_bf16(&h->tmW, W, (uint64_t)N, (uint64_t)K, kTileN, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
     if (!rc) rc = make_map_bf16(&h->tmX, X, (uint64_t)Mpad, (uint64_t)K, (uint32_t)Mpad, CU_TENSOR_MAP_L2_PROMOTION_L2_128B);
     if (rc) {
         free(h);
@@ -653,21 +750,21 @@ int card_linear_run(card_linear* h, const int32_t* dM, void* stream) {
     a.dM = dM;
     if (h->kind == 0) {
         switch (h->epi) {
-            case EPI_STORE_F32: tc_gemm_kernel<EPI_STORE_F32><<<h->grid, kTcThreads, h->smem, s>>>(h->tmW, h->tmX, a); break;
-            case EPI_RESID_F32: tc_gemm_kernel<EPI_RESID_F32><<<h->grid, kTcThreads, h->smem, s>>>(h->tmW, h->tmX, a); break;
-            case EPI_STORE_BF16: tc_gemm_kernel<EPI_STORE_BF16><<<h->grid, kTcThreads, h->smem, s>>>(h->tmW, h->tmX, a); break;
-            case EPI_SWIGLU_BF16: tc_gemm_kernel<EPI_SWIGLU_BF16><<<h->grid, kTcThreads, h->smem, s>>>(h->tmW, h->tmX, a); break;
+            case EPI_STORE_F32: CARD_PDL((tc_gemm_kernel<EPI_STORE_F32>), dim3(h->grid), dim3(kTcThreads), h->smem, s, h->tmW, h->tmX, a); break;
+            case EPI_RESID_F32: CARD_PDL((tc_gemm_kernel<EPI_RESID_F32>), dim3(h->grid), dim3(kTcThreads), h->smem, s, h->tmW, h->tmX, a); break;
+            case EPI_STORE_BF16: CARD_PDL((tc_gemm_kernel<EPI_STORE_BF16>), dim3(h->grid), dim3(kTcThreads), h->smem, s, h->tmW, h->tmX, a); break;
+            case EPI_SWIGLU_BF16: CARD_PDL((tc_gemm_kernel<EPI_SWIGLU_BF16>), dim3(h->grid), dim3(kTcThreads), h->smem, s, h->tmW, h->tmX, a); break;
         }
     } else if (h->kind == 1) {
         const __nv_bfloat16* W = (const __nv_bfloat16*)h->W;
         const __nv_bfloat16* X = (const __nv_bfloat16*)h->X;
         switch (h->epi) {
-            case EPI_STORE_F32: gemv_bf16_kernel<EPI_STORE_F32><<<h->grid, 256, h->smem, s>>>(W, X, h->N, h->K, a); break;
-            case EPI_RESID_F32: gemv_bf16_kernel<EPI_RESID_F32><<<h->grid, 256, h->smem, s>>>(W, X, h->N, h->K, a); break;
-            case EPI_STORE_BF16: gemv_bf16_kernel<EPI_STORE_BF16><<<h->grid, 256, h->smem, s>>>(W, X, h->N, h->K, a); break;
+            case EPI_STORE_F32: CARD_PDL((gemv_bf16_kernel<EPI_STORE_F32>), dim3(h->grid), dim3(256), h->smem, s, W, X, h->N, h->K, a); break;
+            case EPI_RESID_F32: CARD_PDL((gemv_bf16_kernel<EPI_RESID_F32>), dim3(h->grid), dim3(256), h->smem, s, W, X, h->N, h->K, a); break;
+            case EPI_STORE_BF16: CARD_PDL((gemv_bf16_kernel<EPI_STORE_BF16>), dim3(h->grid), dim3(256), h->smem, s, W, X, h->N, h->K, a); break;
             case EPI_SWIGLU_BF16:
-                gemv_bf16_kernel<EPI_STORE_F32><<<h->grid, 256, h->smem, s>>>(W, X, h->N, h->K, a);
-                swiglu_from_rows_kernel<<<(h->N / 2 + 255) / 256, 256, 0, s>>>(h->scratch, dM, h->N, h->args.out_bf16,
+                CARD_PDL((gemv_bf16_kernel<EPI_STORE_F32>), dim3(h->grid), dim3(256), h->smem, s, W, X, h->N, h->K, a);
+                CARD_PDL((swiglu_from_rows_kernel), dim3((h->N / 2 + 255) / 256), dim3(256), 0, s, h->scratch, dM, h->N, h->args.out_bf16,
                                                                              h->N / 2);
                 break;
         }
@@ -675,12 +772,12 @@ int card_linear_run(card_linear* h, const int32_t* dM, void* stream) {
         const float* W = (const float*)h->W;
         const float* X = (const float*)h->X;
         switch (h->epi) {
-            case EPI_STORE_F32: f32_gemm_kernel<EPI_STORE_F32><<<h->grid, 256, 0, s>>>(W, X, h->N, h->K, a); break;
-            case EPI_RESID_F32: f32_gemm_kernel<EPI_RESID_F32><<<h->grid, 256, 0, s>>>(W, X, h->N, h->K, a); break;
-            case EPI_STORE_BF16: f32_gemm_kernel<EPI_STORE_F32><<<h->grid, 256, 0, s>>>(W, X, h->N, h->K, a); break;
+            case EPI_STORE_F32: CARD_PDL((f32_gemm_kernel<EPI_STORE_F32>), dim3(h->grid), dim3(256), 0, s, W, X, h->N, h->K, a); break;
+            case EPI_RESID_F32: CARD_PDL((f32_gemm_kernel<EPI_RESID_F32>), dim3(h->grid), dim3(256), 0, s, W, X, h->N, h->K, a); break;
+            case EPI_STORE_BF16: CARD_PDL((f32_gemm_kernel<EPI_STORE_F32>), dim3(h->grid), dim3(256), 0, s, W, X, h->N, h->K, a); break;
             case EPI_SWIGLU_BF16:
-                f32_gemm_kernel<EPI_STORE_F32><<<h->grid, 256, 0, s>>>(W, X, h->N, h->K, a);
-                swiglu_f32_kernel<<<256, 256, 0, s>>>(h->scratch, dM, h->N, (float*)h->args.out_bf16, h->N / 2);
+                CARD_PDL((f32_gemm_kernel<EPI_STORE_F32>), dim3(h->grid), dim3(256), 0, s, W, X, h->N, h->K, a);
+                CARD_PDL((swiglu_f32_kernel), dim3(256), dim3(256), 0, s, h->scratch, dM, h->N, (float*)h->args.out_bf16, h->N / 2);
                 break;
         }
     }

@@ -51,6 +51,8 @@ __device__ __forceinline__ void stf<__nv_bfloat16>(__nv_bfloat16* p, int64_t i, 
 template <typename W>
 __global__ void embed_kernel(const int32_t* __restrict__ tok, const int32_t* dM, const W* __restrict__ E, int H,
                              float* __restrict__ x) {
+    pdl_wait();     // predecessor outputs visible from here
+    pdl_trigger();  // let the next kernel start its prologue
     const int r = blockIdx.x;
     if (r >= *dM) return;
     const int64_t t = tok[r];
@@ -61,6 +63,8 @@ __global__ void embed_kernel(const int32_t* __restrict__ tok, const int32_t* dM,
 template <typename Y>
 __global__ void rmsnorm_kernel(const float* __restrict__ x, const float* __restrict__ w, int H, float eps,
                                const int32_t* dM, const int32_t* gather, Y* __restrict__ y) {
+    pdl_wait();     // predecessor outputs visible from here
+    pdl_trigger();  // let the next kernel start its prologue
     const int r = blockIdx.x;
     if (r >= *dM) return;
     const int src = gather ? gather[r] : r;
@@ -87,6 +91,8 @@ __global__ void rope_kv_kernel(const float* __restrict__ qkv, const int32_t* dM,
                                const int32_t* __restrict__ slot, const float* __restrict__ cos_t,
                                const float* __restrict__ sin_t, int nh, int nkv, int hd, float qscale,
                                float* __restrict__ q, KV* __restrict__ kc, KV* __restrict__ vc) {
+    pdl_wait();     // predecessor outputs visible from here
+    pdl_trigger();  // let the next kernel start its prologue
     const int r = blockIdx.x;
     if (r >= *dM) return;
     const int half = hd / 2;
@@ -126,6 +132,8 @@ __global__ void __launch_bounds__(256) attn_prefix_kernel(const float* __restric
                                                           const int32_t* __restrict__ plen, const KV* __restrict__ kc,
                                                           const KV* __restrict__ vc, int nh, int nkv, int hd,
                                                           int n_splits, float* __restrict__ work) {
+    pdl_wait();     // predecessor outputs visible from here
+    pdl_trigger();  // let the next kernel start its prologue
     extern __shared__ float sm[];
     const int g = blockIdx.x;          // kv head
     const int sidx = blockIdx.y;       // split
@@ -197,12 +205,180 @@ __global__ void __launch_bounds__(256) attn_prefix_kernel(const float* __restric
     }
 }
 
+
+// ---------------------------------------------------------------- tensor-core prefix attention
+// CTA = (kv head g, 64-key chunk).  The chunk's K (row-major) and V
+// (transposed) are staged once in smem as bf16; every query (row r, head h
+// in g's group) with plen[r] > chunk start is processed in tiles of 16 by
+// mma.sync.m16n8k16 (bf16 in, fp32 acc): S = Q K^T, masked, exp, O = P V.
+// Partials (m, l, o[hd]) go to the same workspace layout as the CUDA-core
+// kernel, merged by attn_combine_kernel.
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+    __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+    return *reinterpret_cast<uint32_t*>(&v);
+}
+__device__ __forceinline__ void mma_bf16_16816(float* c, const uint32_t* a, const uint32_t* b) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+}
+
+template <int HD>
+__global__ void __launch_bounds__(128) attn_prefix_tc_kernel(const float* __restrict__ q, const int32_t* dM,
+                                                            const int32_t* __restrict__ plen,
+                                                            const __nv_bfloat16* __restrict__ kc,
+                                                            const __nv_bfloat16* __restrict__ vc, int nh, int nkv,
+                                                            int n_splits, float* __restrict__ work) {
+    pdl_wait();     // predecessor outputs visible from here
+    pdl_trigger();  // let the next kernel start its prologue
+    constexpr int CH = kChunk;          // 64 keys
+    constexpr int KLD = HD + 8;         // padded K row (bf16)
+    constexpr int VLD = CH + 8;         // padded V^T row (bf16)
+    __shared__ __align__(16) __nv_bfloat16 Ks[CH * KLD];
+    __shared__ __align__(16) __nv_bfloat16 Vt[HD * VLD];
+    __shared__ int need;
+    const int g = blockIdx.x, sidx = blockIdx.y, k0 = sidx * CH;
+    const int M = *dM;
+    if (threadIdx.x == 0) need = 0;
+    __syncthreads();
+    for (int r = threadIdx.x; r < M; r += blockDim.x)
+        if (plen[r] > k0) need = 1;
+    __syncthreads();
+    if (!need) return;
+    // stage K (16-byte vectors) and V^T
+    for (int idx = threadIdx.x; idx < CH * HD / 8; idx += blockDim.x) {
+        const int j = idx / (HD / 8), d8 = (idx % (HD / 8)) * 8;
+        const int64_t base = (((int64_t)(k0 + j)) * nkv + g) * HD + d8;
+        const uint4 kv = *reinterpret_cast<const uint4*>(kc + base);
+        *reinterpret_cast<uint4*>(Ks + j * KLD + d8) = kv;
+        const uint4 vv = *reinterpret_cast<const uint4*>(vc + base);
+        const __nv_bfloat16* ve = reinterpret_cast<const __nv_bfloat16*>(&vv);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) Vt[(d8 + e) * VLD + j] = ve[e];
+    }
+    __syncthreads();
+    const int G = nh / nkv;
+    const int nq = M * G;
+    const int lane = lane_id(), warp = warp_id();
+    const int gq = lane >> 2, tq = lane & 3;
+    for (int tile = warp; tile * 16 < nq; tile += blockDim.x >> 5) {
+        // query rows of this tile handled by this thread: gq and gq + 8
+        int qa = tile * 16 + gq, qb = qa + 8;
+        const int ra = qa < nq ? qa / G : 0, rb = qb < nq ? qb / G : 0;
+        const int ha = g * G + (qa % G), hb = g * G + (qb % G);
+        const int la = qa < nq ? plen[ra] - k0 : 0, lb = qb < nq ? plen[rb] - k0 : 0;
+        const float* qpa = q + ((int64_t)ra * nh + ha) * HD;
+        const float* qpb = q + ((int64_t)rb * nh + hb) * HD;
+        // S = Q K^T over HD in 16-wide slices
+        float s[CH / 8][4];
+#pragma unroll
+        for (int n = 0; n < CH / 8; ++n) s[n][0] = s[n][1] = s[n][2] = s[n][3] = 0.f;
+#pragma unroll
+        for (int ks = 0; ks < HD / 16; ++ks) {
+            const int d0 = ks * 16 + 2 * tq;
+            uint32_t a[4];
+            const float2 xa0 = qa < nq ? *reinterpret_cast<const float2*>(qpa + d0) : make_float2(0.f, 0.f);
+            const float2 xb0 = qb < nq ? *reinterpret_cast<const float2*>(qpb + d0) : make_float2(0.f, 0.f);
+            const float2 xa1 = qa < nq ? *reinterpret_cast<const float2*>(qpa + d0 + 8) : make_float2(0.f, 0.f);
+            const float2 xb1 = qb < nq ? *reinterpret_cast<const float2*>(qpb + d0 + 8) : make_float2(0.f, 0.f);
+            a[0] = pack_bf16(xa0.x, xa0.y);
+            a[1] = pack_bf16(xb0.x, xb0.y);
+            a[2] = pack_bf16(xa1.x, xa1.y);
+            a[3] = pack_bf16(xb1.x, xb1.y);
+#pragma unroll
+            for (int n = 0; n < CH / 8; ++n) {
+                const __nv_bfloat16* kr = Ks + (n * 8 + gq) * KLD + ks * 16 + 2 * tq;
+                uint32_t b[2];
+                b[0] = *reinterpret_cast<const uint32_t*>(kr);
+                b[1] = *reinterpret_cast<const uint32_t*>(kr + 8);
+                mma_bf16_16816(s[n], a, b);
+            }
+        }
+        // mask + row max over the 4 threads sharing a row
+        float ma = -INFINITY, mb = -INFINITY;
+#pragma unroll
+        for (int n = 0; n < CH / 8; ++n) {
+            const int j0 = n * 8 + 2 * tq;
+            if (j0 >= la) s[n][0] = -INFINITY;
+            if (j0 + 1 >= la) s[n][1] = -INFINITY;
+            if (j0 >= lb) s[n][2] = -INFINITY;
+            if (j0 + 1 >= lb) s[n][3] = -INFINITY;
+            ma = fmaxf(ma, fmaxf(s[n][0], s[n][1]));
+            mb = fmaxf(mb, fmaxf(s[n][2], s[n][3]));
+        }
+        ma = fmaxf(ma, __shfl_xor_sync(0xffffffffu, ma, 1));
+        ma = fmaxf(ma, __shfl_xor_sync(0xffffffffu, ma, 2));
+        mb = fmaxf(mb, __shfl_xor_sync(0xffffffffu, mb, 1));
+        mb = fmaxf(mb, __shfl_xor_sync(0xffffffffu, mb, 2));
+        const float sa = ma == -INFINITY ? 0.f : ma, sb = mb == -INFINITY ? 0.f : mb;
+        float suma = 0.f, sumb = 0.f;
+        uint32_t p[CH / 16][4];
+#pragma unroll
+        for (int n = 0; n < CH / 8; ++n) {
+            const float e0 = __expf(s[n][0] - sa), e1 = __expf(s[n][1] - sa);
+            const float e2 = __expf(s[n][2] - sb), e3 = __expf(s[n][3] - sb);
+            suma += e0 + e1;
+            sumb += e2 + e3;
+            // C layout of n-tile n -> A fragment of key slice n/2 (FA2 register reuse)
+            if ((n & 1) == 0) {
+                p[n >> 1][0] = pack_bf16(e0, e1);
+                p[n >> 1][1] = pack_bf16(e2, e3);
+            } else {
+                p[n >> 1][2] = pack_bf16(e0, e1);
+                p[n >> 1][3] = pack_bf16(e2, e3);
+            }
+        }
+        suma += __shfl_xor_sync(0xffffffffu, suma, 1);
+        suma += __shfl_xor_sync(0xffffffffu, suma, 2);
+        sumb += __shfl_xor_sync(0xffffffffu, sumb, 1);
+        sumb += __shfl_xor_sync(0xffffffffu, sumb, 2);
+        // O = P V  (B operand from V^T rows: dims x keys)
+        float* outa = work + (((int64_t)ra * nh + ha) * (n_splits + 1) + sidx) * (HD + 2);
+        float* outb = work + (((int64_t)rb * nh + hb) * (n_splits + 1) + sidx) * (HD + 2);
+#pragma unroll
+        for (int nd = 0; nd < HD / 8; ++nd) {
+            float o[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+            for (int kk = 0; kk < CH / 16; ++kk) {
+                const __nv_bfloat16* vr = Vt + (nd * 8 + gq) * VLD + kk * 16 + 2 * tq;
+                uint32_t b[2];
+                b[0] = *reinterpret_cast<const uint32_t*>(vr);
+                b[1] = *reinterpret_cast<const uint32_t*>(vr + 8);
+                mma_bf16_16816(o, p[kk], b);
+            }
+            const int dcol = nd * 8 + 2 * tq;
+            if (qa < nq && la > 0) {
+                outa[2 + dcol] = o[0];
+                outa[2 + dcol + 1] = o[1];
+            }
+            if (qb < nq && lb > 0) {
+                outb[2 + dcol] = o[2];
+                outb[2 + dcol + 1] = o[3];
+            }
+        }
+        if (tq == 0) {
+            if (qa < nq && la > 0) {
+                outa[0] = ma;
+                outa[1] = suma;
+            }
+            if (qb < nq && lb > 0) {
+                outb[0] = mb;
+                outb[1] = sumb;
+            }
+        }
+    }
+}
+
 // extra slots (tree ancestors + self): one warp per (row, head)
 template <typename KV>
 __global__ void attn_extra_kernel(const float* __restrict__ q, const int32_t* dM, const int32_t* __restrict__ n_extra,
                                   const int32_t* __restrict__ extra, int extra_max, const KV* __restrict__ kc,
                                   const KV* __restrict__ vc, int nh, int nkv, int hd, int n_splits,
                                   float* __restrict__ work) {
+    pdl_wait();     // predecessor outputs visible from here
+    pdl_trigger();  // let the next kernel start its prologue
     const int M = *dM;
     const int gw = blockIdx.x * (blockDim.x >> 5) + warp_id();
     if (gw >= M * nh) return;
@@ -250,6 +426,8 @@ __global__ void attn_extra_kernel(const float* __restrict__ q, const int32_t* dM
 template <typename O>
 __global__ void attn_combine_kernel(const int32_t* dM, const int32_t* __restrict__ plen, int nh, int hd, int n_splits,
                                     const float* __restrict__ work, O* __restrict__ o) {
+    pdl_wait();     // predecessor outputs visible from here
+    pdl_trigger();  // let the next kernel start its prologue
     const int r = blockIdx.x, h = blockIdx.y;
     if (r >= *dM) return;
     const int ns = (plen[r] + kChunk - 1) / kChunk;
@@ -271,24 +449,30 @@ __global__ void attn_combine_kernel(const int32_t* dM, const int32_t* __restrict
     }
 }
 
-// ---------------------------------------------------------------- lm_head epilogues
-constexpr int kTopkRegs = 8;
-
+// ---------------------------------------------------------------- lm_head epilogues (split over the vocab)
+// Stage 1: CTA (row, split) scans a vocab slice: online max / sum-exp and a
+// register-resident sorted top-KT (static indices, bubble insertion).
+// Stage 2: one warp per row merges the splits: fp64 log-sum-exp and top-k.
 __device__ __forceinline__ bool lbefore(float a, int ta, float b, int tb) { return a > b || (a == b && ta < tb); }
 
-// One CTA per row: online max / sum-exp (fp32 per thread, fp64 merge) and
-// per-thread sorted top-k, merged by k rounds of block arg-best.
-__global__ void __launch_bounds__(512) topk_logits_kernel(const float* __restrict__ logits, const int32_t* dM, int V,
-                                                          int k, float inv_temp, int32_t* __restrict__ out_tok,
-                                                          double* __restrict__ out_logp, int32_t* __restrict__ out_cnt) {
-    const int r = blockIdx.x;
+template <int KT>
+__global__ void __launch_bounds__(256) topk_partial_kernel(const float* __restrict__ logits, const int32_t* dM, int V,
+                                                           int S, float inv_temp, float* __restrict__ work) {
+    pdl_wait();     // predecessor outputs visible from here
+    pdl_trigger();  // let the next kernel start its prologue
+    const int r = blockIdx.x, sp = blockIdx.y;
     if (r >= *dM) return;
+    const int lo = (int)((int64_t)V * sp / S), hi = (int)((int64_t)V * (sp + 1) / S);
     const float* lr = logits + (int64_t)r * V;
-    float tv[kTopkRegs];
-    int tt[kTopkRegs];
-    int m = 0;
+    float tv[KT];
+    int tt[KT];
+#pragma unroll
+    for (int j = 0; j < KT; ++j) {
+        tv[j] = -INFINITY;
+        tt[j] = 0x7fffffff;
+    }
     float mx = -INFINITY, sum = 0.f;
-    for (int i = threadIdx.x; i < V; i += blockDim.x) {
+    for (int i = lo + threadIdx.x; i < hi; i += blockDim.x) {
         const float v = lr[i] * inv_temp;
         if (v > mx) {
             sum = sum * __expf(mx - v) + 1.f;
@@ -296,51 +480,51 @@ __global__ void __launch_bounds__(512) topk_logits_kernel(const float* __restric
         } else {
             sum += __expf(v - mx);
         }
-        int p = m;
-        while (p > 0 && lbefore(v, i, tv[p - 1], tt[p - 1])) --p;
-        if (p < k) {
-            int end = m < k ? m : k - 1;
-            for (int j = end; j > p; --j) {
-                tv[j] = tv[j - 1];
-                tt[j] = tt[j - 1];
+        if (lbefore(v, i, tv[KT - 1], tt[KT - 1])) {
+            float cv = v;
+            int ci = i;
+#pragma unroll
+            for (int j = 0; j < KT; ++j) {
+                const bool b = lbefore(cv, ci, tv[j], tt[j]);
+                const float ov = tv[j];
+                const int oi = tt[j];
+                tv[j] = b ? cv : ov;
+                tt[j] = b ? ci : oi;
+                cv = b ? ov : cv;
+                ci = b ? oi : ci;
             }
-            tv[p] = v;
-            tt[p] = i;
-            if (m < k) ++m;
         }
     }
-    __shared__ double sh_m[32], sh_s[32];
-    __shared__ float bv[32];
-    __shared__ int bt[32], bl[32];
-    __shared__ double lse_sh;
-    // block max
+    // block reduction: max/sum then KT rounds of arg-best
+    __shared__ float sm_m[8], sm_s[8], bv[8];
+    __shared__ int bt[8], bw[8];
     float wm = mx;
     for (int o = 16; o > 0; o >>= 1) wm = fmaxf(wm, __shfl_xor_sync(0xffffffffu, wm, o));
-    if (lane_id() == 0) sh_m[warp_id()] = wm;
+    if (lane_id() == 0) sm_m[warp_id()] = wm;
     __syncthreads();
+    float gm = sm_m[0];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) gm = fmaxf(gm, sm_m[w]);
+    float ss = mx == -INFINITY ? 0.f : sum * __expf(mx - gm);
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    if (lane_id() == 0) sm_s[warp_id()] = ss;
+    __syncthreads();
+    float* out = work + ((int64_t)r * S + sp) * (2 + 2 * KT);
     if (threadIdx.x == 0) {
-        double g = -INFINITY;
-        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) g = fmax(g, sh_m[w]);
-        sh_m[0] = g;
+        float t = 0.f;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += sm_s[w];
+        out[0] = gm;
+        out[1] = t;
     }
-    __syncthreads();
-    const double gmax = sh_m[0];
-    double ds = (mx == -INFINITY) ? 0.0 : (double)sum * exp((double)mx - gmax);
-    for (int o = 16; o > 0; o >>= 1) ds += __shfl_xor_sync(0xffffffffu, ds, o);
-    __syncthreads();
-    if (lane_id() == 0) sh_s[warp_id()] = ds;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double t = 0.0;
-        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += sh_s[w];
-        lse_sh = gmax + log(t);
-    }
-    __syncthreads();
-    const double lse = lse_sh;
     int head = 0;
-    for (int round = 0; round < k; ++round) {
-        float v = head < m ? tv[head] : -INFINITY;
-        int t = head < m ? tt[head] : 0x7fffffff;
+    for (int round = 0; round < KT; ++round) {
+        float v = -INFINITY;
+        int t = 0x7fffffff;
+#pragma unroll
+        for (int j = 0; j < KT; ++j)
+            if (j == head) {
+                v = tv[j];
+                t = tt[j];
+            }
         int who = threadIdx.x;
         for (int o = 16; o > 0; o >>= 1) {
             const float ov = __shfl_xor_sync(0xffffffffu, v, o);
@@ -355,7 +539,7 @@ __global__ void __launch_bounds__(512) topk_logits_kernel(const float* __restric
         if (lane_id() == 0) {
             bv[warp_id()] = v;
             bt[warp_id()] = t;
-            bl[warp_id()] = who;
+            bw[warp_id()] = who;
         }
         __syncthreads();
         if (threadIdx.x == 0) {
@@ -363,28 +547,85 @@ __global__ void __launch_bounds__(512) topk_logits_kernel(const float* __restric
                 if (lbefore(bv[w], bt[w], bv[0], bt[0])) {
                     bv[0] = bv[w];
                     bt[0] = bt[w];
-                    bl[0] = bl[w];
+                    bw[0] = bw[w];
                 }
-            out_tok[(int64_t)r * k + round] = bt[0];
-            out_logp[(int64_t)r * k + round] = (double)bv[0] - lse;
+            out[2 + 2 * round] = bv[0];
+            out[3 + 2 * round] = __int_as_float(bt[0]);
         }
         __syncthreads();
-        if (threadIdx.x == bl[0]) ++head;
+        if (threadIdx.x == bw[0]) ++head;
         __syncthreads();
     }
-    if (threadIdx.x == 0) out_cnt[r] = k < V ? k : V;
 }
 
-__global__ void __launch_bounds__(512) argmax_logits_kernel(const float* __restrict__ logits, const int32_t* dM, int V,
-                                                            int32_t* __restrict__ out) {
-    const int r = blockIdx.x;
+template <int KT>
+__global__ void topk_merge_kernel(const int32_t* dM, int S, int k, int V, const float* __restrict__ work,
+                                  int32_t* __restrict__ out_tok, double* __restrict__ out_logp,
+                                  int32_t* __restrict__ out_cnt) {
+    pdl_wait();     // predecessor outputs visible from here
+    pdl_trigger();  // let the next kernel start its prologue
+    const int r = blockIdx.x * (blockDim.x >> 5) + warp_id();
     if (r >= *dM) return;
+    const int lane = lane_id();
+    const float* base = work + (int64_t)r * S * (2 + 2 * KT);
+    double gm = -INFINITY;
+    for (int s = lane; s < S; s += 32) gm = fmax(gm, (double)base[s * (2 + 2 * KT)]);
+    for (int o = 16; o > 0; o >>= 1) gm = fmax(gm, __shfl_xor_sync(0xffffffffu, gm, o));
+    double tot = 0.0;
+    for (int s = lane; s < S; s += 32) {
+        const float* p = base + s * (2 + 2 * KT);
+        if (p[1] > 0.f) tot += (double)p[1] * exp((double)p[0] - gm);
+    }
+    for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+    const double lse = gm + log(tot);
+    // candidates: S * KT, lane-strided; k rounds of warp arg-best with exclusion
+    int last_t = -1;
+    float last_v = INFINITY;
+    for (int round = 0; round < k; ++round) {
+        float v = -INFINITY;
+        int t = 0x7fffffff;
+        for (int c = lane; c < S * KT; c += 32) {
+            const float* p = base + (c / KT) * (2 + 2 * KT) + 2 + 2 * (c % KT);
+            const float cv = p[0];
+            const int ct = __float_as_int(p[1]);
+            // strictly after the previous pick in (value desc, token asc) order
+            if (lbefore(last_v, last_t, cv, ct) && lbefore(cv, ct, v, t)) {
+                v = cv;
+                t = ct;
+            }
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            const float ov = __shfl_xor_sync(0xffffffffu, v, o);
+            const int ot = __shfl_xor_sync(0xffffffffu, t, o);
+            if (lbefore(ov, ot, v, t)) {
+                v = ov;
+                t = ot;
+            }
+        }
+        if (lane == 0) {
+            out_tok[(int64_t)r * k + round] = t;
+            out_logp[(int64_t)r * k + round] = (double)v - lse;
+        }
+        last_v = v;
+        last_t = t;
+    }
+    if (lane == 0) out_cnt[r] = k < V ? k : V;
+}
+
+// greedy: first maximum per row, split over the vocab then merged
+__global__ void __launch_bounds__(256) argmax_partial_kernel(const float* __restrict__ logits, const int32_t* dM,
+                                                             int V, int S, float* __restrict__ work) {
+    pdl_wait();     // predecessor outputs visible from here
+    pdl_trigger();  // let the next kernel start its prologue
+    const int r = blockIdx.x, sp = blockIdx.y;
+    if (r >= *dM) return;
+    const int lo = (int)((int64_t)V * sp / S), hi = (int)((int64_t)V * (sp + 1) / S);
     const float* lr = logits + (int64_t)r * V;
     float bv = -INFINITY;
     int bi = 0x7fffffff;
-    for (int i = threadIdx.x; i < V; i += blockDim.x) {
+    for (int i = lo + threadIdx.x; i < hi; i += blockDim.x) {
         const float v = lr[i];
-        if (v > bv) {   // strided ascending scan: first max per thread
+        if (v > bv) {   // ascending strided scan: first max per thread
             bv = v;
             bi = i;
         }
@@ -397,8 +638,8 @@ __global__ void __launch_bounds__(512) argmax_logits_kernel(const float* __restr
             bi = oi;
         }
     }
-    __shared__ float sv[32];
-    __shared__ int si[32];
+    __shared__ float sv[8];
+    __shared__ int si[8];
     if (lane_id() == 0) {
         sv[warp_id()] = bv;
         si[warp_id()] = bi;
@@ -410,13 +651,42 @@ __global__ void __launch_bounds__(512) argmax_logits_kernel(const float* __restr
                 bv = sv[w];
                 bi = si[w];
             }
-        out[r] = bi;
+        work[((int64_t)r * S + sp) * 2] = bv;
+        work[((int64_t)r * S + sp) * 2 + 1] = __int_as_float(bi);
     }
+}
+
+__global__ void argmax_merge_kernel(const int32_t* dM, int S, const float* __restrict__ work, int32_t* __restrict__ out) {
+    pdl_wait();     // predecessor outputs visible from here
+    pdl_trigger();  // let the next kernel start its prologue
+    const int r = blockIdx.x * (blockDim.x >> 5) + warp_id();
+    if (r >= *dM) return;
+    float bv = -INFINITY;
+    int bi = 0x7fffffff;
+    for (int s = lane_id(); s < S; s += 32) {
+        const float v = work[((int64_t)r * S + s) * 2];
+        const int i = __float_as_int(work[((int64_t)r * S + s) * 2 + 1]);
+        if (v > bv || (v == bv && i < bi)) {
+            bv = v;
+            bi = i;
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ov > bv || (ov == bv && oi < bi)) {
+            bv = ov;
+            bi = oi;
+        }
+    }
+    if (lane_id() == 0) out[r] = bi;
 }
 
 // softmax(logits / T) in fp64, for the stochastic verify path
 __global__ void __launch_bounds__(512) softmax64_kernel(const float* __restrict__ logits, const int32_t* dM, int V,
                                                         double inv_temp, double* __restrict__ out) {
+    pdl_wait();     // predecessor outputs visible from here
+    pdl_trigger();  // let the next kernel start its prologue
     const int r = blockIdx.x;
     if (r >= *dM) return;
     const float* lr = logits + (int64_t)r * V;
@@ -455,6 +725,8 @@ __global__ void __launch_bounds__(512) softmax64_kernel(const float* __restrict_
 __global__ void logit_bias_kernel(float* __restrict__ logits, const int32_t* dM, int V,
                                   const int32_t* __restrict__ tail, int order, int stride, uint64_t seed,
                                   uint64_t seed2, float mixw, float sharp) {
+    pdl_wait();     // predecessor outputs visible from here
+    pdl_trigger();  // let the next kernel start its prologue
     const int r = blockIdx.x;
     if (r >= *dM) return;
     __shared__ uint64_t st[2];
@@ -489,7 +761,7 @@ int card_logit_bias(float* logits, const int32_t* dM, int m_max, int V, const in
                     int stride, uint64_t seed, uint64_t seed2, float mix_weight, float sharpness, void* stream) {
     if (sharpness == 0.f || m_max <= 0) return CARD_OK;
     if (stride < order) return CARD_E_INPUT;
-    logit_bias_kernel<<<m_max, 512, 0, (cudaStream_t)stream>>>(logits, dM, V, ctx_tail, order, stride, seed, seed2,
+    CARD_PDL((logit_bias_kernel), dim3(m_max), dim3(512), 0, (cudaStream_t)stream, logits, dM, V, ctx_tail, order, stride, seed, seed2,
                                                                mix_weight, sharpness);
     CARD_LAUNCH_CHECK();
     return CARD_OK;
@@ -498,8 +770,8 @@ int card_logit_bias(float* logits, const int32_t* dM, int m_max, int V, const in
 int card_embed(const int32_t* tok, const int32_t* dM, int m_max, const void* E, int wdtype, int H, float* x,
                void* stream) {
     cudaStream_t s = (cudaStream_t)stream;
-    if (wdtype == 0) embed_kernel<<<m_max, 256, 0, s>>>(tok, dM, (const __nv_bfloat16*)E, H, x);
-    else embed_kernel<<<m_max, 256, 0, s>>>(tok, dM, (const float*)E, H, x);
+    if (wdtype == 0) CARD_PDL((embed_kernel<__nv_bfloat16>), dim3(m_max), dim3(256), 0, s, tok, dM, (const __nv_bfloat16*)E, H, x);
+    else CARD_PDL((embed_kernel<float>), dim3(m_max), dim3(256), 0, s, tok, dM, (const float*)E, H, x);
     CARD_LAUNCH_CHECK();
     return CARD_OK;
 }
@@ -507,8 +779,8 @@ int card_embed(const int32_t* tok, const int32_t* dM, int m_max, const void* E, 
 int card_rmsnorm(const float* x, const float* w, int H, float eps, const int32_t* dM, int m_max, const int32_t* gather,
                  void* y, int ydtype, void* stream) {
     cudaStream_t s = (cudaStream_t)stream;
-    if (ydtype == 0) rmsnorm_kernel<<<m_max, 256, 0, s>>>(x, w, H, eps, dM, gather, (__nv_bfloat16*)y);
-    else rmsnorm_kernel<<<m_max, 256, 0, s>>>(x, w, H, eps, dM, gather, (float*)y);
+    if (ydtype == 0) CARD_PDL((rmsnorm_kernel<__nv_bfloat16>), dim3(m_max), dim3(256), 0, s, x, w, H, eps, dM, gather, (__nv_bfloat16*)y);
+    else CARD_PDL((rmsnorm_kernel<float>), dim3(m_max), dim3(256), 0, s, x, w, H, eps, dM, gather, (float*)y);
     CARD_LAUNCH_CHECK();
     return CARD_OK;
 }
@@ -519,10 +791,10 @@ int card_rope_kv(const float* qkv, const int32_t* dM, int m_max, const int32_t* 
     cudaStream_t s = (cudaStream_t)stream;
     const float qscale = 1.0f / sqrtf((float)hd);
     if (kvdtype == 0)
-        rope_kv_kernel<<<m_max, 256, 0, s>>>(qkv, dM, pos, slot, cos_t, sin_t, nh, nkv, hd, qscale, q,
+        CARD_PDL((rope_kv_kernel<__nv_bfloat16>), dim3(m_max), dim3(256), 0, s, qkv, dM, pos, slot, cos_t, sin_t, nh, nkv, hd, qscale, q,
                                              (__nv_bfloat16*)kc, (__nv_bfloat16*)vc);
     else
-        rope_kv_kernel<<<m_max, 256, 0, s>>>(qkv, dM, pos, slot, cos_t, sin_t, nh, nkv, hd, qscale, q, (float*)kc,
+        CARD_PDL((rope_kv_kernel<float>), dim3(m_max), dim3(256), 0, s, qkv, dM, pos, slot, cos_t, sin_t, nh, nkv, hd, qscale, q, (float*)kc,
                                              (float*)vc);
     CARD_LAUNCH_CHECK();
     return CARD_OK;
@@ -549,41 +821,77 @@ int card_attention(const float* q, const int32_t* dM, int m_max, const int32_t* 
     dim3 g1(nkv, n_splits);
     const int ew = (m_max * nh + 7) / 8;
     if (kvdtype == 0) {
-        attn_prefix_kernel<<<g1, threads, smem, s>>>(q, dM, plen, (const __nv_bfloat16*)kc, (const __nv_bfloat16*)vc,
-                                                     nh, nkv, hd, n_splits, work);
-        attn_extra_kernel<<<ew, 256, 0, s>>>(q, dM, n_extra, extra, extra_max, (const __nv_bfloat16*)kc,
+        if (hd == 64)
+            CARD_PDL((attn_prefix_tc_kernel<64>), dim3(g1), dim3(128), 0, s, q, dM, plen, (const __nv_bfloat16*)kc,
+                                                         (const __nv_bfloat16*)vc, nh, nkv, n_splits, work);
+        else if (hd == 128)
+            CARD_PDL((attn_prefix_tc_kernel<128>), dim3(g1), dim3(128), 0, s, q, dM, plen, (const __nv_bfloat16*)kc,
+                                                          (const __nv_bfloat16*)vc, nh, nkv, n_splits, work);
+        else
+            CARD_PDL((attn_prefix_kernel<__nv_bfloat16>), dim3(g1), dim3(threads), smem, s, q, dM, plen, (const __nv_bfloat16*)kc,
+                                                         (const __nv_bfloat16*)vc, nh, nkv, hd, n_splits, work);
+        CARD_PDL((attn_extra_kernel<__nv_bfloat16>), dim3(ew), dim3(256), 0, s, q, dM, n_extra, extra, extra_max, (const __nv_bfloat16*)kc,
                                              (const __nv_bfloat16*)vc, nh, nkv, hd, n_splits, work);
     } else {
-        attn_prefix_kernel<<<g1, threads, smem, s>>>(q, dM, plen, (const float*)kc, (const float*)vc, nh, nkv, hd,
+        CARD_PDL((attn_prefix_kernel<float>), dim3(g1), dim3(threads), smem, s, q, dM, plen, (const float*)kc, (const float*)vc, nh, nkv, hd,
                                                      n_splits, work);
-        attn_extra_kernel<<<ew, 256, 0, s>>>(q, dM, n_extra, extra, extra_max, (const float*)kc, (const float*)vc, nh,
+        CARD_PDL((attn_extra_kernel<float>), dim3(ew), dim3(256), 0, s, q, dM, n_extra, extra, extra_max, (const float*)kc, (const float*)vc, nh,
                                              nkv, hd, n_splits, work);
     }
     dim3 g3(m_max, nh);
-    if (odtype == 0) attn_combine_kernel<<<g3, 64, 0, s>>>(dM, plen, nh, hd, n_splits, work, (__nv_bfloat16*)o);
-    else attn_combine_kernel<<<g3, 64, 0, s>>>(dM, plen, nh, hd, n_splits, work, (float*)o);
+    if (odtype == 0) CARD_PDL((attn_combine_kernel<__nv_bfloat16>), dim3(g3), dim3(64), 0, s, dM, plen, nh, hd, n_splits, work, (__nv_bfloat16*)o);
+    else CARD_PDL((attn_combine_kernel<float>), dim3(g3), dim3(64), 0, s, dM, plen, nh, hd, n_splits, work, (float*)o);
     CARD_LAUNCH_CHECK();
     return CARD_OK;
 }
+
+static int vocab_splits(int m_max) {
+    int s = (2 * 148 + m_max - 1) / (m_max > 0 ? m_max : 1);
+    return s < 1 ? 1 : (s > 64 ? 64 : s);
+}
+
+int card_lmhead_work_floats(int m_max, int k) { return m_max * vocab_splits(m_max) * (2 + 2 * 8); }
 
 int card_topk_logits(const float* logits, const int32_t* dM, int m_max, int V, int k, double inv_temp,
-                     int32_t* out_tok, double* out_logp, int32_t* out_cnt, void* stream) {
-    if (k < 1 || k > kTopkRegs) return CARD_E_CONFIG;
-    topk_logits_kernel<<<m_max, 512, 0, (cudaStream_t)stream>>>(logits, dM, V, k, (float)inv_temp, out_tok, out_logp,
-                                                                out_cnt);
+                     int32_t* out_tok, double* out_logp, int32_t* out_cnt, float* work, void* stream) {
+    if (k < 1 || k > 8) return CARD_E_CONFIG;
+    cudaStream_t s = (cudaStream_t)stream;
+    const int S = vocab_splits(m_max);
+    dim3 g(m_max, S);
+    const float it = (float)inv_temp;
+    switch (k) {
+#define CARD_TOPK_CASE(KT)                                                                                   \
+    case KT:                                                                                                 \
+        CARD_PDL((topk_partial_kernel<KT>), dim3(g), dim3(256), 0, s, logits, dM, V, S, it, work);                                \
+        CARD_PDL((topk_merge_kernel<KT>), dim3((m_max + 7) / 8), dim3(256), 0, s, dM, S, k, V, work, out_tok, out_logp, out_cnt); \
+        break;
+        CARD_TOPK_CASE(1)
+        CARD_TOPK_CASE(2)
+        CARD_TOPK_CASE(3)
+        CARD_TOPK_CASE(4)
+        CARD_TOPK_CASE(5)
+        CARD_TOPK_CASE(6)
+        CARD_TOPK_CASE(7)
+        CARD_TOPK_CASE(8)
+#undef CARD_TOPK_CASE
+    }
     CARD_LAUNCH_CHECK();
     return CARD_OK;
 }
 
-int card_argmax_logits(const float* logits, const int32_t* dM, int m_max, int V, int32_t* out, void* stream) {
-    argmax_logits_kernel<<<m_max, 512, 0, (cudaStream_t)stream>>>(logits, dM, V, out);
+int card_argmax_logits(const float* logits, const int32_t* dM, int m_max, int V, int32_t* out, float* work,
+                       void* stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    const int S = vocab_splits(m_max);
+    CARD_PDL((argmax_partial_kernel), dim3(m_max, S), dim3(256), 0, s, logits, dM, V, S, work);
+    CARD_PDL((argmax_merge_kernel), dim3((m_max + 7) / 8), dim3(256), 0, s, dM, S, work, out);
     CARD_LAUNCH_CHECK();
     return CARD_OK;
 }
 
 int card_softmax64(const float* logits, const int32_t* dM, int m_max, int V, double inv_temp, double* out,
                    void* stream) {
-    softmax64_kernel<<<m_max, 512, 0, (cudaStream_t)stream>>>(logits, dM, V, inv_temp, out);
+    CARD_PDL((softmax64_kernel), dim3(m_max), dim3(512), 0, (cudaStream_t)stream, logits, dM, V, inv_temp, out);
     CARD_LAUNCH_CHECK();
     return CARD_OK;
 }

@@ -7,12 +7,21 @@
 // the toy-model parity path and the drop-in TreeCache.expand_layer; the
 // transformer path produces candidates from logits in card_llm.cu.
 #include <stdio.h>
+#include <stdlib.h>
 
 #include "card_common.cuh"
 
 namespace card {
 
 static thread_local char g_cuda_err[256] = {0};
+bool pdl_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("CARD_PDL");
+        v = (e && e[0] == '0') ? 0 : 1;
+    }
+    return v != 0;
+}
 void set_cuda_error(cudaError_t e) {
     snprintf(g_cuda_err, sizeof(g_cuda_err), "%s: %s", cudaGetErrorName(e), cudaGetErrorString(e));
 }

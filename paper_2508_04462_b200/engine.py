@@ -225,6 +225,7 @@ class _LlamaAdapter:
         self.logp = torch.zeros((rows_max, self.k), dtype=torch.float64, device=dev)
         self.cnt = torch.zeros(rows_max, dtype=torch.int32, device=dev)
         self.amax = torch.zeros(rows_max, dtype=torch.int32, device=dev)
+        self.lm_work = torch.zeros(lib().card_lmhead_work_floats(rows_max, self.k), dtype=torch.float32, device=dev)
         self.probs = torch.zeros((rows_max, V), dtype=torch.float64, device=dev) if run.sampling else None
         self.prefill_rows = None
         if role == "draft":
@@ -264,7 +265,7 @@ class _LlamaAdapter:
         self._bias(run.drt)
         raise_for_status(lib().card_topk_logits(ptr(self.rt.logits), ptr(rows.n_out), self.rows_max, self.V, self.k,
                                                 1.0 / run.t_score, ptr(self.tok), ptr(self.logp), ptr(self.cnt),
-                                                stream_ptr()), "topk_logits")
+                                                ptr(self.lm_work), stream_ptr()), "topk_logits")
         return self.tok, self.logp, self.cnt, 0
 
     def target(self, run):
@@ -279,7 +280,7 @@ class _LlamaAdapter:
                                                   ptr(run.uni), stream_ptr()), "verify_probs")
         else:
             raise_for_status(L_.card_argmax_logits(ptr(self.rt.logits), ptr(rows.n_out), self.rows_max, self.V,
-                                                   ptr(self.amax), stream_ptr()), "argmax")
+                                                   ptr(self.amax), ptr(self.lm_work), stream_ptr()), "argmax")
             raise_for_status(L_.card_verify_argmax(run.E_ptr, run.q_tok_ptr, ptr(self.amax), stream_ptr()),
                              "verify_argmax")
 
@@ -517,17 +518,24 @@ class DeviceRun:
         """Capture one draft step and one target step as CUDA graphs."""
         if not self.cfg.correction_enabled:
             raise ConfigError("graph mode needs correction_enabled=True (the ablation resets on the host)")
+        from . import _lib
+
         g_d, g_t = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
         s = torch.cuda.Stream()
         s.wait_stream(torch.cuda.current_stream())
-        # state snapshot so warmup-by-capture leaves no trace: capture does not execute
+        # capture records without executing: the run state is untouched
         with torch.cuda.stream(s):
+            c0 = _lib.launch_count[0]
             with torch.cuda.graph(g_d, stream=s):
                 self.launch_draft_step()
+            c1 = _lib.launch_count[0]
             with torch.cuda.graph(g_t, stream=s):
                 self.launch_target_step(with_correct=True, readback=True)
+            c2 = _lib.launch_count[0]
         torch.cuda.current_stream().wait_stream(s)
         self.graphs = (g_d, g_t)
+        self.launches_per_graph = (c1 - c0, c2 - c1)
+        self.replays = [0, 0]
 
     def run_graphs(self, max_cycles: int | None = None):
         """Throughput driver: one host<->device round trip per cycle."""
@@ -539,6 +547,7 @@ class DeviceRun:
         depth = 0
         for _ in range(cfg.query_depth):   # warm-up (engine.py:295-301)
             g_d.replay()
+            self.replays[0] += 1
         E = self.read_state()
         for i in range(min(E.n_widths, 64)):
             w = E.widths[i]
@@ -556,6 +565,8 @@ class DeviceRun:
             for _ in range(n_exp):
                 g_d.replay()
             g_t.replay()
+            self.replays[0] += n_exp
+            self.replays[1] += 1
             torch.cuda.current_stream().synchronize()
             E = EngineState.from_buffer_copy(self._host.numpy().tobytes())
             start, k = clock, 0
@@ -615,6 +626,9 @@ def run_speculative(draft, target, prompt: Sequence[TokenId], config: EngineConf
         ev1.record()
         ev1.synchronize()
         run.timing["decode_ms"] = ev0.elapsed_time(ev1)
+        run.timing["gpu_launches"] = (run.replays[0] * run.launches_per_graph[0] +
+                                      run.replays[1] * run.launches_per_graph[1])
+        run.timing["draft_steps"], run.timing["target_steps"] = run.replays
     else:
         run.run_stepwise()
     run.timing["wall_s"] = time.perf_counter() - t0
@@ -672,12 +686,16 @@ class VanillaRun:
         self.ta.prefill(self, self.prompt[:-1])
 
     def capture(self):
+        from . import _lib
+
         g = torch.cuda.CUDAGraph()
         s = torch.cuda.Stream()
         s.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(s):
+            c0 = _lib.launch_count[0]
             with torch.cuda.graph(g, stream=s):
                 self.step()
+            self.launches_per_step = _lib.launch_count[0] - c0
         torch.cuda.current_stream().wait_stream(s)
         self.graph = g
 
@@ -718,8 +736,10 @@ def run_vanilla(target, prompt: Sequence[TokenId], config: EngineConfig, *, use_
     out = run.output()
     t_lat = target.spec.forward_latency
     trace = [StepTrace(i, (i + 1) * t_lat, False, 0, 0, 1, 0, "miss_step") for i in range(len(out))]
-    return RunResult(output=out, metrics=finalize(trace, target.spec), trace=trace,
-                     wall={"decode_ms": ev0.elapsed_time(ev1), "wall_s": time.perf_counter() - t0})
+    wall = {"decode_ms": ev0.elapsed_time(ev1), "wall_s": time.perf_counter() - t0}
+    if use_graph:
+        wall["gpu_launches"] = run.cfg.max_new_tokens * run.launches_per_step
+    return RunResult(output=out, metrics=finalize(trace, target.spec), trace=trace, wall=wall)
 
 
 def forward_context_logits(model, context: list[int]) -> torch.Tensor:

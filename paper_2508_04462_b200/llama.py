@@ -154,6 +154,20 @@ def init_weights(cfg: LlamaConfig, seed: int, device="cpu", dtype=torch.float32)
     return w
 
 
+def tile_sw128(w: torch.Tensor) -> torch.Tensor:
+    """Row-major bf16 [N, K] -> pre-tiled [N/128, K/64, 128, 64] blocks with the
+    SWIZZLE_128B XOR applied (16-byte chunk c of row r stored at c ^ (r % 8)),
+    so one contiguous 16 KB bulk copy lands exactly as a swizzled TMA tile."""
+    N, K = w.shape
+    t = w.view(N // 128, 128, K // 64, 64).permute(0, 2, 1, 3)          # [nt, kb, 128, 64]
+    t = t.reshape(N // 128, K // 64, 128, 8, 8)                          # chunks of 8 bf16 (16 B)
+    r = torch.arange(128, device=w.device).view(128, 1)
+    j = torch.arange(8, device=w.device).view(1, 8)
+    src = (j ^ (r % 8)).expand(128, 8)                                   # new[r, j] = old[r, j ^ (r%8)]
+    idx = src.view(1, 1, 128, 8, 1).expand(N // 128, K // 64, 128, 8, 8)
+    return torch.gather(t, 3, idx).reshape(N // 128, K // 64, 128, 64).contiguous()
+
+
 def interleave_gate_up(wg: torch.Tensor, wu: torch.Tensor) -> torch.Tensor:
     """[2F, H]: per 128-row tile, 64 gate rows then the 64 matching up rows."""
     F, H = wg.shape
@@ -169,15 +183,17 @@ def pack_weights(cfg: LlamaConfig, weights: dict, dtype: str = "bf16", device=No
     wdt = torch.bfloat16 if dtype == "bf16" else torch.float32
     to = lambda t: t.to(device=dev, dtype=wdt).contiguous()  # noqa: E731
     f32 = lambda t: t.to(device=dev, dtype=torch.float32).contiguous()  # noqa: E731
+    # bf16 linear weights live pre-tiled (tile_sw128); fp32 parity weights row-major
+    lin = (lambda t: tile_sw128(to(t))) if dtype == "bf16" else to  # noqa: E731
     out = {"dtype": dtype, "embed": to(weights["embed"]), "norm": f32(weights["norm"]), "layers": []}
-    out["lm_head"] = out["embed"] if cfg.tie_embeddings else to(weights["lm_head"])
+    out["lm_head"] = lin(weights["lm_head"])
     for i in range(cfg.n_layers):
         p = f"l{i}."
         out["layers"].append({
-            "wqkv": to(torch.cat([weights[p + "wq"], weights[p + "wk"], weights[p + "wv"]], 0)),
-            "wo": to(weights[p + "wo"]),
-            "wgu": to(interleave_gate_up(weights[p + "wg"], weights[p + "wu"])),
-            "wd": to(weights[p + "wd"]),
+            "wqkv": lin(torch.cat([weights[p + "wq"], weights[p + "wk"], weights[p + "wv"]], 0)),
+            "wo": lin(weights[p + "wo"]),
+            "wgu": lin(interleave_gate_up(weights[p + "wg"], weights[p + "wu"])),
+            "wd": lin(weights[p + "wd"]),
             "attn_norm": f32(weights[p + "attn_norm"]),
             "mlp_norm": f32(weights[p + "mlp_norm"]),
             "bqkv": f32(torch.cat([weights[p + "bq"], weights[p + "bk"], weights[p + "bv"]], 0))
@@ -189,18 +205,28 @@ def pack_weights(cfg: LlamaConfig, weights: dict, dtype: str = "bf16", device=No
 class _Linear:
     def __init__(self, W: torch.Tensor, X: torch.Tensor, m_max: int, epi: int, out: torch.Tensor, ldo: int,
                  bias: torch.Tensor | None = None):
+        """W: row-major [N, K] (bf16 or fp32) or pre-tiled bf16 [N/128, K/64, 128, 64]."""
         self.keep = (W, X, out, bias)
+        self._swiglu = epi == EPI_SWIGLU_BF16
         h = ctypes.c_void_p()
-        wd = 0 if W.dtype == torch.bfloat16 else 1
-        rc = lib().card_linear_create(ptr(W), W.shape[0], W.shape[1], wd, ptr(X), m_max, epi, ptr(out), ldo,
-                                      ptr(bias), ctypes.byref(h))
-        raise_for_status(rc, f"card_linear_create(N={W.shape[0]}, K={W.shape[1]}, m_max={m_max})")
+        if W.dim() == 4:
+            wd, N, K = 2, W.shape[0] * 128, W.shape[1] * 64
+        else:
+            wd, N, K = (0 if W.dtype == torch.bfloat16 else 1), W.shape[0], W.shape[1]
+        self.N, self.K = N, K
+        self.nbytes = N * K * W.element_size()
+        rc = lib().card_linear_create(ptr(W), N, K, wd, ptr(X), m_max, epi, ptr(out), ldo, ptr(bias),
+                                      ctypes.byref(h))
+        raise_for_status(rc, f"card_linear_create(N={N}, K={K}, m_max={m_max})")
         self.h = h
         info = (ctypes.c_int32 * 8)()
         lib().card_linear_info(h, info)
         self.info = dict(zip(("kind", "splits", "stages", "grid", "smem", "Mpad", "tmem_cols", "items"), list(info)))
 
     def run(self, dM: torch.Tensor):
+        from . import _lib
+
+        _lib.launch_count[0] += 2 if (self.info["kind"] != 0 and self.keep and self._swiglu) else 1
         rc = lib().card_linear_run(self.h, ptr(dM), stream_ptr())
         if rc:
             raise_for_status(rc, "card_linear_run")

@@ -16,10 +16,10 @@ def declared_functions():
 
 
 def test_library_exports_every_declared_symbol():
-    from paper_2508_04462_b200._lib import LIB_PATH, SIGNATURES, lib
+    from paper_2508_04462_b200._lib import LIB_PATH, SIGNATURES, raw
 
     assert os.path.exists(LIB_PATH), "run __graft_entry__.build() first"
-    handle = lib()
+    handle = raw()
     decl = declared_functions()
     assert decl, "no declarations parsed"
     for name in decl:

@@ -22,8 +22,9 @@ def card():
 @pytest.mark.parametrize("M", [1, 2, 5, 8, 16, 37, 100, 128])
 @pytest.mark.parametrize("NK", [(256, 512), (1024, 4096), (384, 1536)])
 @pytest.mark.parametrize("epi", [0, 1, 3])
-def test_linear_bf16_vs_torch(card, M, NK, epi):
-    from paper_2508_04462_b200.llama import _Linear
+@pytest.mark.parametrize("layout", ["rowmajor", "tiled"])
+def test_linear_bf16_vs_torch(card, M, NK, epi, layout):
+    from paper_2508_04462_b200.llama import _Linear, tile_sw128
 
     N, K = NK
     g = torch.Generator(device="cuda").manual_seed(M * 131 + N + epi)
@@ -33,6 +34,8 @@ def test_linear_bf16_vs_torch(card, M, NK, epi):
     X[:M] = torch.randn(M, K, device="cuda", generator=g).to(torch.bfloat16)
     ref = X[:M].float() @ W.float().T
     dM = torch.tensor([M], dtype=torch.int32, device="cuda")
+    if layout == "tiled":
+        W = tile_sw128(W)
     if epi == 3:
         out = torch.zeros(mpad, N // 2, device="cuda", dtype=torch.bfloat16)
         lin = _Linear(W, X, M, 3, out, N // 2)
