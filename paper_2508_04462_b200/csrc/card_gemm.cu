@@ -98,6 +98,37 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
     for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+// address of the same smem variable in cluster CTA `rank` (DSMEM)
+__device__ __forceinline__ uint32_t dsmem_addr(uint32_t local, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ float dsmem_ld(uint32_t addr) {
+    float v;
+    asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+    return v;
+}
+// sum over the S cluster ranks of the float at byte offset `off` of each
+// rank's staging buffer: all S remote loads are issued before the first add
+// (in-order issue would otherwise serialise them), summed in rank order.
+__device__ __forceinline__ float dsmem_sum(const uint32_t* bases, int S, uint32_t off) {
+    float t[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) t[q] = q < S ? dsmem_ld(bases[q] + off) : 0.f;
+    float v = 0.f;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) v += t[q];
+    return v;
+}
 
 // K-major SWIZZLE_128B shared-memory matrix descriptor (sm100 encoding):
 // start>>4 | LBO(16B)=1 <<16 | SBO(1024B)=64 <<32 | version 1 <<46 | layout 2 <<61
@@ -121,6 +152,7 @@ struct TcArgs {
     const int32_t* dM;
     const uint8_t* w_tiled;   // non-null: [n_tiles][kb_total][128 x 128 B] pre-swizzled blocks
     int epi;
+    int cluster;      // > 1: split-K over a thread-block cluster, DSMEM reduction
     float* out_f32;
     __nv_bfloat16* out_bf16;
     const float* bias;
@@ -350,12 +382,17 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
             const uint32_t trow = tmem_base + ((uint32_t)(warp * 32) << 16) + (uint32_t)(acc * a.Mpad);
             const bool direct = a.splits == 1;
             float* wsp = a.ws + (size_t)item * kTileN * a.Mpad;
+            float* red = reinterpret_cast<float*>(sA);   // cluster mode: [Mpad][128] partial in own smem
             for (int m0 = 0; m0 < M; m0 += 16) {
                 float v[16];
                 tmem_ld16(trow + (uint32_t)m0, v);
                 const int mc = (M - m0) < 16 ? (M - m0) : 16;
                 if (direct) {
                     epi_chunk<EPI>(a, tile, n_glob, n_local, m0, mc, v, xch);
+                } else if (a.cluster > 1) {
+#pragma unroll
+                    for (int j = 0; j < 16; ++j)
+                        if (j < mc) red[(m0 + j) * kTileN + n_local] = v[j];
                 } else {
 #pragma unroll
                     for (int j = 0; j < 16; ++j)
@@ -371,7 +408,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
             } else {
                 acc_phase ^= 1;
             }
-            if (!direct) {
+            if (!direct && a.cluster <= 1) {
                 // deterministic split-K fixup: the last arriver sums splits 0..S-1 in order.
                 // bar.sync orders this CTA's partial stores before thread 0's release.
                 named_bar(1, kEpiThreads);
@@ -401,6 +438,47 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
                 }
             }
         }
+    }
+    if (a.cluster > 1) {
+        // split-K over the cluster: every CTA staged its partial tile in smem;
+        // rank r reduces a slice of the tile's rows over all ranks (DSMEM) in
+        // rank order (deterministic) and applies the epilogue.
+        cluster_sync_all();
+        if (warp < 4 && M > 0) {
+            const int S = a.cluster;
+            const int r = (int)cluster_rank();
+            const int tile = blockIdx.x / S;
+            const uint32_t red_local = smem_u32(sA);
+            const int tid = threadIdx.x;
+            uint32_t bases[16];
+#pragma unroll
+            for (int q = 0; q < 16; ++q) bases[q] = q < S ? dsmem_addr(red_local, (uint32_t)q) : 0u;
+            if (EPI == EPI_SWIGLU_BF16) {
+                const int f0 = 64 * r / S, f1 = 64 * (r + 1) / S, w = f1 - f0;
+                for (int e = tid; e < w * M; e += kEpiThreads) {
+                    const int m = e / w, f = f0 + e % w;
+                    float g = dsmem_sum(bases, S, (uint32_t)((m * kTileN + f) * 4));
+                    float u = dsmem_sum(bases, S, (uint32_t)((m * kTileN + 64 + f) * 4));
+                    if (a.bias) {
+                        g += a.bias[tile * kTileN + f];
+                        u += a.bias[tile * kTileN + 64 + f];
+                    }
+                    a.out_bf16[(int64_t)m * a.ldo + tile * 64 + f] = __float2bfloat16(silu(g) * u);
+                }
+            } else {
+                const int n0 = kTileN * r / S, n1 = kTileN * (r + 1) / S, w = n1 - n0;
+                for (int e = tid; e < w * M; e += kEpiThreads) {
+                    const int m = e / w, n = n0 + e % w;
+                    float v = dsmem_sum(bases, S, (uint32_t)((m * kTileN + n) * 4));
+                    const int ng = tile * kTileN + n;
+                    if (a.bias) v += a.bias[ng];
+                    if (EPI == EPI_STORE_F32) a.out_f32[(int64_t)m * a.ldo + ng] = v;
+                    else if (EPI == EPI_RESID_F32) a.out_f32[(int64_t)m * a.ldo + ng] += v;
+                    else a.out_bf16[(int64_t)m * a.ldo + ng] = __float2bfloat16(v);
+                }
+            }
+        }
+        cluster_sync_all();   // peers may not exit while their smem is being read
     }
     tc_fence_before();
     __syncthreads();
@@ -607,7 +685,31 @@ namespace card {
 template <int EPI>
 static cudaError_t set_tc_attr(int smem) {
     (void)smem;
+    cudaFuncSetAttribute(tc_gemm_kernel<EPI>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     return cudaFuncSetAttribute(tc_gemm_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+}
+
+template <int EPI>
+static cudaError_t launch_tc(const card_linear* h, const TcArgs& a, cudaStream_t s) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(h->grid);
+    cfg.blockDim = dim3(kTcThreads);
+    cfg.dynamicSmemBytes = h->smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    int n = 1;
+    if (a.cluster > 1) {
+        attr[1].id = cudaLaunchAttributeClusterDimension;
+        attr[1].val.clusterDim.x = a.cluster;
+        attr[1].val.clusterDim.y = 1;
+        attr[1].val.clusterDim.z = 1;
+        n = 2;
+    }
+    cfg.attrs = attr;
+    cfg.numAttrs = n;
+    return cudaLaunchKernelEx(&cfg, tc_gemm_kernel<EPI>, h->tmW, h->tmX, a);
 }
 
 // Split choice (calibrated on B200 with tools/split_sweep.sh): a work item
@@ -712,10 +814,26 @@ int card_linear_create(const void* W, int N, int K, int wdtype, const void* X, i
     h->smem = stages * stage_bytes + extra;
     const int slots = num_sms() * ctas_per_sm;
     a.splits = choose_splits(a.n_tiles, a.kb_total, Mpad, slots);
+    a.cluster = 1;
+    // cluster split-K when the tiles alone leave SMs idle: one item per CTA,
+    // the S K-slices of a tile form a cluster and reduce through DSMEM
+    // (measured: a win for the wide draft tiles, a loss for Mpad=16 verify tiles)
+    if (!getenv("CARD_NO_CLUSTER") && Mpad >= 64 && 2 * a.n_tiles <= slots) {
+        int S = slots / a.n_tiles;
+        if (S > 16) S = 16;
+        if (S > a.kb_total) S = a.kb_total;
+        while (S > 1 && (size_t)Mpad * kTileN * 4 > (size_t)stages * (kTileN * kBK * 2 + Mpad * kBK * 2)) --S;
+        if (S > 1) {
+            a.splits = S;
+            a.cluster = S;
+        }
+    }
     if (getenv("CARD_SPLITS")) a.splits = atoi(getenv("CARD_SPLITS"));   // tuning knob
+    if (a.cluster > 1) a.cluster = a.splits;
     a.items = a.n_tiles * a.splits;
     h->grid = a.items < slots ? a.items : slots;
-    if (a.splits > 1) {
+    if (a.cluster > 1) h->grid = a.items;
+    if (a.splits > 1 && a.cluster <= 1) {
         CARD_CUDA_TRY(cudaMalloc(&a.ws, (size_t)a.items * kTileN * Mpad * 4));
         CARD_CUDA_TRY(cudaMalloc(&a.counters, (size_t)a.n_tiles * 4));
         CARD_CUDA_TRY(cudaMemset(a.counters, 0, (size_t)a.n_tiles * 4));
@@ -749,11 +867,16 @@ int card_linear_run(card_linear* h, const int32_t* dM, void* stream) {
     TcArgs a = h->args;
     a.dM = dM;
     if (h->kind == 0) {
+        cudaError_t e = cudaSuccess;
         switch (h->epi) {
-            case EPI_STORE_F32: CARD_PDL((tc_gemm_kernel<EPI_STORE_F32>), dim3(h->grid), dim3(kTcThreads), h->smem, s, h->tmW, h->tmX, a); break;
-            case EPI_RESID_F32: CARD_PDL((tc_gemm_kernel<EPI_RESID_F32>), dim3(h->grid), dim3(kTcThreads), h->smem, s, h->tmW, h->tmX, a); break;
-            case EPI_STORE_BF16: CARD_PDL((tc_gemm_kernel<EPI_STORE_BF16>), dim3(h->grid), dim3(kTcThreads), h->smem, s, h->tmW, h->tmX, a); break;
-            case EPI_SWIGLU_BF16: CARD_PDL((tc_gemm_kernel<EPI_SWIGLU_BF16>), dim3(h->grid), dim3(kTcThreads), h->smem, s, h->tmW, h->tmX, a); break;
+            case EPI_STORE_F32: e = launch_tc<EPI_STORE_F32>(h, a, s); break;
+            case EPI_RESID_F32: e = launch_tc<EPI_RESID_F32>(h, a, s); break;
+            case EPI_STORE_BF16: e = launch_tc<EPI_STORE_BF16>(h, a, s); break;
+            case EPI_SWIGLU_BF16: e = launch_tc<EPI_SWIGLU_BF16>(h, a, s); break;
+        }
+        if (e != cudaSuccess) {
+            set_cuda_error(e);
+            return CARD_E_CUDA;
         }
     } else if (h->kind == 1) {
         const __nv_bfloat16* W = (const __nv_bfloat16*)h->W;
@@ -794,7 +917,7 @@ int card_linear_info(card_linear* h, int32_t* info8) {
     info8[4] = h->smem;
     info8[5] = h->Mpad;
     info8[6] = h->args.tmem_cols;
-    info8[7] = h->args.items;
+    info8[7] = h->args.cluster > 1 ? -h->args.cluster : h->args.items;
     return CARD_OK;
 }
 

@@ -69,9 +69,18 @@ __global__ void rmsnorm_kernel(const float* __restrict__ x, const float* __restr
     if (r >= *dM) return;
     const int src = gather ? gather[r] : r;
     const float* xr = x + (int64_t)src * H;
-    float ss = 0.f;
-    for (int i = threadIdx.x; i < H; i += blockDim.x) ss = fmaf(xr[i], xr[i], ss);
     __shared__ float red[32];
+    float ss = 0.f;
+    const bool vec = (H % 4) == 0;
+    if (vec) {
+        const float4* x4 = reinterpret_cast<const float4*>(xr);
+        for (int i = threadIdx.x; i < H / 4; i += blockDim.x) {
+            const float4 v = x4[i];
+            ss = fmaf(v.x, v.x, fmaf(v.y, v.y, fmaf(v.z, v.z, fmaf(v.w, v.w, ss))));
+        }
+    } else {
+        for (int i = threadIdx.x; i < H; i += blockDim.x) ss = fmaf(xr[i], xr[i], ss);
+    }
     for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
     if (lane_id() == 0) red[warp_id()] = ss;
     __syncthreads();
@@ -82,7 +91,20 @@ __global__ void rmsnorm_kernel(const float* __restrict__ x, const float* __restr
     }
     __syncthreads();
     const float inv = rsqrtf(red[0] / (float)H + eps);
-    for (int i = threadIdx.x; i < H; i += blockDim.x) stf(y, (int64_t)r * H + i, (xr[i] * inv) * w[i]);
+    if (vec) {
+        const float4* x4 = reinterpret_cast<const float4*>(xr);
+        const float4* w4 = reinterpret_cast<const float4*>(w);
+        for (int i = threadIdx.x; i < H / 4; i += blockDim.x) {
+            const float4 v = x4[i], g = w4[i];
+            const int64_t o = (int64_t)r * H + 4 * i;
+            stf(y, o, (v.x * inv) * g.x);
+            stf(y, o + 1, (v.y * inv) * g.y);
+            stf(y, o + 2, (v.z * inv) * g.z);
+            stf(y, o + 3, (v.w * inv) * g.w);
+        }
+    } else {
+        for (int i = threadIdx.x; i < H; i += blockDim.x) stf(y, (int64_t)r * H + i, (xr[i] * inv) * w[i]);
+    }
 }
 
 // ---------------------------------------------------------------- rope + kv write
@@ -462,7 +484,9 @@ __global__ void __launch_bounds__(256) topk_partial_kernel(const float* __restri
     pdl_trigger();  // let the next kernel start its prologue
     const int r = blockIdx.x, sp = blockIdx.y;
     if (r >= *dM) return;
-    const int lo = (int)((int64_t)V * sp / S), hi = (int)((int64_t)V * (sp + 1) / S);
+    // split boundaries on 4-element multiples so slices stay float4-aligned
+    const int lo = (int)(((int64_t)V * sp / S) & ~3LL);
+    const int hi = sp == S - 1 ? V : (int)(((int64_t)V * (sp + 1) / S) & ~3LL);
     const float* lr = logits + (int64_t)r * V;
     float tv[KT];
     int tt[KT];
@@ -472,8 +496,7 @@ __global__ void __launch_bounds__(256) topk_partial_kernel(const float* __restri
         tt[j] = 0x7fffffff;
     }
     float mx = -INFINITY, sum = 0.f;
-    for (int i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-        const float v = lr[i] * inv_temp;
+    auto consume = [&](float v, int i) {
         if (v > mx) {
             sum = sum * __expf(mx - v) + 1.f;
             mx = v;
@@ -494,7 +517,38 @@ __global__ void __launch_bounds__(256) topk_partial_kernel(const float* __restri
                 ci = b ? oi : ci;
             }
         }
+    };
+    // aligned float4 body (4 vectors in flight per thread), scalar head/tail
+    int a0 = lo, a1 = hi;
+    if (((uintptr_t)(lr + lo) & 15) == 0 && ((int64_t)r * V) % 4 == 0) {
+        const int nv = (hi - lo) / 4;
+        const float4* l4 = reinterpret_cast<const float4*>(lr + lo);
+        int vi = threadIdx.x;
+        for (; vi + 3 * (int)blockDim.x < nv; vi += 4 * blockDim.x) {
+            float4 q[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) q[u] = __ldg(l4 + vi + u * blockDim.x);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int i = lo + 4 * (vi + u * blockDim.x);
+                consume(q[u].x * inv_temp, i);
+                consume(q[u].y * inv_temp, i + 1);
+                consume(q[u].z * inv_temp, i + 2);
+                consume(q[u].w * inv_temp, i + 3);
+            }
+        }
+        for (; vi < nv; vi += blockDim.x) {
+            const float4 q = __ldg(l4 + vi);
+            const int i = lo + 4 * vi;
+            consume(q.x * inv_temp, i);
+            consume(q.y * inv_temp, i + 1);
+            consume(q.z * inv_temp, i + 2);
+            consume(q.w * inv_temp, i + 3);
+        }
+        a0 = lo + 4 * nv;
+        a1 = hi;
     }
+    for (int i = a0 + threadIdx.x; i < a1; i += blockDim.x) consume(lr[i] * inv_temp, i);
     // block reduction: max/sum then KT rounds of arg-best
     __shared__ float sm_m[8], sm_s[8], bv[8];
     __shared__ int bt[8], bw[8];
@@ -619,17 +673,47 @@ __global__ void __launch_bounds__(256) argmax_partial_kernel(const float* __rest
     pdl_trigger();  // let the next kernel start its prologue
     const int r = blockIdx.x, sp = blockIdx.y;
     if (r >= *dM) return;
-    const int lo = (int)((int64_t)V * sp / S), hi = (int)((int64_t)V * (sp + 1) / S);
+    // split boundaries on 4-element multiples so slices stay float4-aligned
+    const int lo = (int)(((int64_t)V * sp / S) & ~3LL);
+    const int hi = sp == S - 1 ? V : (int)(((int64_t)V * (sp + 1) / S) & ~3LL);
     const float* lr = logits + (int64_t)r * V;
     float bv = -INFINITY;
     int bi = 0x7fffffff;
-    for (int i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-        const float v = lr[i];
-        if (v > bv) {   // ascending strided scan: first max per thread
+    auto take = [&](float v, int i) {
+        if (v > bv || (v == bv && i < bi)) {
             bv = v;
             bi = i;
         }
+    };
+    int a0 = lo;
+    if (((uintptr_t)(lr + lo) & 15) == 0) {
+        const int nv = (hi - lo) / 4;
+        const float4* l4 = reinterpret_cast<const float4*>(lr + lo);
+        int vi = threadIdx.x;
+        for (; vi + 3 * (int)blockDim.x < nv; vi += 4 * blockDim.x) {
+            float4 q[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) q[u] = __ldg(l4 + vi + u * blockDim.x);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int i = lo + 4 * (vi + u * blockDim.x);
+                take(q[u].x, i);
+                take(q[u].y, i + 1);
+                take(q[u].z, i + 2);
+                take(q[u].w, i + 3);
+            }
+        }
+        for (; vi < nv; vi += blockDim.x) {
+            const float4 q = __ldg(l4 + vi);
+            const int i = lo + 4 * vi;
+            take(q.x, i);
+            take(q.y, i + 1);
+            take(q.z, i + 2);
+            take(q.w, i + 3);
+        }
+        a0 = lo + 4 * nv;
     }
+    for (int i = a0 + threadIdx.x; i < hi; i += blockDim.x) take(lr[i], i);
     for (int o = 16; o > 0; o >>= 1) {
         const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
         const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
