@@ -173,6 +173,8 @@ int card_linear_create(const void* W, int N, int K, int wdtype, const void* X, i
                        void* out, int ldo, const float* bias, card_linear** out_h);
 int card_linear_run(card_linear* h, const int32_t* dM, void* stream);
 int card_linear_info(card_linear* h, int32_t* info8);
+/* tuning: per-CTA %globaltimer stamps [grid][16] (NULL disables) */
+int card_linear_trace(card_linear* h, unsigned long long* trace);
 int card_linear_destroy(card_linear* h);
 
 int card_embed(const int32_t* tok, const int32_t* dM, int m_max, const void* E, int wdtype, int H,

@@ -55,6 +55,7 @@ SIGNATURES = {
     "card_linear_create": (c_int, [_P, c_int, c_int, c_int, _P, c_int, c_int, _P, c_int, _P, POINTER(c_void_p)]),
     "card_linear_run": (c_int, [_P, _P, _P]),
     "card_linear_info": (c_int, [_P, _P]),
+    "card_linear_trace": (c_int, [_P, _P]),
     "card_linear_destroy": (c_int, [_P]),
     "card_embed": (c_int, [_P, _P, c_int, _P, c_int, c_int, _P, _P]),
     "card_rmsnorm": (c_int, [_P, _P, c_int, ctypes.c_float, _P, c_int, _P, _P, c_int, _P]),

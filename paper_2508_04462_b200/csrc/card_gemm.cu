@@ -8,9 +8,10 @@
 //     elected thread issues tcgen05.mma kind::f16 (A = weights, K-major,
 //     SWIZZLE_128B; B = activations) into a TMEM accumulator (128 lanes x
 //     Mpad fp32 columns, double-buffered); four epilogue warps drain TMEM
-//     with tcgen05.ld and apply the fused epilogue.  Persistent CTAs walk
-//     (tile, k-split) work items; split partials are reduced in a fixed
-//     order by the last-arriving CTA (deterministic).
+//     with tcgen05.ld and apply the fused epilogue.  Either persistent CTAs
+//     walk whole tiles (wide N), or the K range of each tile is split over
+//     the S ranks of a thread-block cluster whose partial sums are reduced
+//     through distributed shared memory in rank order (deterministic).
 //   * gemv      (bf16 weights, M == 1): 128-bit vectorised weight loads,
 //     one warp per output row group, fp32 accumulation.
 //   * f32_gemm  (fp32 weights — the parity mode against the CPU oracle).
@@ -112,21 +113,9 @@ __device__ __forceinline__ uint32_t dsmem_addr(uint32_t local, uint32_t rank) {
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local), "r"(rank));
     return r;
 }
-__device__ __forceinline__ float dsmem_ld(uint32_t addr) {
+__device__ __forceinline__ float lds_f32(uint32_t addr) {
     float v;
-    asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(addr));
-    return v;
-}
-// sum over the S cluster ranks of the float at byte offset `off` of each
-// rank's staging buffer: all S remote loads are issued before the first add
-// (in-order issue would otherwise serialise them), summed in rank order.
-__device__ __forceinline__ float dsmem_sum(const uint32_t* bases, int S, uint32_t off) {
-    float t[16];
-#pragma unroll
-    for (int q = 0; q < 16; ++q) t[q] = q < S ? dsmem_ld(bases[q] + off) : 0.f;
-    float v = 0.f;
-#pragma unroll
-    for (int q = 0; q < 16; ++q) v += t[q];
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
     return v;
 }
 
@@ -136,6 +125,16 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
     return (uint64_t)((saddr & 0x3FFFF) >> 4) | ((uint64_t)1 << 16) | ((uint64_t)64 << 32) | ((uint64_t)1 << 46) |
            ((uint64_t)2 << 61);
 }
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define TC_STAMP(k) \
+    do {            \
+        if (a.trace) a.trace[blockIdx.x * 16 + (k)] = gtimer(); \
+    } while (0)
 
 __device__ __forceinline__ float silu(float x) { return x / (1.0f + __expf(-x)); }
 
@@ -152,36 +151,39 @@ struct TcArgs {
     const int32_t* dM;
     const uint8_t* w_tiled;   // non-null: [n_tiles][kb_total][128 x 128 B] pre-swizzled blocks
     int epi;
-    int cluster;      // > 1: split-K over a thread-block cluster, DSMEM reduction
+    int cluster;      // == splits: split-K over a thread-block cluster, DSMEM reduction
     float* out_f32;
     __nv_bfloat16* out_bf16;
     const float* bias;
     int ldo;
-    float* ws;
-    int32_t* counters;
+    unsigned long long* trace;   // optional [grid][16] %globaltimer stamps (tuning)
 };
 
 // Epilogue for one 16-column chunk (tokens m0..m0+mc) of output row n_glob.
-// All loads of a chunk are issued before any store so they overlap.
+// All loads of a chunk are issued before any store so they overlap.  xch is
+// the shared-memory address of a [16][64] fp32 exchange buffer (SwiGLU).
+__device__ __forceinline__ void sts_f32(uint32_t addr, float v) {
+    asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
+}
 template <int EPI>
 __device__ __forceinline__ void epi_chunk(const TcArgs& a, int tile, int n_glob, int n_local, int m0, int mc,
-                                          float* v, float* xch) {
+                                          float* v, uint32_t xch) {
     const float b = a.bias ? a.bias[n_glob] : 0.f;
     if (EPI == EPI_SWIGLU_BF16) {
-        // rows [0,64) of a tile are gates, [64,128) the matching ups (xch: [16][64])
+        // rows [0,64) of a tile are gates, [64,128) the matching ups
         if (n_local >= 64)
 #pragma unroll
             for (int j = 0; j < 16; ++j)
-                if (j < mc) xch[j * 64 + (n_local - 64)] = v[j] + b;
+                if (j < mc) sts_f32(xch + (uint32_t)((j * 64 + (n_local - 64)) * 4), v[j] + b);
         named_bar(1, kEpiThreads);
         if (n_local < 64) {
             const int f = tile * 64 + n_local;
+            float u[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) u[j] = j < mc ? lds_f32(xch + (uint32_t)((j * 64 + n_local) * 4)) : 0.f;
 #pragma unroll
             for (int j = 0; j < 16; ++j)
-                if (j < mc) {
-                    const float g = v[j] + b, u = xch[j * 64 + n_local];
-                    a.out_bf16[(int64_t)(m0 + j) * a.ldo + f] = __float2bfloat16(silu(g) * u);
-                }
+                if (j < mc) a.out_bf16[(int64_t)(m0 + j) * a.ldo + f] = __float2bfloat16(silu(v[j] + b) * u[j]);
         }
         named_bar(1, kEpiThreads);
         return;
@@ -203,13 +205,6 @@ __device__ __forceinline__ void epi_chunk(const TcArgs& a, int tile, int n_glob,
     }
 }
 
-// gpu-scope release/acquire add on the per-tile split counter
-__device__ __forceinline__ int atom_add_acq_rel(int* p, int v) {
-    int old;
-    asm volatile("atom.add.acq_rel.gpu.global.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
-    return old;
-}
-
 template <int EPI>
 __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_constant__ CUtensorMap tmW,
                                                                const __grid_constant__ CUtensorMap tmX, TcArgs a) {
@@ -227,9 +222,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
     uint64_t* tempty = tfull + 2;   // [2]
     uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
     float* xch = (float*)(tmem_slot + 4);   // [16][64]
-    int* sh_last = (int*)(xch + 16 * 64);
 
     const int warp = warp_id(), lane = lane_id();
+    if (threadIdx.x == 0) TC_STAMP(0);
     if (warp == 4 && lane == 0) {
         for (int i = 0; i < S; ++i) {
             mbar_init(&full[i], 1);
@@ -271,6 +266,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
     }
     pdl_wait();
     pdl_trigger();
+    if (threadIdx.x == 0) TC_STAMP(1);
     const int M = *a.dM;
     const int m_rt = M < 1 ? 1 : M;
     const int n_mma = ((m_rt + 15) / 16) * 16;   // runtime MMA N (tokens), <= Mpad
@@ -333,6 +329,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
                 const uint32_t d_tmem = tmem_base + (uint32_t)(acc * a.Mpad);
                 for (int kb = kb0; kb < kb1; ++kb) {
                     mbar_wait(&full[stage], phase);
+                    if (kb == kb0) TC_STAMP(2);
                     tc_fence_after();
                     const uint32_t a0 = smem_u32(sA + (size_t)stage * bytesA);
                     const uint32_t b0 = smem_u32(sB + (size_t)stage * bytesB);
@@ -347,6 +344,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
                         phase ^= 1;
                     }
                 }
+                TC_STAMP(3);
                 tc_commit(&tfull[acc]);   // accumulator ready for the epilogue
                 if (a.n_acc_buf == 2) {
                     acc ^= 1;
@@ -375,29 +373,21 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
                     : "=r"(ok)
                     : "r"(smem_u32(&tfull[acc])), "r"(acc_phase)
                     : "memory");
-                if (ok) break;
+                if (ok) {
+                    if (threadIdx.x == 0) TC_STAMP(4);
+                    break;
+                }
                 __nanosleep(128);
             }
             tc_fence_after();
             const uint32_t trow = tmem_base + ((uint32_t)(warp * 32) << 16) + (uint32_t)(acc * a.Mpad);
-            const bool direct = a.splits == 1;
-            float* wsp = a.ws + (size_t)item * kTileN * a.Mpad;
-            float* red = reinterpret_cast<float*>(sA);   // cluster mode: [Mpad][128] partial in own smem
-            for (int m0 = 0; m0 < M; m0 += 16) {
+            // cluster mode (splits > 1): the accumulator stays in TMEM until
+            // every rank of the cluster has finished its main loop (below)
+            for (int m0 = 0; m0 < M && a.splits == 1; m0 += 16) {
                 float v[16];
                 tmem_ld16(trow + (uint32_t)m0, v);
                 const int mc = (M - m0) < 16 ? (M - m0) : 16;
-                if (direct) {
-                    epi_chunk<EPI>(a, tile, n_glob, n_local, m0, mc, v, xch);
-                } else if (a.cluster > 1) {
-#pragma unroll
-                    for (int j = 0; j < 16; ++j)
-                        if (j < mc) red[(m0 + j) * kTileN + n_local] = v[j];
-                } else {
-#pragma unroll
-                    for (int j = 0; j < 16; ++j)
-                        if (j < mc) __stcg(wsp + (size_t)(m0 + j) * kTileN + n_local, v[j]);
-                }
+                epi_chunk<EPI>(a, tile, n_glob, n_local, m0, mc, v, smem_u32(xch));
             }
             tc_fence_before();
             __syncwarp();
@@ -408,78 +398,101 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
             } else {
                 acc_phase ^= 1;
             }
-            if (!direct && a.cluster <= 1) {
-                // deterministic split-K fixup: the last arriver sums splits 0..S-1 in order.
-                // bar.sync orders this CTA's partial stores before thread 0's release.
-                named_bar(1, kEpiThreads);
-                if (n_local == 0) {
-                    const int prev = atom_add_acq_rel(&a.counters[tile], 1);
-                    *sh_last = (prev == a.splits - 1);
-                    if (prev == a.splits - 1) a.counters[tile] = 0;   // reusable next launch / graph replay
-                }
-                named_bar(1, kEpiThreads);
-                if (*sh_last) {
-                    const float* base = a.ws + (size_t)tile * a.splits * kTileN * a.Mpad;
-                    for (int m0 = 0; m0 < M; m0 += 16) {
-                        const int mc = (M - m0) < 16 ? (M - m0) : 16;
-                        float v[16];
-#pragma unroll
-                        for (int j = 0; j < 16; ++j) v[j] = 0.f;
-                        for (int sp = 0; sp < a.splits; ++sp) {
-                            const float* p = base + ((size_t)sp * a.Mpad + m0) * kTileN + n_local;
-                            float t[16];
-#pragma unroll
-                            for (int j = 0; j < 16; ++j) t[j] = j < mc ? __ldcg(p + (size_t)j * kTileN) : 0.f;
-#pragma unroll
-                            for (int j = 0; j < 16; ++j) v[j] += t[j];
-                        }
-                        epi_chunk<EPI>(a, tile, n_glob, n_local, m0, mc, v, xch);
-                    }
-                }
-            }
         }
     }
     if (a.cluster > 1) {
-        // split-K over the cluster: every CTA staged its partial tile in smem;
-        // rank r reduces a slice of the tile's rows over all ranks (DSMEM) in
-        // rank order (deterministic) and applies the epilogue.
+        // split-K over the cluster (S = a.cluster ranks = the K-slices of one
+        // tile).  Push-based DSMEM reduction: rank r owns R = 128/S rows of the
+        // tile (for SwiGLU: 64/S features = their gate and up rows).  After
+        // barrier 1 every rank's pipeline smem is free; each epilogue thread
+        // (one tile row) stores its Mpad partial sums into the owner's smem
+        // with 16-byte st.shared::cluster (fire-and-forget, no round trips).
+        // After barrier 2 each owner sums its S slices in rank order
+        // (deterministic) from local smem and applies the epilogue.
+        const int S = a.cluster;
+        const int R = kTileN / S;
+        const int ld = a.Mpad + 4;   // padded slice row (floats): spreads banks
+        float* buf = reinterpret_cast<float*>(smem);   // [S][R][ld] over the stage buffers
         cluster_sync_all();
+        if (threadIdx.x == 0) TC_STAMP(5);
         if (warp < 4 && M > 0) {
-            const int S = a.cluster;
+            const int me = (int)cluster_rank();
+            const int n_local = warp * 32 + lane;
+            int owner, lr;
+            if (EPI == EPI_SWIGLU_BF16) {
+                const int f = n_local & 63, Rf = 64 / S;
+                owner = f / Rf;
+                lr = (f - owner * Rf) + (n_local >= 64 ? Rf : 0);
+            } else {
+                owner = n_local / R;
+                lr = n_local - owner * R;
+            }
+            const uint32_t dst = dsmem_addr(smem_u32(buf), (uint32_t)owner) + (uint32_t)(((me * R + lr) * ld) * 4);
+            const uint32_t trow = tmem_base + ((uint32_t)(warp * 32) << 16);
+            for (int m0 = 0; m0 < M; m0 += 16) {
+                float v[16];
+                tmem_ld16(trow + (uint32_t)m0, v);
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(dst + (uint32_t)((m0 + 4 * q) * 4)),
+                                 "f"(v[4 * q]), "f"(v[4 * q + 1]), "f"(v[4 * q + 2]), "f"(v[4 * q + 3])
+                                 : "memory");
+            }
+        }
+        if (threadIdx.x == 0) TC_STAMP(6);
+        cluster_sync_all();   // all pushes landed; no remote access after this point
+        if (threadIdx.x == 0) TC_STAMP(7);
+        if (warp < 4 && M > 0) {
+            // owner reduction: thread -> (output row j, token stripe); RJ outputs
+            // per token (R rows, or R/2 gate/up feature pairs for SwiGLU), TP
+            // token lanes; B tokens per pass with every load issued first.
             const int r = (int)cluster_rank();
             const int tile = blockIdx.x / S;
-            const uint32_t red_local = smem_u32(sA);
-            const int tid = threadIdx.x;
-            uint32_t bases[16];
+            const uint32_t sbuf = smem_u32(buf);
+            const int RJ = (EPI == EPI_SWIGLU_BF16) ? R / 2 : R;
+            const int TP = kEpiThreads / RJ;
+            const int j = threadIdx.x % RJ, m_first = threadIdx.x / RJ;
+            const int f_out = (EPI == EPI_SWIGLU_BF16) ? tile * 64 + r * RJ + j : tile * kTileN + r * R + j;
+            const float bias0 = a.bias ? a.bias[(EPI == EPI_SWIGLU_BF16) ? tile * kTileN + r * RJ + j : f_out] : 0.f;
+            const float bias1 = (a.bias && EPI == EPI_SWIGLU_BF16) ? a.bias[tile * kTileN + 64 + r * RJ + j] : 0.f;
+            constexpr int B = 8;
+            for (int mb = m_first; mb < M; mb += TP * B) {
+                float v0[B], v1[B], old[B];
 #pragma unroll
-            for (int q = 0; q < 16; ++q) bases[q] = q < S ? dsmem_addr(red_local, (uint32_t)q) : 0u;
-            if (EPI == EPI_SWIGLU_BF16) {
-                const int f0 = 64 * r / S, f1 = 64 * (r + 1) / S, w = f1 - f0;
-                for (int e = tid; e < w * M; e += kEpiThreads) {
-                    const int m = e / w, f = f0 + e % w;
-                    float g = dsmem_sum(bases, S, (uint32_t)((m * kTileN + f) * 4));
-                    float u = dsmem_sum(bases, S, (uint32_t)((m * kTileN + 64 + f) * 4));
-                    if (a.bias) {
-                        g += a.bias[tile * kTileN + f];
-                        u += a.bias[tile * kTileN + 64 + f];
-                    }
-                    a.out_bf16[(int64_t)m * a.ldo + tile * 64 + f] = __float2bfloat16(silu(g) * u);
+                for (int q = 0; q < B; ++q) {
+                    v0[q] = 0.f;
+                    v1[q] = 0.f;
+                    old[q] = 0.f;
+                    const int m = mb + q * TP;
+                    if (EPI == EPI_RESID_F32 && m < M) old[q] = a.out_f32[(int64_t)m * a.ldo + f_out];
                 }
-            } else {
-                const int n0 = kTileN * r / S, n1 = kTileN * (r + 1) / S, w = n1 - n0;
-                for (int e = tid; e < w * M; e += kEpiThreads) {
-                    const int m = e / w, n = n0 + e % w;
-                    float v = dsmem_sum(bases, S, (uint32_t)((m * kTileN + n) * 4));
-                    const int ng = tile * kTileN + n;
-                    if (a.bias) v += a.bias[ng];
-                    if (EPI == EPI_STORE_F32) a.out_f32[(int64_t)m * a.ldo + ng] = v;
-                    else if (EPI == EPI_RESID_F32) a.out_f32[(int64_t)m * a.ldo + ng] += v;
-                    else a.out_bf16[(int64_t)m * a.ldo + ng] = __float2bfloat16(v);
+                for (int sl = 0; sl < S; ++sl) {
+                    const uint32_t row0 = sbuf + (uint32_t)(((sl * R + j) * ld) * 4);
+                    const uint32_t row1 = sbuf + (uint32_t)(((sl * R + RJ + j) * ld) * 4);
+#pragma unroll
+                    for (int q = 0; q < B; ++q) {
+                        const int m = mb + q * TP;
+                        if (m < M) {
+                            v0[q] += lds_f32(row0 + (uint32_t)(m * 4));
+                            if (EPI == EPI_SWIGLU_BF16) v1[q] += lds_f32(row1 + (uint32_t)(m * 4));
+                        }
+                    }
+                }
+#pragma unroll
+                for (int q = 0; q < B; ++q) {
+                    const int m = mb + q * TP;
+                    if (m >= M) continue;
+                    const float x = v0[q] + bias0;
+                    if (EPI == EPI_SWIGLU_BF16)
+                        a.out_bf16[(int64_t)m * a.ldo + f_out] = __float2bfloat16(silu(x) * (v1[q] + bias1));
+                    else if (EPI == EPI_STORE_F32) a.out_f32[(int64_t)m * a.ldo + f_out] = x;
+                    else if (EPI == EPI_RESID_F32) a.out_f32[(int64_t)m * a.ldo + f_out] = old[q] + x;
+                    else a.out_bf16[(int64_t)m * a.ldo + f_out] = __float2bfloat16(x);
                 }
             }
         }
-        cluster_sync_all();   // peers may not exit while their smem is being read
     }
+    if (threadIdx.x == 0) TC_STAMP(8);
     tc_fence_before();
     __syncthreads();
     if (warp == 0) {
@@ -712,18 +725,37 @@ static cudaError_t launch_tc(const card_linear* h, const TcArgs& a, cudaStream_t
     return cudaLaunchKernelEx(&cfg, tc_gemm_kernel<EPI>, h->tmW, h->tmX, a);
 }
 
-// Split choice (calibrated on B200 with tools/split_sweep.sh): a work item
-// carries a large fixed cost (~9 us: pipeline ramp, TMEM drain, fixup), so
-// items should be long — just enough of them to cover ~80% of the resident
-// CTA slots — and the split partial traffic (write + read, 2*128*Mpad*4 B
-// per split) must stay <= 1/4 of the tile's weight bytes (128*K*2 B).
-static int choose_splits(int n_tiles, int kb_total, int Mpad, int slots) {
-    int s = (int)(0.8 * slots / n_tiles + 0.5);
-    int max_s = (kb_total * kBK) / (16 * Mpad);
-    if (s > max_s) s = max_s;
-    if (s > kb_total) s = kb_total;
-    if (s > 32) s = 32;
-    return s < 1 ? 1 : s;
+// Cluster split-K choice.  Wide N (>= half the resident CTA slots in
+// tiles): S = 1, persistent CTAs walk whole tiles.  Otherwise the K range of
+// each tile is split over S in {2, 4, 8} cluster ranks (S divides the 128
+// tile rows for the DSMEM reduction), the largest S such that every cluster
+// is resident at once (one wave) and the [128][Mpad+4] fp32 reduction
+// buffer fits in the freed pipeline stages.
+template <int EPI>
+static int choose_cluster(int n_tiles, int kb_total, int Mpad, int slots, int smem, int stage_smem) {
+    if (getenv("CARD_NO_CLUSTER") || 2 * n_tiles > slots) return 1;
+    int S = 8;
+    while (S > 1 && (n_tiles * S > slots || S > kb_total || (size_t)kTileN * (Mpad + 4) * 4 > (size_t)stage_smem))
+        S >>= 1;
+    if (getenv("CARD_SPLITS")) S = atoi(getenv("CARD_SPLITS"));   // tuning knob (must divide 128)
+    while (S > 1) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(n_tiles * S);
+        cfg.blockDim = dim3(kTcThreads);
+        cfg.dynamicSmemBytes = smem;
+        cudaLaunchAttribute attr;
+        attr.id = cudaLaunchAttributeClusterDimension;
+        attr.val.clusterDim.x = S;
+        attr.val.clusterDim.y = 1;
+        attr.val.clusterDim.z = 1;
+        cfg.attrs = &attr;
+        cfg.numAttrs = 1;
+        int nc = 0;
+        if (cudaOccupancyMaxActiveClusters(&nc, tc_gemm_kernel<EPI>, &cfg) == cudaSuccess && nc >= n_tiles) break;
+        cudaGetLastError();
+        S >>= 1;
+    }
+    return S < 1 ? 1 : S;
 }
 
 }  // namespace card
@@ -805,7 +837,8 @@ int card_linear_create(const void* W, int N, int K, int wdtype, const void* X, i
     int ctas_per_sm = (cols <= 256) ? 2 : 1;
     if (getenv("CARD_CTAS_PER_SM")) ctas_per_sm = atoi(getenv("CARD_CTAS_PER_SM"));   // tuning knob
     const int stage_bytes = kTileN * kBK * 2 + Mpad * kBK * 2;
-    const int budget = (ctas_per_sm == 2 ? 110 : 220) * 1024;
+    int budget = (ctas_per_sm == 2 ? 110 : 220) * 1024;
+    if (getenv("CARD_GEMM_SMEM_KB")) budget = atoi(getenv("CARD_GEMM_SMEM_KB")) * 1024;   // tuning knob
     const int extra = 1024 + 64 * 8 + 16 * 64 * 4 + 64;
     int stages = (budget - extra) / stage_bytes;
     if (stages > 8) stages = 8;
@@ -813,37 +846,6 @@ int card_linear_create(const void* W, int N, int K, int wdtype, const void* X, i
     a.stages = stages;
     h->smem = stages * stage_bytes + extra;
     const int slots = num_sms() * ctas_per_sm;
-    a.splits = choose_splits(a.n_tiles, a.kb_total, Mpad, slots);
-    a.cluster = 1;
-    // cluster split-K when the tiles alone leave SMs idle: one item per CTA,
-    // the S K-slices of a tile form a cluster and reduce through DSMEM
-    // (measured: a win for the wide draft tiles, a loss for Mpad=16 verify tiles)
-    if (!getenv("CARD_NO_CLUSTER") && Mpad >= 64 && 2 * a.n_tiles <= slots) {
-        int S = slots / a.n_tiles;
-        if (S > 16) S = 16;
-        if (S > a.kb_total) S = a.kb_total;
-        while (S > 1 && (size_t)Mpad * kTileN * 4 > (size_t)stages * (kTileN * kBK * 2 + Mpad * kBK * 2)) --S;
-        if (S > 1) {
-            a.splits = S;
-            a.cluster = S;
-        }
-    }
-    if (getenv("CARD_SPLITS")) a.splits = atoi(getenv("CARD_SPLITS"));   // tuning knob
-    if (a.cluster > 1) a.cluster = a.splits;
-    a.items = a.n_tiles * a.splits;
-    h->grid = a.items < slots ? a.items : slots;
-    if (a.cluster > 1) h->grid = a.items;
-    if (a.splits > 1 && a.cluster <= 1) {
-        CARD_CUDA_TRY(cudaMalloc(&a.ws, (size_t)a.items * kTileN * Mpad * 4));
-        CARD_CUDA_TRY(cudaMalloc(&a.counters, (size_t)a.n_tiles * 4));
-        CARD_CUDA_TRY(cudaMemset(a.counters, 0, (size_t)a.n_tiles * 4));
-    }
-    int rc = tiled ? CARD_OK : make_map_bf16(&h->tmW, W, (uint64_t)N, (uint64_t)K, kTileN, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
-    if (!rc) rc = make_map_bf16(&h->tmX, X, (uint64_t)Mpad, (uint64_t)K, (uint32_t)Mpad, CU_TENSOR_MAP_L2_PROMOTION_L2_128B);
-    if (rc) {
-        free(h);
-        return rc;
-    }
     cudaError_t e;
     switch (epi) {
         case EPI_STORE_F32: e = set_tc_attr<EPI_STORE_F32>(h->smem); break;
@@ -856,6 +858,28 @@ int card_linear_create(const void* W, int N, int K, int wdtype, const void* X, i
         set_cuda_error(e);
         free(h);
         return CARD_E_CUDA;
+    }
+    const int stage_smem = stages * stage_bytes;
+    int S = 1;
+    switch (epi) {
+        case EPI_STORE_F32: S = choose_cluster<EPI_STORE_F32>(a.n_tiles, a.kb_total, Mpad, slots, h->smem, stage_smem); break;
+        case EPI_RESID_F32: S = choose_cluster<EPI_RESID_F32>(a.n_tiles, a.kb_total, Mpad, slots, h->smem, stage_smem); break;
+        case EPI_STORE_BF16: S = choose_cluster<EPI_STORE_BF16>(a.n_tiles, a.kb_total, Mpad, slots, h->smem, stage_smem); break;
+        case EPI_SWIGLU_BF16: S = choose_cluster<EPI_SWIGLU_BF16>(a.n_tiles, a.kb_total, Mpad, slots, h->smem, stage_smem); break;
+    }
+    if (S > 1 && (kTileN % S != 0 || (size_t)kTileN * (Mpad + 4) * 4 > (size_t)stage_smem)) {
+        free(h);
+        return CARD_E_CONFIG;
+    }
+    a.splits = S;
+    a.cluster = S;
+    a.items = a.n_tiles * a.splits;
+    h->grid = S > 1 ? a.items : (a.items < slots ? a.items : slots);
+    int rc = tiled ? CARD_OK : make_map_bf16(&h->tmW, W, (uint64_t)N, (uint64_t)K, kTileN, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
+    if (!rc) rc = make_map_bf16(&h->tmX, X, (uint64_t)Mpad, (uint64_t)K, (uint32_t)Mpad, CU_TENSOR_MAP_L2_PROMOTION_L2_128B);
+    if (rc) {
+        free(h);
+        return rc;
     }
     *out_h = h;
     return CARD_OK;
@@ -908,6 +932,12 @@ int card_linear_run(card_linear* h, const int32_t* dM, void* stream) {
     return CARD_OK;
 }
 
+int card_linear_trace(card_linear* h, unsigned long long* trace) {
+    if (!h) return CARD_E_INPUT;
+    h->args.trace = trace;
+    return CARD_OK;
+}
+
 int card_linear_info(card_linear* h, int32_t* info8) {
     if (!h || !info8) return CARD_E_INPUT;
     info8[0] = h->kind;
@@ -923,8 +953,6 @@ int card_linear_info(card_linear* h, int32_t* info8) {
 
 int card_linear_destroy(card_linear* h) {
     if (!h) return CARD_OK;
-    if (h->args.ws) cudaFree(h->args.ws);
-    if (h->args.counters) cudaFree(h->args.counters);
     if (h->scratch) cudaFree(h->scratch);
     free(h);
     return CARD_OK;

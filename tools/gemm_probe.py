@@ -5,7 +5,7 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 
-from paper_2508_04462_b200.llama import _Linear
+from paper_2508_04462_b200.llama import _Linear, tile_sw128
 
 N, K, M, epi = (int(x) for x in sys.argv[1:5])
 reps = int(sys.argv[5]) if len(sys.argv) > 5 else 3
@@ -14,7 +14,8 @@ mpad = ((M + 15) // 16) * 16
 X = torch.randn(mpad, K, device="cuda").to(torch.bfloat16)
 out = torch.zeros(mpad, N if epi != 3 else N // 2, device="cuda", dtype=torch.float32 if epi < 2 else torch.bfloat16)
 dM = torch.tensor([M], dtype=torch.int32, device="cuda")
-lin = _Linear(W, X, M, epi, out, out.shape[1])
+Wl = W if os.environ.get("ROWMAJOR") else tile_sw128(W)   # production layout: pre-tiled SW128
+lin = _Linear(Wl, X, M, epi, out, out.shape[1])
 print(lin.info)
 for _ in range(reps):
     lin.run(dM)

@@ -89,7 +89,17 @@ def bench_model(name, preset, m_rows, ctx_len):
         rt.forward(rows, m_rows)
     torch.cuda.current_stream().wait_stream(st)
     t_g = timeit(lambda: g.replay(), reps=10)
+    # GEMM-only graph: the same 4*L+1 linears in forward order, nothing else
+    lins = [L[k] for L in plan["layers"] for k in ("qkv", "o", "gu", "d")]
+    g2 = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(st), torch.cuda.graph(g2, stream=st):
+        for lin in lins:
+            lin.run(dM)
+        plan["lm_head"].run(rows.n_out)
+    torch.cuda.current_stream().wait_stream(st)
+    t_g2 = timeit(lambda: g2.replay(), reps=10)
     sb = cfg.stream_params() * 2
+    print(f"  GEMM-only graph {t_g2:.3f} ms -> {sb/t_g2/1e6:.0f} GB/s; non-GEMM share of forward {t_g - t_g2:.3f} ms")
     print(f"  full forward {t_fwd:.3f} ms   graph replay {t_g:.3f} ms  -> {sb/t_g/1e6:.0f} GB/s weight stream "
           f"({sb/t_g/1e6/PEAK*100:.1f}% of {PEAK:.0f})")
     del rt, m
