@@ -1,0 +1,368 @@
+// card_attn.cu — one-launch attention for the draft tree forward and the
+// target chain verify (bf16 KV, head_dim 64 / 128).
+//
+// Every query row r attends to the prefix KV slots [0, plen[r]) plus
+// n_extra[r] listed slots (its tree ancestors and itself) — the tree mask of
+// mask.py:173-217 without materialising it.  Causal chains (verify, draft
+// catch-up, prefill) have plen = pos + 1 and no extras.
+//
+// Grid (S, n_qt, nkv), thread-block cluster (S, 1, 1):
+//   * z = kv head g; y = tile of 64 query-heads (row r, head h in g's GQA
+//     group, ordered (r, h)); x = cluster rank: rank s owns prefix chunks
+//     s, s+S, ... (64 keys each).
+//   * Each warp keeps 16 query-heads as bf16 mma.sync A fragments and runs a
+//     flash-style online softmax over the rank's chunks (K and V staged
+//     row-major by cp.async; V^T fragments via ldmatrix.trans).
+//   * Tree extras are more chunks: the tile rows' extra slots are gathered
+//     row after row into one key list; row i sees keys [xoff[i], xoff[i] +
+//     n_extra) of it.  Extra chunks are dealt to the ranks after the prefix
+//     chunks and use the same tensor-core path with a range mask.
+//   * Combine without a global round trip: every rank pushes its partial
+//     (m, l, o[HD]) into the owner rank's shared memory
+//     (st.shared::cluster); after one cluster barrier each owner merges its
+//     64/S query-heads in rank order and writes o (bf16) for the o-proj GEMM.
+// This replaces the split-KV partial round trip through HBM (the old
+// prefix + extra + combine kernels, kept for the fp32 parity path).
+#include <cuda_bf16.h>
+#include <math.h>
+
+#include "card_common.cuh"
+#include "card_llm.h"
+
+namespace card {
+
+namespace {
+
+constexpr int kCh = 64;      // keys per chunk
+constexpr int kQT = 64;      // query-heads per CTA (4 warps x 16)
+constexpr int kThreads = 128;
+constexpr int kMaxTileRows = 72;   // rows per tile of 64 query-heads (GQA group >= 1)
+constexpr int kMaxExtra = 1024;    // gathered extra slots per tile
+
+__device__ __forceinline__ uint32_t s_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ uint32_t pack2(float lo, float hi) {
+    __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+    return *reinterpret_cast<uint32_t*>(&v);
+}
+__device__ __forceinline__ void mma16816(float* c, const uint32_t* a, const uint32_t* b) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+}
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+__device__ __forceinline__ void ldsm_x4_trans(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(addr));
+}
+__device__ __forceinline__ void cl_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t cl_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ uint32_t cl_map(uint32_t local, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void st_cl_f32(uint32_t addr, float v) {
+    asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
+}
+__device__ __forceinline__ void st_cl_v2(uint32_t addr, float a, float b) {
+    asm volatile("st.shared::cluster.v2.f32 [%0], {%1, %2};" ::"r"(addr), "f"(a), "f"(b) : "memory");
+}
+
+}  // namespace
+
+// smem: K[kCh][HD+8] bf16 | V[kCh][HD+8] bf16 | recv[S][kQT/S][HD+2] f32
+template <int HD>
+__global__ void __launch_bounds__(kThreads) attn_fused_kernel(const float* __restrict__ q, const int32_t* dM,
+                                                             const int32_t* __restrict__ plen,
+                                                             const int32_t* __restrict__ n_extra,
+                                                             const int32_t* __restrict__ extra, int extra_max,
+                                                             const __nv_bfloat16* __restrict__ kc,
+                                                             const __nv_bfloat16* __restrict__ vc, int nh, int nkv,
+                                                             __nv_bfloat16* __restrict__ o_out) {
+    constexpr int LD = HD + 8;   // padded bf16 row: 16-byte aligned, conflict-free 32-bit fragment loads
+    constexpr int PW = HD + 2;   // partial record: m, l, o[HD]
+    extern __shared__ __align__(16) uint8_t smem[];
+    __nv_bfloat16* Ks = reinterpret_cast<__nv_bfloat16*>(smem);
+    __nv_bfloat16* Vs = Ks + kCh * LD;
+    float* recv = reinterpret_cast<float*>(Vs + kCh * LD);
+
+    pdl_wait();
+    pdl_trigger();
+    const int S = gridDim.x;
+    const int rank = (int)cl_rank();
+    const int qt = blockIdx.y, g = blockIdx.z;
+    const int M = *dM;
+    const int G = nh / nkv;
+    const int nq = M * G;
+    const int q0 = qt * kQT;
+    if (q0 >= nq) return;   // the whole cluster shares qt: consistent early exit
+    const int QO = kQT / S;   // query-heads owned per rank in the combine
+    const int warp = warp_id(), lane = lane_id();
+    const int gq = lane >> 2, tq = lane & 3;
+
+    // keys needed by this tile: max plen over its rows (prefix chunks), and
+    // the tile rows' extra slots concatenated row by row (extra chunks: row
+    // i's keys are [xoff[i], xoff[i] + xne[i]) of the gathered list)
+    __shared__ int s_kmax, s_nx;
+    __shared__ int xoff[kMaxTileRows], xne[kMaxTileRows];
+    __shared__ int xs[kMaxExtra];
+    const int r0 = q0 / G, r1 = min(M - 1, (q0 + kQT - 1) / G);
+    if (threadIdx.x == 0) {
+        int kmax = 0, off = 0;
+        for (int i = 0; i <= r1 - r0; ++i) {
+            const int r = r0 + i;
+            kmax = max(kmax, plen[r]);
+            int ne = min(n_extra[r], extra_max);
+            ne = max(0, min(ne, kMaxExtra - off));
+            xoff[i] = off;
+            xne[i] = ne;
+            off += ne;
+        }
+        s_kmax = kmax;
+        s_nx = off;
+    }
+    __syncthreads();
+    for (int i = 0; i <= r1 - r0; ++i)
+        for (int j = threadIdx.x; j < xne[i]; j += kThreads) xs[xoff[i] + j] = extra[(int64_t)(r0 + i) * extra_max + j];
+    const int n_ch = (s_kmax + kCh - 1) / kCh;
+    const int n_xch = (s_nx + kCh - 1) / kCh;
+    const int n_all = n_ch + n_xch;
+
+    // this warp's 16 query-heads: rows a = gq, b = gq + 8
+    const int qa = q0 + warp * 16 + gq, qb = qa + 8;
+    const bool va = qa < nq, vb = qb < nq;
+    const int ra = va ? qa / G : 0, rb = vb ? qb / G : 0;
+    const int ha = g * G + (va ? qa % G : 0), hb = g * G + (vb ? qb % G : 0);
+    const int pla = va ? plen[ra] : 0, plb = vb ? plen[rb] : 0;
+    const int ia = ra - r0, ib = rb - r0;
+    const bool warp_live = (q0 + warp * 16) < nq;
+
+    uint32_t qf[HD / 16][4];
+    {
+        const float* qpa = q + ((int64_t)ra * nh + ha) * HD;
+        const float* qpb = q + ((int64_t)rb * nh + hb) * HD;
+#pragma unroll
+        for (int ks = 0; ks < HD / 16; ++ks) {
+            const int d0 = ks * 16 + 2 * tq;
+            const float2 a0 = va ? *reinterpret_cast<const float2*>(qpa + d0) : make_float2(0.f, 0.f);
+            const float2 b0 = vb ? *reinterpret_cast<const float2*>(qpb + d0) : make_float2(0.f, 0.f);
+            const float2 a1 = va ? *reinterpret_cast<const float2*>(qpa + d0 + 8) : make_float2(0.f, 0.f);
+            const float2 b1 = vb ? *reinterpret_cast<const float2*>(qpb + d0 + 8) : make_float2(0.f, 0.f);
+            qf[ks][0] = pack2(a0.x, a0.y);
+            qf[ks][1] = pack2(b0.x, b0.y);
+            qf[ks][2] = pack2(a1.x, a1.y);
+            qf[ks][3] = pack2(b1.x, b1.y);
+        }
+    }
+    float oacc[HD / 8][4];
+#pragma unroll
+    for (int n = 0; n < HD / 8; ++n) oacc[n][0] = oacc[n][1] = oacc[n][2] = oacc[n][3] = 0.f;
+    float ma = -INFINITY, mb = -INFINITY, la = 0.f, lb = 0.f;
+
+    const uint32_t ks_base = s_u32(Ks), vs_base = s_u32(Vs);
+    __syncthreads();   // xs complete
+    for (int c = rank; c < n_all; c += S) {
+        const bool xc = c >= n_ch;   // extra (gathered) chunk
+        const int k0 = (xc ? c - n_ch : c) * kCh;
+        __syncthreads();   // previous chunk fully consumed
+        for (int idx = threadIdx.x; idx < kCh * HD / 8; idx += kThreads) {
+            const int j = idx / (HD / 8), d8 = (idx % (HD / 8)) * 8;
+            // gathered padding rows read slot xs[0] (finite data: 0 * V must stay 0)
+            const int64_t slot = xc ? (int64_t)xs[(k0 + j < s_nx) ? k0 + j : 0] : (int64_t)(k0 + j);
+            const int64_t src = (slot * nkv + g) * HD + d8;
+            cp_async16(ks_base + (uint32_t)((j * LD + d8) * 2), kc + src);
+            cp_async16(vs_base + (uint32_t)((j * LD + d8) * 2), vc + src);
+        }
+        cp_async_wait_all();
+        __syncthreads();
+        if (!warp_live) continue;
+        // visible chunk keys of rows a / b: [loa, hia) / [lob, hib)
+        int loa = 0, hia = pla - k0, lob = 0, hib = plb - k0;
+        if (xc) {
+            loa = va ? xoff[ia] - k0 : 0;
+            hia = va ? loa + xne[ia] : 0;
+            lob = vb ? xoff[ib] - k0 : 0;
+            hib = vb ? lob + xne[ib] : 0;
+        }
+        if (__all_sync(0xffffffffu, max(0, loa) >= min(kCh, hia) && max(0, lob) >= min(kCh, hib))) continue;
+        float s[kCh / 8][4];
+#pragma unroll
+        for (int n = 0; n < kCh / 8; ++n) s[n][0] = s[n][1] = s[n][2] = s[n][3] = 0.f;
+#pragma unroll
+        for (int ks = 0; ks < HD / 16; ++ks)
+#pragma unroll
+            for (int n = 0; n < kCh / 8; ++n) {
+                const __nv_bfloat16* kr = Ks + (n * 8 + gq) * LD + ks * 16 + 2 * tq;
+                uint32_t b[2];
+                b[0] = *reinterpret_cast<const uint32_t*>(kr);
+                b[1] = *reinterpret_cast<const uint32_t*>(kr + 8);
+                mma16816(s[n], qf[ks], b);
+            }
+        float cma = -INFINITY, cmb = -INFINITY;
+#pragma unroll
+        for (int n = 0; n < kCh / 8; ++n) {
+            const int j0 = n * 8 + 2 * tq;
+            if (j0 < loa || j0 >= hia) s[n][0] = -INFINITY;
+            if (j0 + 1 < loa || j0 + 1 >= hia) s[n][1] = -INFINITY;
+            if (j0 < lob || j0 >= hib) s[n][2] = -INFINITY;
+            if (j0 + 1 < lob || j0 + 1 >= hib) s[n][3] = -INFINITY;
+            cma = fmaxf(cma, fmaxf(s[n][0], s[n][1]));
+            cmb = fmaxf(cmb, fmaxf(s[n][2], s[n][3]));
+        }
+        cma = fmaxf(cma, __shfl_xor_sync(0xffffffffu, cma, 1));
+        cma = fmaxf(cma, __shfl_xor_sync(0xffffffffu, cma, 2));
+        cmb = fmaxf(cmb, __shfl_xor_sync(0xffffffffu, cmb, 1));
+        cmb = fmaxf(cmb, __shfl_xor_sync(0xffffffffu, cmb, 2));
+        const float na = fmaxf(ma, cma), nb = fmaxf(mb, cmb);
+        const float sa = na == -INFINITY ? 0.f : na, sb = nb == -INFINITY ? 0.f : nb;
+        const float fa = __expf(ma - sa), fb = __expf(mb - sb);   // 0 when the old max is -inf
+        ma = na;
+        mb = nb;
+        float suma = 0.f, sumb = 0.f;
+        uint32_t p[kCh / 16][4];
+#pragma unroll
+        for (int n = 0; n < kCh / 8; ++n) {
+            const float e0 = __expf(s[n][0] - sa), e1 = __expf(s[n][1] - sa);
+            const float e2 = __expf(s[n][2] - sb), e3 = __expf(s[n][3] - sb);
+            suma += e0 + e1;
+            sumb += e2 + e3;
+            if ((n & 1) == 0) {
+                p[n >> 1][0] = pack2(e0, e1);
+                p[n >> 1][1] = pack2(e2, e3);
+            } else {
+                p[n >> 1][2] = pack2(e0, e1);
+                p[n >> 1][3] = pack2(e2, e3);
+            }
+        }
+        suma += __shfl_xor_sync(0xffffffffu, suma, 1);
+        suma += __shfl_xor_sync(0xffffffffu, suma, 2);
+        sumb += __shfl_xor_sync(0xffffffffu, sumb, 1);
+        sumb += __shfl_xor_sync(0xffffffffu, sumb, 2);
+        la = la * fa + suma;
+        lb = lb * fb + sumb;
+#pragma unroll
+        for (int n = 0; n < HD / 8; ++n) {
+            oacc[n][0] *= fa;
+            oacc[n][1] *= fa;
+            oacc[n][2] *= fb;
+            oacc[n][3] *= fb;
+        }
+        // O += P V: B fragments of V (keys x dims) via ldmatrix.trans, two dim tiles per x4
+        const int mat = lane >> 3, mrow = lane & 7;
+#pragma unroll
+        for (int kk = 0; kk < kCh / 16; ++kk)
+#pragma unroll
+            for (int nd = 0; nd < HD / 8; nd += 2) {
+                // matrices: 0 keys kk*16+0..7 dims nd*8, 1 keys +8..15 dims nd*8, 2/3 the same for nd+1
+                const int key = kk * 16 + (mat & 1) * 8 + mrow;
+                const int dim = (nd + (mat >> 1)) * 8;
+                uint32_t b0, b1, b2, b3;
+                ldsm_x4_trans(vs_base + (uint32_t)((key * LD + dim) * 2), b0, b1, b2, b3);
+                const uint32_t bA[2] = {b0, b1}, bB[2] = {b2, b3};
+                mma16816(oacc[nd], p[kk], bA);
+                mma16816(oacc[nd + 1], p[kk], bB);
+            }
+    }
+
+    // push this rank's partial (m, l, o) for its 64 query-heads to the owners
+    const uint32_t recv_base = s_u32(recv);
+    if (warp_live) {
+        const int la_loc = warp * 16 + gq, lb_loc = la_loc + 8;
+        const int oa = la_loc / QO, ob = lb_loc / QO;
+        const uint32_t da = cl_map(recv_base, (uint32_t)oa) + (uint32_t)(((rank * QO + la_loc - oa * QO) * PW) * 4);
+        const uint32_t db = cl_map(recv_base, (uint32_t)ob) + (uint32_t)(((rank * QO + lb_loc - ob * QO) * PW) * 4);
+        if (tq == 0) {
+            st_cl_v2(da, ma, la);
+            st_cl_v2(db, mb, lb);
+        }
+#pragma unroll
+        for (int nd = 0; nd < HD / 8; ++nd) {
+            const int d = nd * 8 + 2 * tq;
+            st_cl_v2(da + (uint32_t)((2 + d) * 4), oacc[nd][0], oacc[nd][1]);
+            st_cl_v2(db + (uint32_t)((2 + d) * 4), oacc[nd][2], oacc[nd][3]);
+        }
+    }
+    cl_sync();   // every partial has landed in its owner's smem
+    // owner merge: query-heads [rank*QO, rank*QO + QO), S partials in rank order
+    for (int e = threadIdx.x; e < QO * HD; e += kThreads) {
+        const int ql = e / HD, d = e - ql * HD;
+        const int qi = q0 + rank * QO + ql;
+        if (qi >= nq) break;
+        float Mx = -INFINITY;
+        for (int s = 0; s < S; ++s) Mx = fmaxf(Mx, recv[(s * QO + ql) * PW]);
+        const float Ms = Mx == -INFINITY ? 0.f : Mx;
+        float L = 0.f, acc = 0.f;
+        for (int s = 0; s < S; ++s) {
+            const float* rec = recv + (s * QO + ql) * PW;
+            const float w = rec[0] == -INFINITY ? 0.f : __expf(rec[0] - Ms);
+            L += w * rec[1];
+            acc += w * rec[2 + d];
+        }
+        const int r = qi / G, h = g * G + qi % G;
+        o_out[((int64_t)r * nh + h) * HD + d] = __float2bfloat16(L > 0.f ? acc / L : 0.f);
+    }
+}
+
+int attn_fused_smem(int hd, int S) { return 2 * kCh * (hd + 8) * 2 + S * (kQT / S) * (hd + 2) * 4; }
+
+int launch_attn_fused(const float* q, const int32_t* dM, int m_max, const int32_t* plen, const int32_t* n_extra,
+                      const int32_t* extra, int extra_max, const void* kc, const void* vc, int nh, int nkv, int hd,
+                      int max_plen, void* o, cudaStream_t s) {
+    const int G = nh / nkv;
+    const int n_qt = (m_max * G + kQT - 1) / kQT;
+    const int n_ch = (max_plen + kCh - 1) / kCh;
+    int S = n_qt * nkv <= 37 ? 8 : 4;
+    while (S > 1 && S > n_ch) S >>= 1;
+    const int smem = attn_fused_smem(hd, S);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(S, n_qt, nkv);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = S;
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 2;
+    cudaError_t e;
+    if (hd == 64) {
+        static bool a64 = false;
+        if (!a64) {
+            cudaFuncSetAttribute(attn_fused_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+            a64 = true;
+        }
+        e = cudaLaunchKernelEx(&cfg, attn_fused_kernel<64>, q, dM, plen, n_extra, extra, extra_max,
+                               (const __nv_bfloat16*)kc, (const __nv_bfloat16*)vc, nh, nkv, (__nv_bfloat16*)o);
+    } else {
+        static bool a128 = false;
+        if (!a128) {
+            cudaFuncSetAttribute(attn_fused_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+            a128 = true;
+        }
+        e = cudaLaunchKernelEx(&cfg, attn_fused_kernel<128>, q, dM, plen, n_extra, extra, extra_max,
+                               (const __nv_bfloat16*)kc, (const __nv_bfloat16*)vc, nh, nkv, (__nv_bfloat16*)o);
+    }
+    if (e != cudaSuccess) {
+        set_cuda_error(e);
+        return CARD_E_CUDA;
+    }
+    return CARD_OK;
+}
+
+}  // namespace card

@@ -902,6 +902,8 @@ int card_attention(const float* q, const int32_t* dM, int m_max, const int32_t* 
         cudaFuncSetAttribute(attn_prefix_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
         attr = true;
     }
+    if (kvdtype == 0 && odtype == 0 && (hd == 64 || hd == 128) && !getenv("CARD_ATTN_SPLITKV"))
+        return launch_attn_fused(q, dM, m_max, plen, n_extra, extra, extra_max, kc, vc, nh, nkv, hd, max_plen, o, s);
     dim3 g1(nkv, n_splits);
     const int ew = (m_max * nh + 7) / 8;
     if (kvdtype == 0) {

@@ -326,7 +326,7 @@ class DeviceLlama:
         plan = self.plans[m_max]
         dM, dOut = rows.M, rows.n_out
         hd = c.head_dim
-        mm = self.mpad
+        mm = plan["m_max"]   # grids sized for this plan's rows (rows >= M exit at once)
         chk = raise_for_status
         chk(L_.card_embed(ptr(rows.tok), ptr(dM), mm, ptr(self.embed), self.code, c.hidden, ptr(self.x), s), "embed")
         for li, (L, P) in enumerate(zip(self.layers, plan["layers"])):

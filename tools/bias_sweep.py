@@ -15,7 +15,10 @@ target = card.LlamaModel(PRESETS["llama-3.1-8b"], seed=2, dtype="bf16", spec=car
 draft = card.LlamaModel(PRESETS["llama-3.2-1b"], seed=1, dtype="bf16", spec=card.ModelSpec(1.2, 1.0))
 prompt = [int(x) for x in np.random.default_rng(1000).integers(0, 128256, 512)]
 cfg = card.EngineConfig(K=100, k=3, ratio=7, max_new_tokens=new)
-for sharp, mix in [(0, 0), (300, 0), (1000, 0), (3000, 0), (10000, 0), (30000, 0), (3000, 0.001), (10000, 0.0005)]:
+SWEEP = [(0, 0), (1e5, 0), (3e5, 0), (6e5, 0), (1e6, 0), (2e6, 0), (4e6, 0), (1e7, 0), (2e6, 0.02), (2e6, 0.05)]
+if os.environ.get("SWEEP"):
+    SWEEP = [tuple(float(v) for v in x.split(":")) for x in os.environ["SWEEP"].split(",")]
+for sharp, mix in SWEEP:
     b = LogitBias(11, 2, float(sharp), 131, float(mix))
     target.bias = b
     draft.bias = LogitBias(11, 2, float(sharp), 131, float(mix))
