@@ -45,7 +45,7 @@ def parse():
     ap.add_argument("--k", type=int, default=3)
     ap.add_argument("--ratio", type=int, default=7)
     ap.add_argument("--temperature", type=float, default=0.0)
-    ap.add_argument("--bias-sharpness", type=float, default=float(os.environ.get("CARD_BIAS", "3000")))
+    ap.add_argument("--bias-sharpness", type=float, default=float(os.environ.get("CARD_BIAS", "1e6")))
     ap.add_argument("--bias-mix", type=float, default=0.0)
     ap.add_argument("--draft", default="llama-3.2-1b")
     ap.add_argument("--target", default="llama-3.1-8b")
@@ -198,6 +198,8 @@ def measure_roofline(target, rows_max, ctx_len, peak):
     toks = [int(x) for x in np.random.default_rng(5).integers(0, target.cfg.vocab_size, rows_max)]
     rows.set_chain(toks, ctx_len - rows_max, out_last_only=False)
     plan = rt.plans[rows_max]
+    if rt.fused:
+        rt._bind_rows(plan, rows)   # RoPE / KV-slot / lm_head row pointers of the fused epilogues
     lins = [L[k] for L in plan["layers"] for k in ("qkv", "o", "gu", "d")] + [plan["lm_head"]]
     stream = torch.cuda.current_stream()
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")

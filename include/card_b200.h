@@ -164,7 +164,7 @@ typedef struct card_linear card_linear;
 
 /* Y[M,N] = X[M,K] . W[N,K]^T with a fused epilogue (0 store f32, 1 residual
  * add f32, 2 store bf16, 3 SwiGLU -> bf16 with gate/up rows interleaved per
- * 128-row tile).  wdtype: 0 bf16 row-major (tcgen05 + tensor-map TMA for
+ * 128-row tile, 4 QKV RoPE + KV-cache write, see card_linear_fuse_rope).  wdtype: 0 bf16 row-major (tcgen05 + tensor-map TMA for
  * m_max >= 2, 128-bit-load GEMV for m_max == 1), 1 fp32 (parity kernel),
  * 2 bf16 pre-tiled [N/128][K/64][128x64] blocks in SWIZZLE_128B order
  * (card_tile_weights; one contiguous 16 KB bulk copy per pipeline stage).
@@ -173,12 +173,29 @@ int card_linear_create(const void* W, int N, int K, int wdtype, const void* X, i
                        void* out, int ldo, const float* bias, card_linear** out_h);
 int card_linear_run(card_linear* h, const int32_t* dM, void* stream);
 int card_linear_info(card_linear* h, int32_t* info8);
+/* Fused epilogues (bf16 tcgen05 path only):
+ * fuse_norm: the linear consumes the bf16 residual and applies RMSNorm as a
+ *   per-token output scale rsqrt(sum_p ssq[p*ld + off + m] / H + eps) (the norm
+ *   weight is folded into W at pack time); x_row_off (device, may be NULL) is
+ *   the first X row — the lm_head runs over a contiguous output-row range.
+ * fuse_resid: an EPI_RESID_F32 linear also writes bf16(x_new) to xb_out and
+ *   the per-16-column sum of squares of x_new to ssq_out[(col/16)*ld + m].
+ * fuse_rope: an EPI_QKV_ROPE (4) linear writes RoPE(q)/sqrt(hd) to q_out
+ *   [m, nh*hd] fp32 and RoPE(k), v to the KV cache rows slot[m] (bf16).
+ * These replace the rmsnorm and rope kernels between the GEMMs of a layer. */
+int card_linear_fuse_norm(card_linear* h, const float* ssq, int parts, int ld, float eps, int H,
+                          const int32_t* x_row_off);
+int card_linear_fuse_resid(card_linear* h, float* ssq_out, int ld, void* xb_out);
+int card_linear_fuse_rope(card_linear* h, const int32_t* pos, const int32_t* slot, const float* cos_t,
+                          const float* sin_t, int nh, int nkv, int hd, float* q_out, void* k_cache, void* v_cache);
 /* tuning: per-CTA %globaltimer stamps [grid][16] (NULL disables) */
 int card_linear_trace(card_linear* h, unsigned long long* trace);
 int card_linear_destroy(card_linear* h);
 
+/* x[r] = E[tok[r]] (fp32 residual); if xb != NULL also its bf16 copy and the
+ * per-16-column sums of squares ssq[(col/16)*ssq_ld + r] (fused-norm input) */
 int card_embed(const int32_t* tok, const int32_t* dM, int m_max, const void* E, int wdtype, int H,
-               float* x, void* stream);
+               float* x, void* xb, float* ssq, int ssq_ld, void* stream);
 int card_rmsnorm(const float* x, const float* w, int H, float eps, const int32_t* dM, int m_max,
                  const int32_t* gather, void* y, int ydtype, void* stream);
 int card_rope_kv(const float* qkv, const int32_t* dM, int m_max, const int32_t* pos, const int32_t* slot,

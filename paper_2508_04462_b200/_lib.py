@@ -56,8 +56,11 @@ SIGNATURES = {
     "card_linear_run": (c_int, [_P, _P, _P]),
     "card_linear_info": (c_int, [_P, _P]),
     "card_linear_trace": (c_int, [_P, _P]),
+    "card_linear_fuse_norm": (c_int, [_P, _P, c_int, c_int, ctypes.c_float, c_int, _P]),
+    "card_linear_fuse_resid": (c_int, [_P, _P, c_int, _P]),
+    "card_linear_fuse_rope": (c_int, [_P, _P, _P, _P, _P, c_int, c_int, c_int, _P, _P, _P]),
     "card_linear_destroy": (c_int, [_P]),
-    "card_embed": (c_int, [_P, _P, c_int, _P, c_int, c_int, _P, _P]),
+    "card_embed": (c_int, [_P, _P, c_int, _P, c_int, c_int, _P, _P, _P, c_int, _P]),
     "card_rmsnorm": (c_int, [_P, _P, c_int, ctypes.c_float, _P, c_int, _P, _P, c_int, _P]),
     "card_rope_kv": (c_int, [_P, _P, c_int, _P, _P, _P, _P, c_int, c_int, c_int, _P, _P, _P, c_int, _P]),
     "card_attention_work_floats": (c_int, [c_int, c_int, c_int, c_int]),

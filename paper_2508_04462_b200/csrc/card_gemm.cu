@@ -157,7 +157,33 @@ struct TcArgs {
     const float* bias;
     int ldo;
     unsigned long long* trace;   // optional [grid][16] %globaltimer stamps (tuning)
+    // consumer-side RMSNorm (the norm weight is folded into W): out = acc *
+    // rsqrt(sum_p ssq_in[p][off + m] * inv_h + eps) + bias, X = bf16 residual
+    const float* ssq_in;
+    int ssq_parts, ssq_ld;
+    float norm_eps, inv_h;
+    const int32_t* x_row_off;   // device: first X row of this GEMM (lm_head output rows)
+    // producer side (RESID): bf16 copy of the new residual and its per-16-column sum of squares
+    float* ssq_out;
+    __nv_bfloat16* xb_out;
+    // QKV epilogue: RoPE on q/k, q * qscale -> q_out (fp32), k/v -> KV cache slots (bf16)
+    const int32_t* pos;
+    const int32_t* slot;
+    const float* cos_t;
+    const float* sin_t;
+    float* q_out;
+    __nv_bfloat16* k_cache;
+    __nv_bfloat16* v_cache;
+    int nh, nkv, hd;
+    float qscale;
 };
+
+// sum over the 16 lanes of a half-warp (all 32 lanes must call)
+__device__ __forceinline__ float half_warp_sum(float v) {
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
 
 // Epilogue for one 16-column chunk (tokens m0..m0+mc) of output row n_glob.
 // All loads of a chunk are issued before any store so they overlap.  xch is
@@ -167,8 +193,57 @@ __device__ __forceinline__ void sts_f32(uint32_t addr, float v) {
 }
 template <int EPI>
 __device__ __forceinline__ void epi_chunk(const TcArgs& a, int tile, int n_glob, int n_local, int m0, int mc,
-                                          float* v, uint32_t xch) {
+                                          float* v, uint32_t xch, const float* invs, const int* tpos,
+                                          const int* tslot) {
     const float b = a.bias ? a.bias[n_glob] : 0.f;
+    if (a.ssq_in)
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] *= invs[m0 + j];
+    if (EPI == EPI_QKV_ROPE) {
+        // pair partner row n_local +- hd/2 of the same head, through xch [16][128]
+#pragma unroll
+        for (int j = 0; j < 16; ++j) sts_f32(xch + (uint32_t)((j * 128 + n_local) * 4), v[j] + b);
+        named_bar(1, kEpiThreads);
+        const int half = a.hd >> 1;
+        const int head = n_glob / a.hd, i = n_glob - head * a.hd;
+        if (i < half) {   // the first-half thread of each pair stores both
+            float o[16], cs[16], sn[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                o[j] = lds_f32(xch + (uint32_t)((j * 128 + n_local + half) * 4));
+                cs[j] = sn[j] = 0.f;
+                if (head < a.nh + a.nkv && j < mc) {   // all table loads in flight at once
+                    const int64_t pi = (int64_t)tpos[m0 + j] * half + i;
+                    cs[j] = a.cos_t[pi];
+                    sn[j] = a.sin_t[pi];
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                if (j >= mc) break;
+                const int m = m0 + j;
+                const float x1 = v[j] + b, x2 = o[j];
+                if (head < a.nh + a.nkv) {
+                    const float o1 = x1 * cs[j] - x2 * sn[j], o2 = x2 * cs[j] + x1 * sn[j];
+                    if (head < a.nh) {
+                        float* qr = a.q_out + ((int64_t)m * a.nh + head) * a.hd;
+                        qr[i] = o1 * a.qscale;
+                        qr[i + half] = o2 * a.qscale;
+                    } else {
+                        __nv_bfloat16* kr = a.k_cache + ((int64_t)tslot[m] * a.nkv + (head - a.nh)) * a.hd;
+                        kr[i] = __float2bfloat16(o1);
+                        kr[i + half] = __float2bfloat16(o2);
+                    }
+                } else {
+                    __nv_bfloat16* vr = a.v_cache + ((int64_t)tslot[m] * a.nkv + (head - a.nh - a.nkv)) * a.hd;
+                    vr[i] = __float2bfloat16(x1);
+                    vr[i + half] = __float2bfloat16(x2);
+                }
+            }
+        }
+        named_bar(1, kEpiThreads);
+        return;
+    }
     if (EPI == EPI_SWIGLU_BF16) {
         // rows [0,64) of a tile are gates, [64,128) the matching ups.  Gate
         // thread f and up thread 64+f swap halves of the chunk through xch
@@ -203,8 +278,17 @@ __device__ __forceinline__ void epi_chunk(const TcArgs& a, int tile, int n_glob,
 #pragma unroll
         for (int j = 0; j < 16; ++j) old[j] = j < mc ? a.out_f32[(int64_t)(m0 + j) * a.ldo + n_glob] : 0.f;
 #pragma unroll
-        for (int j = 0; j < 16; ++j)
-            if (j < mc) a.out_f32[(int64_t)(m0 + j) * a.ldo + n_glob] = old[j] + (v[j] + b);
+        for (int j = 0; j < 16; ++j) {
+            const float x = old[j] + (v[j] + b);
+            if (j < mc) {
+                a.out_f32[(int64_t)(m0 + j) * a.ldo + n_glob] = x;
+                if (a.xb_out) a.xb_out[(int64_t)(m0 + j) * a.ldo + n_glob] = __float2bfloat16(x);
+            }
+            if (a.ssq_out) {   // warp-uniform: every lane of the epilogue warps takes this path
+                const float sq = half_warp_sum(j < mc ? x * x : 0.f);
+                if ((n_local & 15) == 0 && j < mc) a.ssq_out[(int64_t)(n_glob >> 4) * a.ssq_ld + m0 + j] = sq;
+            }
+        }
         return;
     }
 #pragma unroll
@@ -215,7 +299,10 @@ __device__ __forceinline__ void epi_chunk(const TcArgs& a, int tile, int n_glob,
     }
 }
 
-template <int EPI>
+// CL: split-K cluster variant (one item per CTA, DSMEM reduction); else the
+// persistent direct-epilogue variant.  Separate instantiations keep each
+// kernel's code small (instruction-cache misses were a measurable cost).
+template <int EPI, bool CL>
 __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_constant__ CUtensorMap tmW,
                                                                const __grid_constant__ CUtensorMap tmX, TcArgs a) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -232,6 +319,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
     uint64_t* tempty = tfull + 2;   // [2]
     uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
     float* xch = (float*)(tmem_slot + 4);   // [16][128]
+    float* invs = xch + 16 * 128;            // [256] per-token rsqrt(mean x^2 + eps)
+    int* tpos = (int*)(invs + 256);          // [256] QKV: RoPE position of each token row
+    int* tslot = tpos + 256;                 // [256] QKV: KV-cache slot of each token row
 
     const int warp = warp_id(), lane = lane_id();
     if (threadIdx.x == 0) TC_STAMP(0);
@@ -248,6 +338,25 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
         tma_prefetch_desc(&tmW);
         tma_prefetch_desc(&tmX);
     }
+    // Weights do not depend on the previous kernel: the producer streams the
+    // first pipeline stages of weights before the TMEM allocation (which may
+    // wait for a co-resident CTA of the previous GEMM) and the grid dependency.
+    int pre = 0;
+    if (warp == 4 && lane == 0 && a.w_tiled) {
+        const int item = blockIdx.x;
+        if (item < a.items) {
+            const int tile = item / a.splits, split = item % a.splits;
+            const int kb0 = (int)((int64_t)a.kb_total * split / a.splits);
+            const int kb1 = (int)((int64_t)a.kb_total * (split + 1) / a.splits);
+            pre = (kb1 - kb0) < a.stages ? (kb1 - kb0) : a.stages;
+#pragma unroll 1
+            for (int i = 0; i < pre; ++i) {
+                mbar_expect_tx(&full[i], bytesA + bytesB);
+                bulk_load(sA + (size_t)i * bytesA, a.w_tiled + ((size_t)tile * a.kb_total + kb0 + i) * (size_t)bytesA,
+                          bytesA, &full[i]);
+            }
+        }
+    }
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                      "r"(a.tmem_cols));
@@ -257,27 +366,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
-    // Weights do not depend on the previous kernel: the producer streams the
-    // first pipeline stages of weights before waiting on the grid dependency.
-    int pre = 0;
-    if (warp == 4 && lane == 0 && a.w_tiled) {
-        const int item = blockIdx.x;
-        if (item < a.items) {
-            const int tile = item / a.splits, split = item % a.splits;
-            const int kb0 = (int)((int64_t)a.kb_total * split / a.splits);
-            const int kb1 = (int)((int64_t)a.kb_total * (split + 1) / a.splits);
-            pre = (kb1 - kb0) < a.stages ? (kb1 - kb0) : a.stages;
-            for (int i = 0; i < pre; ++i) {
-                mbar_expect_tx(&full[i], bytesA + bytesB);
-                bulk_load(sA + (size_t)i * bytesA, a.w_tiled + ((size_t)tile * a.kb_total + kb0 + i) * (size_t)bytesA,
-                          bytesA, &full[i]);
-            }
-        }
-    }
     pdl_wait();
     pdl_trigger();
     if (threadIdx.x == 0) TC_STAMP(1);
     const int M = *a.dM;
+    const int xoff = a.x_row_off ? *a.x_row_off : 0;   // first X row (contiguous output-row range)
     const int m_rt = M < 1 ? 1 : M;
     const int n_mma = ((m_rt + 15) / 16) * 16;   // runtime MMA N (tokens), <= Mpad
 
@@ -285,7 +378,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
         // zero-row replay: drain the prefetched stages, then leave
         if (warp == 4 && lane == 0)
             for (int i = 0; i < pre; ++i) {
-                tma_load_2d(sB + (size_t)i * bytesB, &tmX, &full[i], 0, 0);
+                tma_load_2d(sB + (size_t)i * bytesB, &tmX, &full[i], 0, xoff);
                 mbar_wait(&full[i], 0);
             }
     } else if (warp == 4) {
@@ -297,9 +390,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
                 const int tile = item / a.splits, split = item % a.splits;
                 const int kb0 = (int)((int64_t)a.kb_total * split / a.splits);
                 const int kb1 = (int)((int64_t)a.kb_total * (split + 1) / a.splits);
+#pragma unroll 1
                 for (int kb = kb0; kb < kb1; ++kb) {
                     if (first && kb - kb0 < pre) {   // weights already in flight
-                        tma_load_2d(sB + (size_t)stage * bytesB, &tmX, &full[stage], kb * kBK, 0);
+                        tma_load_2d(sB + (size_t)stage * bytesB, &tmX, &full[stage], kb * kBK, xoff);
                         if (++stage == S) {
                             stage = 0;
                             phase ^= 1;
@@ -313,7 +407,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
                                   a.w_tiled + ((size_t)tile * a.kb_total + kb) * (size_t)bytesA, bytesA, &full[stage]);
                     else
                         tma_load_2d(sA + (size_t)stage * bytesA, &tmW, &full[stage], kb * kBK, tile * kTileN);
-                    tma_load_2d(sB + (size_t)stage * bytesB, &tmX, &full[stage], kb * kBK, 0);
+                    tma_load_2d(sB + (size_t)stage * bytesB, &tmX, &full[stage], kb * kBK, xoff);
                     if (++stage == S) {
                         stage = 0;
                         phase ^= 1;
@@ -337,6 +431,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
                 mbar_wait(&tempty[acc], acc_phase ^ 1);
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + (uint32_t)(acc * a.Mpad);
+#pragma unroll 1
                 for (int kb = kb0; kb < kb1; ++kb) {
                     mbar_wait(&full[stage], phase);
                     if (kb == kb0) TC_STAMP(2);
@@ -367,6 +462,40 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
     } else {
         // ---------------- epilogue warps 0..3: TMEM lane = tile row n_local
         const int n_local = warp * 32 + lane;
+        if (EPI == EPI_QKV_ROPE) {
+            for (int m = n_local; m < M; m += kEpiThreads) {
+                tpos[m] = a.pos[m];
+                tslot[m] = a.slot[m];
+            }
+            if (!a.ssq_in) named_bar(1, kEpiThreads);
+        }
+        if (a.ssq_in) {
+            // RMSNorm scale of each token row (overlaps the main loop).  T lanes
+            // per token (a power of two, consecutive lanes) each sum a slice of
+            // the partials with 8 loads in flight, then a fixed shuffle tree.
+            int T = 1;
+            while (T < 32 && 2 * T * M <= kEpiThreads) T *= 2;
+            const int t = n_local & (T - 1);
+            const int per = (a.ssq_parts + T - 1) / T;
+            const int p0 = t * per, p1 = min(a.ssq_parts, p0 + per);
+            for (int mb = 0; mb * (kEpiThreads / T) < M; ++mb) {   // uniform trip count (shuffles)
+                const int m = mb * (kEpiThreads / T) + n_local / T;
+                float acc = 0.f;
+                if (m < M) {
+                    const float* src = a.ssq_in + xoff + m;
+                    for (int q = p0; q < p1; q += 32) {
+                        float v8[32];
+#pragma unroll
+                        for (int u = 0; u < 32; ++u) v8[u] = (q + u < p1) ? src[(int64_t)(q + u) * a.ssq_ld] : 0.f;
+#pragma unroll
+                        for (int u = 0; u < 32; ++u) acc += v8[u];
+                    }
+                }
+                for (int o = T >> 1; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+                if (m < M && t == 0) invs[m] = rsqrtf(acc * a.inv_h + a.norm_eps);
+            }
+            named_bar(1, kEpiThreads);
+        }
         int acc = 0;
         uint32_t acc_phase = 0;
         for (int item = blockIdx.x; item < a.items; item += gridDim.x) {
@@ -393,11 +522,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
             const uint32_t trow = tmem_base + ((uint32_t)(warp * 32) << 16) + (uint32_t)(acc * a.Mpad);
             // cluster mode (splits > 1): the accumulator stays in TMEM until
             // every rank of the cluster has finished its main loop (below)
-            for (int m0 = 0; m0 < M && a.splits == 1; m0 += 16) {
+            for (int m0 = 0; m0 < M && !CL; m0 += 16) {
                 float v[16];
                 tmem_ld16(trow + (uint32_t)m0, v);
                 const int mc = (M - m0) < 16 ? (M - m0) : 16;
-                epi_chunk<EPI>(a, tile, n_glob, n_local, m0, mc, v, smem_u32(xch));
+                epi_chunk<EPI>(a, tile, n_glob, n_local, m0, mc, v, smem_u32(xch), invs, tpos, tslot);
             }
             tc_fence_before();
             __syncwarp();
@@ -410,17 +539,20 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
             }
         }
     }
-    if (a.cluster > 1) {
+    if (CL) {
         // split-K over the cluster (S = a.cluster ranks = the K-slices of one
-        // tile).  Push-based DSMEM reduction: rank r owns R = 128/S rows of the
-        // tile (for SwiGLU: 64/S features = their gate and up rows).  After
-        // barrier 1 every rank's pipeline smem is free; each epilogue thread
-        // (one tile row) stores its Mpad partial sums into the owner's smem
-        // with 16-byte st.shared::cluster (fire-and-forget, no round trips).
+        // tile).  Push-based DSMEM reduction.  Tile rows are grouped in pair
+        // blocks of P rows (P = 128 plain, 64 SwiGLU gate/up, hd/2 RoPE): rank
+        // r owns Pp = P/S rows of every P-block, so each pair (n, n + P) stays
+        // on one owner.  After barrier 1 every rank's pipeline smem is free;
+        // each epilogue thread (one tile row) stores its partial sums into the
+        // owner's smem with 16-byte st.shared::cluster (fire-and-forget).
         // After barrier 2 each owner sums its S slices in rank order
         // (deterministic) from local smem and applies the epilogue.
         const int S = a.cluster;
         const int R = kTileN / S;
+        const int P = (EPI == EPI_SWIGLU_BF16) ? 64 : (EPI == EPI_QKV_ROPE) ? (a.hd >> 1) : kTileN;
+        const int Pp = P / S;
         const int ld = a.Mpad + 4;   // padded slice row (floats): spreads banks
         float* buf = reinterpret_cast<float*>(smem);   // [S][R][ld] over the stage buffers
         cluster_sync_all();
@@ -428,15 +560,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
         if (warp < 4 && M > 0) {
             const int me = (int)cluster_rank();
             const int n_local = warp * 32 + lane;
-            int owner, lr;
-            if (EPI == EPI_SWIGLU_BF16) {
-                const int f = n_local & 63, Rf = 64 / S;
-                owner = f / Rf;
-                lr = (f - owner * Rf) + (n_local >= 64 ? Rf : 0);
-            } else {
-                owner = n_local / R;
-                lr = n_local - owner * R;
-            }
+            const int i = n_local % P, qd = n_local / P;
+            const int owner = i / Pp;
+            const int lr = qd * Pp + (i - owner * Pp);
             const uint32_t dst = dsmem_addr(smem_u32(buf), (uint32_t)owner) + (uint32_t)(((me * R + lr) * ld) * 4);
             const uint32_t trow = tmem_base + ((uint32_t)(warp * 32) << 16);
             for (int m0 = 0; m0 < M; m0 += 16) {
@@ -453,51 +579,121 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
         cluster_sync_all();   // all pushes landed; no remote access after this point
         if (threadIdx.x == 0) TC_STAMP(7);
         if (warp < 4 && M > 0) {
-            // owner reduction: thread -> (output row j, token stripe); RJ outputs
-            // per token (R rows, or R/2 gate/up feature pairs for SwiGLU), TP
-            // token lanes; B tokens per pass with every load issued first.
+            // owner reduction: thread -> (output j, token stripe); RJ outputs per
+            // token (R rows, or R/2 pairs), TP token lanes; B tokens per pass
+            // with every load issued first.
             const int r = (int)cluster_rank();
             const int tile = blockIdx.x / S;
             const uint32_t sbuf = smem_u32(buf);
-            const int RJ = (EPI == EPI_SWIGLU_BF16) ? R / 2 : R;
+            const bool paired = (EPI == EPI_SWIGLU_BF16 || EPI == EPI_QKV_ROPE);
+            const int RJ = paired ? R / 2 : R;
             const int TP = kEpiThreads / RJ;
             const int j = threadIdx.x % RJ, m_first = threadIdx.x / RJ;
-            const int f_out = (EPI == EPI_SWIGLU_BF16) ? tile * 64 + r * RJ + j : tile * kTileN + r * R + j;
-            const float bias0 = a.bias ? a.bias[(EPI == EPI_SWIGLU_BF16) ? tile * kTileN + r * RJ + j : f_out] : 0.f;
-            const float bias1 = (a.bias && EPI == EPI_SWIGLU_BF16) ? a.bias[tile * kTileN + 64 + r * RJ + j] : 0.f;
+            // local rows and tile rows of output j (pair: lr0/n0 and lr0 + Pp / n0 + P)
+            int lr0, n0;
+            if (paired) {
+                const int qd2 = j / Pp, jj = j - qd2 * Pp;
+                lr0 = 2 * qd2 * Pp + jj;
+                n0 = 2 * qd2 * P + r * Pp + jj;
+            } else {
+                lr0 = j;
+                n0 = r * R + j;
+            }
+            const int ng0 = tile * kTileN + n0;
+            const float bias0 = a.bias ? a.bias[ng0] : 0.f;
+            const float bias1 = (a.bias && paired) ? a.bias[ng0 + P] : 0.f;
             constexpr int B = 8;
-            for (int mb = m_first; mb < M; mb += TP * B) {
-                float v0[B], v1[B], old[B];
+            const int n_it = (M + TP * B - 1) / (TP * B);
+            // QKV: this thread's pair is dims (i, i + hd/2) of one head
+            const int half = a.hd >> 1;
+            const int qhead = (EPI == EPI_QKV_ROPE) ? ng0 / a.hd : 0;
+            const int qi = (EPI == EPI_QKV_ROPE) ? ng0 - qhead * a.hd : 0;
+            float oldn[B];   // RESID: next pass's residual values, loaded one pass ahead
+#pragma unroll
+            for (int q = 0; q < B; ++q) {
+                const int m = m_first + q * TP;
+                oldn[q] = (EPI == EPI_RESID_F32 && m < M) ? a.out_f32[(int64_t)m * a.ldo + ng0] : 0.f;
+            }
+            for (int it = 0; it < n_it; ++it) {
+                const int mb = m_first + it * TP * B;
+                float v0[B], v1[B], old[B], cs[B], sn[B];
 #pragma unroll
                 for (int q = 0; q < B; ++q) {
                     v0[q] = 0.f;
                     v1[q] = 0.f;
-                    old[q] = 0.f;
+                    old[q] = oldn[q];
+                    const int mn = mb + TP * B + q * TP;
+                    if (EPI == EPI_RESID_F32) oldn[q] = (mn < M) ? a.out_f32[(int64_t)mn * a.ldo + ng0] : 0.f;
                     const int m = mb + q * TP;
-                    if (EPI == EPI_RESID_F32 && m < M) old[q] = a.out_f32[(int64_t)m * a.ldo + f_out];
+                    if (EPI == EPI_QKV_ROPE && qhead < a.nh + a.nkv && m < M) {
+                        const int64_t pi = (int64_t)tpos[m] * half + qi;
+                        cs[q] = a.cos_t[pi];
+                        sn[q] = a.sin_t[pi];
+                    }
                 }
+                if (it == 0 && threadIdx.x == 0) TC_STAMP(9);
                 for (int sl = 0; sl < S; ++sl) {
-                    const uint32_t row0 = sbuf + (uint32_t)(((sl * R + j) * ld) * 4);
-                    const uint32_t row1 = sbuf + (uint32_t)(((sl * R + RJ + j) * ld) * 4);
+                    const uint32_t row0 = sbuf + (uint32_t)(((sl * R + lr0) * ld) * 4);
+                    const uint32_t row1 = sbuf + (uint32_t)(((sl * R + lr0 + Pp) * ld) * 4);
 #pragma unroll
                     for (int q = 0; q < B; ++q) {
                         const int m = mb + q * TP;
                         if (m < M) {
                             v0[q] += lds_f32(row0 + (uint32_t)(m * 4));
-                            if (EPI == EPI_SWIGLU_BF16) v1[q] += lds_f32(row1 + (uint32_t)(m * 4));
+                            if (paired) v1[q] += lds_f32(row1 + (uint32_t)(m * 4));
                         }
                     }
                 }
+                if (it == 0 && threadIdx.x == 0) TC_STAMP(10);
 #pragma unroll
                 for (int q = 0; q < B; ++q) {
                     const int m = mb + q * TP;
                     if (m >= M) continue;
-                    const float x = v0[q] + bias0;
-                    if (EPI == EPI_SWIGLU_BF16)
-                        a.out_bf16[(int64_t)m * a.ldo + f_out] = __float2bfloat16(silu(x) * (v1[q] + bias1));
-                    else if (EPI == EPI_STORE_F32) a.out_f32[(int64_t)m * a.ldo + f_out] = x;
-                    else if (EPI == EPI_RESID_F32) a.out_f32[(int64_t)m * a.ldo + f_out] = old[q] + x;
-                    else a.out_bf16[(int64_t)m * a.ldo + f_out] = __float2bfloat16(x);
+                    const float sc = a.ssq_in ? invs[m] : 1.f;
+                    const float x = v0[q] * sc + bias0;
+                    if (EPI == EPI_SWIGLU_BF16) {
+                        a.out_bf16[(int64_t)m * a.ldo + tile * 64 + n0] = __float2bfloat16(silu(x) * (v1[q] * sc + bias1));
+                    } else if (EPI == EPI_QKV_ROPE) {
+                        const float x2 = v1[q] * sc + bias1;
+                        if (qhead < a.nh + a.nkv) {
+                            const float o1 = x * cs[q] - x2 * sn[q], o2 = x2 * cs[q] + x * sn[q];
+                            if (qhead < a.nh) {
+                                float* qr = a.q_out + ((int64_t)m * a.nh + qhead) * a.hd;
+                                qr[qi] = o1 * a.qscale;
+                                qr[qi + half] = o2 * a.qscale;
+                            } else {
+                                __nv_bfloat16* kr = a.k_cache + ((int64_t)tslot[m] * a.nkv + (qhead - a.nh)) * a.hd;
+                                kr[qi] = __float2bfloat16(o1);
+                                kr[qi + half] = __float2bfloat16(o2);
+                            }
+                        } else {
+                            __nv_bfloat16* vr = a.v_cache + ((int64_t)tslot[m] * a.nkv + (qhead - a.nh - a.nkv)) * a.hd;
+                            vr[qi] = __float2bfloat16(x);
+                            vr[qi + half] = __float2bfloat16(x2);
+                        }
+                    } else if (EPI == EPI_STORE_F32) {
+                        a.out_f32[(int64_t)m * a.ldo + ng0] = x;
+                    } else if (EPI == EPI_RESID_F32) {
+                        const float xn = old[q] + x;
+                        a.out_f32[(int64_t)m * a.ldo + ng0] = xn;
+                        if (a.xb_out) a.xb_out[(int64_t)m * a.ldo + ng0] = __float2bfloat16(xn);
+                        // x_new^2 in place of this thread's own slice-0 element (read above)
+                        if (a.ssq_out) sts_f32(sbuf + (uint32_t)((lr0 * ld + m) * 4), xn * xn);
+                    } else {
+                        a.out_bf16[(int64_t)m * a.ldo + ng0] = __float2bfloat16(x);
+                    }
+                }
+            }
+            if (EPI == EPI_RESID_F32 && a.ssq_out) {
+                // per-16-column sums of squares, fixed order, from slice 0
+                named_bar(1, kEpiThreads);
+                const int G16 = R / 16;
+                for (int e = threadIdx.x; e < G16 * M; e += kEpiThreads) {
+                    const int gi = e / M, m = e - gi * M;
+                    float t = 0.f;
+#pragma unroll
+                    for (int jj = 0; jj < 16; ++jj) t += lds_f32(sbuf + (uint32_t)(((gi * 16 + jj) * ld + m) * 4));
+                    a.ssq_out[(int64_t)((tile * kTileN + r * R) / 16 + gi) * a.ssq_ld + m] = t;
                 }
             }
         }
@@ -708,8 +904,9 @@ namespace card {
 template <int EPI>
 static cudaError_t set_tc_attr(int smem) {
     (void)smem;
-    cudaFuncSetAttribute(tc_gemm_kernel<EPI>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    return cudaFuncSetAttribute(tc_gemm_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(tc_gemm_kernel<EPI, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(tc_gemm_kernel<EPI, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    return cudaFuncSetAttribute(tc_gemm_kernel<EPI, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
 }
 
 template <int EPI>
@@ -732,7 +929,8 @@ static cudaError_t launch_tc(const card_linear* h, const TcArgs& a, cudaStream_t
     }
     cfg.attrs = attr;
     cfg.numAttrs = n;
-    return cudaLaunchKernelEx(&cfg, tc_gemm_kernel<EPI>, h->tmW, h->tmX, a);
+    if (a.cluster > 1) return cudaLaunchKernelEx(&cfg, tc_gemm_kernel<EPI, true>, h->tmW, h->tmX, a);
+    return cudaLaunchKernelEx(&cfg, tc_gemm_kernel<EPI, false>, h->tmW, h->tmX, a);
 }
 
 // Cluster split-K choice.  Wide N (>= half the resident CTA slots in
@@ -761,7 +959,7 @@ static int choose_cluster(int n_tiles, int kb_total, int Mpad, int slots, int sm
         cfg.attrs = &attr;
         cfg.numAttrs = 1;
         int nc = 0;
-        if (cudaOccupancyMaxActiveClusters(&nc, tc_gemm_kernel<EPI>, &cfg) == cudaSuccess && nc >= n_tiles) break;
+        if (cudaOccupancyMaxActiveClusters(&nc, tc_gemm_kernel<EPI, true>, &cfg) == cudaSuccess && nc >= n_tiles) break;
         cudaGetLastError();
         S >>= 1;
     }
@@ -853,7 +1051,7 @@ int card_linear_create(const void* W, int N, int K, int wdtype, const void* X, i
     const int stage_bytes = kTileN * kBK * 2 + Mpad * kBK * 2;
     int budget = (ctas_per_sm == 2 ? 110 : 220) * 1024;
     if (getenv("CARD_GEMM_SMEM_KB")) budget = atoi(getenv("CARD_GEMM_SMEM_KB")) * 1024;   // tuning knob
-    const int extra = 1024 + 64 * 8 + 16 * 128 * 4 + 64;
+    const int extra = 1024 + 64 * 8 + 16 * 128 * 4 + 3 * 256 * 4 + 64;
     int stages = (budget - extra) / stage_bytes;
     if (stages > 8) stages = 8;
     if (stages < 2) stages = 2;
@@ -866,6 +1064,7 @@ int card_linear_create(const void* W, int N, int K, int wdtype, const void* X, i
         case EPI_RESID_F32: e = set_tc_attr<EPI_RESID_F32>(h->smem); break;
         case EPI_STORE_BF16: e = set_tc_attr<EPI_STORE_BF16>(h->smem); break;
         case EPI_SWIGLU_BF16: e = set_tc_attr<EPI_SWIGLU_BF16>(h->smem); break;
+        case EPI_QKV_ROPE: e = set_tc_attr<EPI_QKV_ROPE>(h->smem); break;
         default: free(h); return CARD_E_CONFIG;
     }
     if (e != cudaSuccess) {
@@ -880,6 +1079,7 @@ int card_linear_create(const void* W, int N, int K, int wdtype, const void* X, i
         case EPI_RESID_F32: S = choose_cluster<EPI_RESID_F32>(a.n_tiles, a.kb_total, Mpad, slots, h->smem, stage_smem); break;
         case EPI_STORE_BF16: S = choose_cluster<EPI_STORE_BF16>(a.n_tiles, a.kb_total, Mpad, slots, h->smem, stage_smem); break;
         case EPI_SWIGLU_BF16: S = choose_cluster<EPI_SWIGLU_BF16>(a.n_tiles, a.kb_total, Mpad, slots, h->smem, stage_smem); break;
+        case EPI_QKV_ROPE: S = choose_cluster<EPI_QKV_ROPE>(a.n_tiles, a.kb_total, Mpad, slots, h->smem, stage_smem); break;
     }
     if (S > 1 && (kTileN % S != 0 || (size_t)kTileN * (Mpad + 4) * 4 > (size_t)stage_smem)) {
         free(h);
@@ -911,6 +1111,7 @@ int card_linear_run(card_linear* h, const int32_t* dM, void* stream) {
             case EPI_RESID_F32: e = launch_tc<EPI_RESID_F32>(h, a, s); break;
             case EPI_STORE_BF16: e = launch_tc<EPI_STORE_BF16>(h, a, s); break;
             case EPI_SWIGLU_BF16: e = launch_tc<EPI_SWIGLU_BF16>(h, a, s); break;
+            case EPI_QKV_ROPE: e = launch_tc<EPI_QKV_ROPE>(h, a, s); break;
         }
         if (e != cudaSuccess) {
             set_cuda_error(e);
@@ -943,6 +1144,49 @@ int card_linear_run(card_linear* h, const int32_t* dM, void* stream) {
         }
     }
     CARD_LAUNCH_CHECK();
+    return CARD_OK;
+}
+
+int card_linear_fuse_norm(card_linear* h, const float* ssq, int parts, int ld, float eps, int H,
+                          const int32_t* x_row_off) {
+    if (!h || h->kind != 0 || !ssq || parts <= 0 || H <= 0) return CARD_E_INPUT;
+    if (h->epi == EPI_RESID_F32) return CARD_E_CONFIG;
+    TcArgs& a = h->args;
+    a.ssq_in = ssq;
+    a.ssq_parts = parts;
+    a.ssq_ld = ld;
+    a.norm_eps = eps;
+    a.inv_h = 1.0f / (float)H;
+    a.x_row_off = x_row_off;
+    return CARD_OK;
+}
+
+int card_linear_fuse_resid(card_linear* h, float* ssq_out, int ld, void* xb_out) {
+    if (!h || h->kind != 0 || h->epi != EPI_RESID_F32) return CARD_E_INPUT;
+    if (ssq_out && h->args.cluster > 1 && kTileN / h->args.cluster < 16) return CARD_E_CONFIG;
+    h->args.ssq_out = ssq_out;
+    h->args.ssq_ld = ld;
+    h->args.xb_out = (__nv_bfloat16*)xb_out;
+    return CARD_OK;
+}
+
+int card_linear_fuse_rope(card_linear* h, const int32_t* pos, const int32_t* slot, const float* cos_t,
+                          const float* sin_t, int nh, int nkv, int hd, float* q_out, void* k_cache, void* v_cache) {
+    if (!h || h->kind != 0 || h->epi != EPI_QKV_ROPE || !pos || !slot || !q_out || !k_cache || !v_cache)
+        return CARD_E_INPUT;
+    if ((hd != 64 && hd != 128) || (nh + 2 * nkv) * hd != h->N) return CARD_E_CONFIG;
+    TcArgs& a = h->args;
+    a.pos = pos;
+    a.slot = slot;
+    a.cos_t = cos_t;
+    a.sin_t = sin_t;
+    a.nh = nh;
+    a.nkv = nkv;
+    a.hd = hd;
+    a.qscale = 1.0f / sqrtf((float)hd);
+    a.q_out = q_out;
+    a.k_cache = (__nv_bfloat16*)k_cache;
+    a.v_cache = (__nv_bfloat16*)v_cache;
     return CARD_OK;
 }
 

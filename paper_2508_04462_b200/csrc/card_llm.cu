@@ -48,15 +48,34 @@ __device__ __forceinline__ void stf<__nv_bfloat16>(__nv_bfloat16* p, int64_t i, 
 }
 
 // ---------------------------------------------------------------- embedding
+// xb / ssq (optional): the bf16 copy of the residual row and its per-16-column
+// sums of squares, ssq[(col/16)*ssq_ld + r] — the input of the first fused-norm
+// GEMM (card_linear_fuse_norm).
 template <typename W>
 __global__ void embed_kernel(const int32_t* __restrict__ tok, const int32_t* dM, const W* __restrict__ E, int H,
-                             float* __restrict__ x) {
+                             float* __restrict__ x, __nv_bfloat16* __restrict__ xb, float* __restrict__ ssq,
+                             int ssq_ld) {
     pdl_wait();     // predecessor outputs visible from here
     pdl_trigger();  // let the next kernel start its prologue
     const int r = blockIdx.x;
     if (r >= *dM) return;
     const int64_t t = tok[r];
-    for (int i = threadIdx.x; i < H; i += blockDim.x) x[(int64_t)r * H + i] = ldf(E, t * H + i);
+    if (!xb) {
+        for (int i = threadIdx.x; i < H; i += blockDim.x) x[(int64_t)r * H + i] = ldf(E, t * H + i);
+        return;
+    }
+    for (int g16 = threadIdx.x; g16 < H / 16; g16 += blockDim.x) {
+        float acc = 0.f;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            const int c = g16 * 16 + i;
+            const float v = ldf(E, t * H + c);
+            x[(int64_t)r * H + c] = v;
+            xb[(int64_t)r * H + c] = __float2bfloat16(v);
+            acc = fmaf(v, v, acc);
+        }
+        ssq[(int64_t)g16 * ssq_ld + r] = acc;
+    }
 }
 
 // ---------------------------------------------------------------- rmsnorm
@@ -852,10 +871,14 @@ int card_logit_bias(float* logits, const int32_t* dM, int m_max, int V, const in
 }
 
 int card_embed(const int32_t* tok, const int32_t* dM, int m_max, const void* E, int wdtype, int H, float* x,
-               void* stream) {
+               void* xb, float* ssq, int ssq_ld, void* stream) {
     cudaStream_t s = (cudaStream_t)stream;
-    if (wdtype == 0) CARD_PDL((embed_kernel<__nv_bfloat16>), dim3(m_max), dim3(256), 0, s, tok, dM, (const __nv_bfloat16*)E, H, x);
-    else CARD_PDL((embed_kernel<float>), dim3(m_max), dim3(256), 0, s, tok, dM, (const float*)E, H, x);
+    if (xb && (H % 16 != 0 || !ssq)) return CARD_E_INPUT;
+    __nv_bfloat16* xbb = (__nv_bfloat16*)xb;
+    if (wdtype == 0)
+        CARD_PDL((embed_kernel<__nv_bfloat16>), dim3(m_max), dim3(256), 0, s, tok, dM, (const __nv_bfloat16*)E, H, x, xbb,
+                 ssq, ssq_ld);
+    else CARD_PDL((embed_kernel<float>), dim3(m_max), dim3(256), 0, s, tok, dM, (const float*)E, H, x, xbb, ssq, ssq_ld);
     CARD_LAUNCH_CHECK();
     return CARD_OK;
 }

@@ -19,6 +19,7 @@ enum {
     EPI_RESID_F32 = 1,
     EPI_STORE_BF16 = 2,
     EPI_SWIGLU_BF16 = 3,
+    EPI_QKV_ROPE = 4,   // RoPE + q scale + KV-cache write (card_linear_fuse_rope)
 };
 
 // Per-forward row descriptors written by the row builders (card_engine.cu)

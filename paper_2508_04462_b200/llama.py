@@ -30,7 +30,7 @@ from ._device import ptr, require_cuda, stream_ptr
 from ._lib import lib
 from .errors import ConfigError, raise_for_status
 
-EPI_STORE_F32, EPI_RESID_F32, EPI_STORE_BF16, EPI_SWIGLU_BF16 = 0, 1, 2, 3
+EPI_STORE_F32, EPI_RESID_F32, EPI_STORE_BF16, EPI_SWIGLU_BF16, EPI_QKV_ROPE = 0, 1, 2, 3, 4
 
 
 @dataclass
@@ -176,7 +176,13 @@ def interleave_gate_up(wg: torch.Tensor, wu: torch.Tensor) -> torch.Tensor:
 
 
 def pack_weights(cfg: LlamaConfig, weights: dict, dtype: str = "bf16", device=None) -> dict:
-    """Canonical weights -> the device layout (fused QKV, interleaved gate/up)."""
+    """Canonical weights -> the device layout (fused QKV, interleaved gate/up).
+
+    bf16: each RMSNorm weight is folded into the columns of the linear that
+    consumes the normalised activations (W' = W diag(w): attn_norm -> wqkv,
+    mlp_norm -> wgu, final norm -> lm_head); the GEMM then consumes the bf16
+    residual and applies the per-token rsqrt(mean x^2 + eps) in its epilogue
+    (card_linear_fuse_norm).  fp32 parity weights stay unfolded."""
     if dtype not in ("bf16", "fp32"):
         raise ConfigError(f"dtype must be bf16 or fp32, got {dtype!r}")
     dev = device or require_cuda()
@@ -185,14 +191,19 @@ def pack_weights(cfg: LlamaConfig, weights: dict, dtype: str = "bf16", device=No
     f32 = lambda t: t.to(device=dev, dtype=torch.float32).contiguous()  # noqa: E731
     # bf16 linear weights live pre-tiled (tile_sw128); fp32 parity weights row-major
     lin = (lambda t: tile_sw128(to(t))) if dtype == "bf16" else to  # noqa: E731
-    out = {"dtype": dtype, "embed": to(weights["embed"]), "norm": f32(weights["norm"]), "layers": []}
-    out["lm_head"] = lin(weights["lm_head"])
+    fold = dtype == "bf16"
+    col = (lambda w, g: w.float() * g.float().view(1, -1)) if fold else (lambda w, g: w)  # noqa: E731
+    out = {"dtype": dtype, "embed": to(weights["embed"]), "norm": f32(weights["norm"]), "layers": [],
+           "folded": fold}
+    out["lm_head"] = lin(col(weights["lm_head"].to(dev), weights["norm"].to(dev)))
     for i in range(cfg.n_layers):
         p = f"l{i}."
         out["layers"].append({
-            "wqkv": lin(torch.cat([weights[p + "wq"], weights[p + "wk"], weights[p + "wv"]], 0)),
+            "wqkv": lin(col(torch.cat([weights[p + "wq"], weights[p + "wk"], weights[p + "wv"]], 0).to(dev),
+                            weights[p + "attn_norm"].to(dev))),
             "wo": lin(weights[p + "wo"]),
-            "wgu": lin(interleave_gate_up(weights[p + "wg"], weights[p + "wu"])),
+            "wgu": lin(col(interleave_gate_up(weights[p + "wg"], weights[p + "wu"]).to(dev),
+                           weights[p + "mlp_norm"].to(dev))),
             "wd": lin(weights[p + "wd"]),
             "attn_norm": f32(weights[p + "attn_norm"]),
             "mlp_norm": f32(weights[p + "mlp_norm"]),
@@ -222,6 +233,17 @@ class _Linear:
         info = (ctypes.c_int32 * 8)()
         lib().card_linear_info(h, info)
         self.info = dict(zip(("kind", "splits", "stages", "grid", "smem", "Mpad", "tmem_cols", "items"), list(info)))
+
+    def fuse_norm(self, ssq: torch.Tensor, parts: int, ld: int, eps: float, H: int, x_row_off=None):
+        raise_for_status(lib().card_linear_fuse_norm(self.h, ptr(ssq), parts, ld, eps, H, ptr(x_row_off)),
+                         "card_linear_fuse_norm")
+
+    def fuse_resid(self, ssq: torch.Tensor, ld: int, xb: torch.Tensor):
+        raise_for_status(lib().card_linear_fuse_resid(self.h, ptr(ssq), ld, ptr(xb)), "card_linear_fuse_resid")
+
+    def fuse_rope(self, rows, cos, sin, nh, nkv, hd, q, kc, vc):
+        raise_for_status(lib().card_linear_fuse_rope(self.h, ptr(rows.pos), ptr(rows.slot), ptr(cos), ptr(sin), nh, nkv,
+                                                     hd, ptr(q), ptr(kc), ptr(vc)), "card_linear_fuse_rope")
 
     def run(self, dM: torch.Tensor):
         from . import _lib
@@ -288,6 +310,11 @@ class DeviceLlama:
         self.g = torch.zeros((P, c.ffn), dtype=act, device=dev)
         self.hf = torch.zeros((P, H), dtype=act, device=dev)
         self.logits = torch.zeros((P, c.vocab_size), dtype=torch.float32, device=dev)
+        # fused-norm path (bf16): bf16 residual copy + per-16-column sums of squares
+        self.fused = bool(packed.get("folded")) and H % 16 == 0 and hd in (64, 128) and \
+            (c.qkv_dim % 128 == 0) and (c.n_heads * hd) % 128 == 0 and (c.n_kv_heads * hd) % 128 == 0
+        self.xb = torch.zeros((P, H), dtype=torch.bfloat16, device=dev) if self.fused else None
+        self.ssq = torch.zeros((H // 16, P), dtype=torch.float32, device=dev) if self.fused else None
         nwork = lib().card_attention_work_floats(P, c.n_heads, hd, self.prefix_slots)
         self.work = torch.zeros(nwork, dtype=torch.float32, device=dev)
         # per-layer KV base pointer arrays for the engine's KV movers
@@ -297,6 +324,8 @@ class DeviceLlama:
 
     # ------------------------------------------------------------ plans
     def _make_plan(self, m_max: int) -> dict:
+        if self.fused:
+            return self._make_fused_plan(m_max)
         c = self.cfg
         H = c.hidden
         plan = {"m_max": m_max, "layers": []}
@@ -309,6 +338,39 @@ class DeviceLlama:
             })
         plan["lm_head"] = _Linear(self.lm_head, self.hf, m_max, EPI_STORE_F32, self.logits, c.vocab_size)
         return plan
+
+    def _make_fused_plan(self, m_max: int) -> dict:
+        """bf16: 5 kernels per layer — qkv (+RMSNorm scale, RoPE, KV write),
+        attention, o (+residual, +sum of squares), gate/up (+RMSNorm scale,
+        SwiGLU), down (+residual, +sum of squares)."""
+        c = self.cfg
+        H, P = c.hidden, self.mpad
+        parts = H // 16
+        plan = {"m_max": m_max, "layers": [], "bound_rows": None}
+        for li, L in enumerate(self.layers):
+            qkv = _Linear(L["wqkv"], self.xb, m_max, EPI_QKV_ROPE, self.qkv, c.qkv_dim, L["bqkv"])
+            qkv.fuse_norm(self.ssq, parts, P, c.rms_eps, H)
+            o = _Linear(L["wo"], self.o, m_max, EPI_RESID_F32, self.x, H)
+            o.fuse_resid(self.ssq, P, self.xb)
+            gu = _Linear(L["wgu"], self.xb, m_max, EPI_SWIGLU_BF16, self.g, c.ffn)
+            gu.fuse_norm(self.ssq, parts, P, c.rms_eps, H)
+            d = _Linear(L["wd"], self.g, m_max, EPI_RESID_F32, self.x, H)
+            d.fuse_resid(self.ssq, P, self.xb)
+            plan["layers"].append({"qkv": qkv, "o": o, "gu": gu, "d": d})
+        plan["lm_head"] = _Linear(self.lm_head, self.xb, m_max, EPI_STORE_F32, self.logits, c.vocab_size)
+        return plan
+
+    def _bind_rows(self, plan: dict, rows: "RowBlock"):
+        """Row-dependent epilogue pointers (positions, KV slots, lm_head row offset)."""
+        key = rows.block.data_ptr()
+        if plan.get("bound_rows") == key:
+            return
+        c = self.cfg
+        for li, P_ in enumerate(plan["layers"]):
+            P_["qkv"].fuse_rope(rows, self.cos, self.sin, c.n_heads, c.n_kv_heads, c.head_dim, self.q,
+                                self.k_cache[li], self.v_cache[li])
+        plan["lm_head"].fuse_norm(self.ssq, c.hidden // 16, self.mpad, c.rms_eps, c.hidden, rows.out_rows)
+        plan["bound_rows"] = key
 
     def kv_row_elems(self) -> int:
         return self.cfg.n_kv_heads * self.cfg.head_dim
@@ -324,11 +386,14 @@ class DeviceLlama:
         L_ = lib()
         s = stream_ptr()
         plan = self.plans[m_max]
+        if self.fused:
+            return self._forward_fused(rows, plan)
         dM, dOut = rows.M, rows.n_out
         hd = c.head_dim
         mm = plan["m_max"]   # grids sized for this plan's rows (rows >= M exit at once)
         chk = raise_for_status
-        chk(L_.card_embed(ptr(rows.tok), ptr(dM), mm, ptr(self.embed), self.code, c.hidden, ptr(self.x), s), "embed")
+        chk(L_.card_embed(ptr(rows.tok), ptr(dM), mm, ptr(self.embed), self.code, c.hidden, ptr(self.x), None, None, 0, s),
+            "embed")
         for li, (L, P) in enumerate(zip(self.layers, plan["layers"])):
             chk(L_.card_rmsnorm(ptr(self.x), ptr(L["attn_norm"]), c.hidden, c.rms_eps, ptr(dM), mm, None,
                                 ptr(self.h), self.code, s), "rmsnorm")
@@ -348,6 +413,27 @@ class DeviceLlama:
         chk(L_.card_rmsnorm(ptr(self.x), ptr(self.norm), c.hidden, c.rms_eps, ptr(dOut), mm, ptr(rows.out_rows),
                             ptr(self.hf), self.code, s), "final norm")
         plan["lm_head"].run(dOut)
+
+    def _forward_fused(self, rows: "RowBlock", plan: dict):
+        c = self.cfg
+        L_ = lib()
+        s = stream_ptr()
+        self._bind_rows(plan, rows)
+        dM = rows.M
+        mm = plan["m_max"]
+        chk = raise_for_status
+        chk(L_.card_embed(ptr(rows.tok), ptr(dM), mm, ptr(self.embed), self.code, c.hidden, ptr(self.x), ptr(self.xb),
+                          ptr(self.ssq), self.mpad, s), "embed")
+        for li, P in enumerate(plan["layers"]):
+            P["qkv"].run(dM)
+            chk(L_.card_attention(ptr(self.q), ptr(dM), mm, ptr(rows.plen), ptr(rows.n_extra), ptr(rows.extra),
+                                  rows.extra_max, ptr(self.k_cache[li]), ptr(self.v_cache[li]), self.code,
+                                  c.n_heads, c.n_kv_heads, c.head_dim, self.prefix_slots, ptr(self.work), ptr(self.o),
+                                  self.code, s), "attention")
+            P["o"].run(dM)
+            P["gu"].run(dM)
+            P["d"].run(dM)
+        plan["lm_head"].run(rows.n_out)
 
     def launches_per_forward(self) -> int:
         gu_extra = 0

@@ -40,6 +40,8 @@ def bench_model(name, preset, m_rows, ctx_len):
     rows.set_chain(toks, ctx_len - m_rows, out_last_only=False)
     dM = rows.M
     plan = rt.plans[m_rows]
+    if rt.fused:
+        rt._bind_rows(plan, rows)
     total_b = total_t = 0.0
     print(f"== {name} M={m_rows} ctx={ctx_len}")
     for key in ("qkv", "o", "gu", "d"):
