@@ -470,11 +470,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
             if (!a.ssq_in) named_bar(1, kEpiThreads);
         }
         if (a.ssq_in) {
-            // RMSNorm scale of each token row (overlaps the main loop).  T lanes
-            // per token (a power of two, consecutive lanes) each sum a slice of
-            // the partials with 8 loads in flight, then a fixed shuffle tree.
-            int T = 1;
-            while (T < 32 && 2 * T * M <= kEpiThreads) T *= 2;
+            // RMSNorm scale of each token row (overlaps the main loop).  T = 8
+            // lanes per token each sum a fixed slice of the partials, then a
+            // fixed shuffle tree: the summation order must not depend on M, or
+            // the same token would get a different scale in an M=1 AR step
+            // than in an M=8 verify step (greedy CARD must equal greedy AR).
+            constexpr int T = 8;
             const int t = n_local & (T - 1);
             const int per = (a.ssq_parts + T - 1) / T;
             const int p0 = t * per, p1 = min(a.ssq_parts, p0 + per);

@@ -154,3 +154,19 @@ def test_fp32_card_matches_oracle_engine(card):
     rt = RefModel(ct, wt, forward_latency=7.0, params_billions=8.0, bias=bias)
     out, trace = O.run_serial(rd, rt, prompt, **cfg)
     assert res.output == out
+
+
+def test_card_greedy_lossless_high_acceptance_bf16(card):
+    """bf16 CARD at high acceptance (long verify chains, M up to r+1 rows)
+    emits exactly the greedy AR tokens: the verify forward must compute each
+    row bit-identically to a 1-row forward (no M-dependent reduction order)."""
+    from paper_2508_04462_b200.lm import LogitBias
+
+    bias = LogitBias(seed=11, order=2, sharpness=4000.0, mix_seed=131, mix_weight=0.0)
+    d, t, *_ = _tiny_pair(card, "bf16", "small-target", "small-draft", bias=bias)
+    prompt = [int(x) for x in np.random.default_rng(5).integers(0, t.vocab.size, 64)]
+    cfg = card.EngineConfig(K=24, k=3, ratio=7, max_new_tokens=256)
+    van = card.run_vanilla(t, prompt, cfg)
+    res = card.run_speculative(d, t, prompt, cfg, use_graphs=True)
+    assert res.metrics.mean_acceptance_length > 2.5, res.metrics.mean_acceptance_length
+    assert res.output == van.output
