@@ -207,14 +207,19 @@ int card_attention(const float* q, const int32_t* dM, int m_max, const int32_t* 
                    const void* v_cache, int kvdtype, int nh, int nkv, int hd, int max_plen, float* work,
                    void* o, int odtype, void* stream);
 /* draft lm_head epilogue: per-row top-k by (logit desc, token asc) with
- * log-probs logit/T - logsumexp (replaces extension_pool's rows_topk+log). */
+ * log-probs logit/T - logsumexp (replaces extension_pool's rows_topk+log).
+ * If ctx_tail != NULL the k-gram logit bias of card_logit_bias is applied on
+ * the fly (same arithmetic); likewise for card_argmax_logits. */
 int card_lmhead_work_floats(int m_max, int k);
 int card_topk_logits(const float* logits, const int32_t* dM, int m_max, int V, int k, double inv_temp,
-                     int32_t* out_tok, double* out_logp, int32_t* out_cnt, float* work, void* stream);
+                     int32_t* out_tok, double* out_logp, int32_t* out_cnt, float* work, const int32_t* ctx_tail,
+                     int order, int stride, uint64_t seed, uint64_t seed2, float mix_weight, float sharpness,
+                     void* stream);
 /* target greedy: first maximum per row (verify.py:38-40); vocab split over
  * CTAs, merged in a second launch.  work: card_lmhead_work_floats floats. */
 int card_argmax_logits(const float* logits, const int32_t* dM, int m_max, int V, int32_t* out, float* work,
-                       void* stream);
+                       const int32_t* ctx_tail, int order, int stride, uint64_t seed, uint64_t seed2,
+                       float mix_weight, float sharpness, void* stream);
 int card_softmax64(const float* logits, const int32_t* dM, int m_max, int V, double inv_temp, double* out,
                    void* stream);
 /* agreement knob: logits[r] += sharpness * (u1 + mix_weight * u2), u the

@@ -67,8 +67,10 @@ SIGNATURES = {
     "card_attention": (c_int, [_P, _P, c_int, _P, _P, _P, c_int, _P, _P, c_int, c_int, c_int, c_int, c_int, _P,
                                _P, c_int, _P]),
     "card_lmhead_work_floats": (c_int, [c_int, c_int]),
-    "card_topk_logits": (c_int, [_P, _P, c_int, c_int, c_int, c_double, _P, _P, _P, _P, _P]),
-    "card_argmax_logits": (c_int, [_P, _P, c_int, c_int, _P, _P, _P]),
+    "card_topk_logits": (c_int, [_P, _P, c_int, c_int, c_int, c_double, _P, _P, _P, _P, _P, c_int, c_int, c_uint64,
+                                 c_uint64, ctypes.c_float, ctypes.c_float, _P]),
+    "card_argmax_logits": (c_int, [_P, _P, c_int, c_int, _P, _P, _P, c_int, c_int, c_uint64, c_uint64, ctypes.c_float,
+                                   ctypes.c_float, _P]),
     "card_softmax64": (c_int, [_P, _P, c_int, c_int, c_double, _P, _P]),
     "card_logit_bias": (c_int, [_P, _P, c_int, c_int, _P, c_int, c_int, c_uint64, c_uint64, ctypes.c_float,
                                 ctypes.c_float, _P]),

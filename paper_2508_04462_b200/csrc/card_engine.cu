@@ -47,54 +47,64 @@ __global__ void draft_rows_kernel(card_engine_state* E, const card_cache_state* 
                                   const int32_t* __restrict__ nparent, const int32_t* __restrict__ nlayer,
                                   const int32_t* __restrict__ frontier, const int32_t* __restrict__ committed,
                                   CardRows R, int tree_base, int32_t* ctx_tail, int order) {
-    if (threadIdx.x != 0) return;
+    // one thread per catch-up row and per frontier row (the ancestor walks of
+    // the frontier nodes run in parallel)
+    const int tid = threadIdx.x;
     if (E->stop || E->done) {
-        *R.M = 0;
-        *R.n_out = 0;
+        if (tid == 0) {
+            *R.M = 0;
+            *R.n_out = 0;
+        }
         return;
     }
     const int C = E->C;
     const int nf = S->n_frontier;
     const int anchor = E->anchor_origin ? 0 : S->root;
     const int base = E->anchor_origin ? E->base_len : C;
-    int m = 0;
+    const int Pd = E->Pd;
     if (nf == 0) {
         // flat forward of the committed context (engine.py:210-213)
-        int start = E->Pd < C - 1 ? E->Pd : C - 1;
-        for (int p = start; p < C; ++p, ++m) {
+        const int start = Pd < C - 1 ? Pd : C - 1;
+        for (int p = start + tid; p < C; p += blockDim.x) {
+            const int m = p - start;
             R.tok[m] = committed[p];
             R.pos[m] = p;
             R.slot[m] = p;
             R.plen[m] = p + 1;
             R.n_extra[m] = 0;
         }
-        R.out_rows[0] = m - 1;
         if (ctx_tail)
-            for (int j = 0; j < order; ++j) {
+            for (int j = tid; j < order; j += blockDim.x) {
                 const int p = C - order + j;
                 ctx_tail[j] = p >= 0 ? committed[p] : -1;
             }
-        *R.n_out = 1;
-        *R.M = m;
-        E->Pd = C;
+        __syncthreads();
+        if (tid == 0) {
+            R.out_rows[0] = C - start - 1;
+            *R.n_out = 1;
+            *R.M = C - start;
+            E->Pd = C;
+        }
         return;
     }
-    for (int p = E->Pd; p < base; ++p, ++m) {   // catch-up rows (no outputs)
-        R.tok[m] = committed[p];
-        R.pos[m] = p;
-        R.slot[m] = p;
-        R.plen[m] = p + 1;
-        R.n_extra[m] = 0;
+    const int n_catch = Pd < base ? base - Pd : 0;
+    for (int i = tid; i < n_catch; i += blockDim.x) {   // catch-up rows (no outputs)
+        const int p = Pd + i;
+        R.tok[i] = committed[p];
+        R.pos[i] = p;
+        R.slot[i] = p;
+        R.plen[i] = p + 1;
+        R.n_extra[i] = 0;
     }
-    if (E->Pd < base) E->Pd = base;
     const int anchor_layer = nlayer[anchor];
-    int chain[64];
-    for (int i = 0; i < nf; ++i, ++m) {
+    for (int i = tid; i < nf; i += blockDim.x) {
+        const int m = n_catch + i;
         const int f = frontier[i];
         const int d = nlayer[f] - anchor_layer;
+        int32_t* ex = R.extra + (int64_t)m * R.extra_max;
         int cur = f;
-        for (int j = d - 1; j >= 0; --j) {
-            chain[j] = cur;
+        for (int j = d - 1; j >= 0; --j) {   // ancestors, root side first
+            ex[j] = tree_base + cur;
             cur = nparent[cur];
         }
         R.tok[m] = ntoken[f];
@@ -102,14 +112,13 @@ __global__ void draft_rows_kernel(card_engine_state* E, const card_cache_state* 
         R.slot[m] = tree_base + f;
         R.plen[m] = base;
         R.n_extra[m] = d;
-        for (int j = 0; j < d; ++j) R.extra[(int64_t)m * R.extra_max + j] = tree_base + chain[j];
         R.out_rows[i] = m;
         if (ctx_tail) {
-            // tail of base + path: last `order` tokens
+            // tail of base + path: last `order` tokens (path node = ex[q] - tree_base)
             for (int j = 0; j < order; ++j) {
                 const int q = d - order + j;   // index into path (0..d-1), negative -> base
                 int t;
-                if (q >= 0) t = ntoken[chain[q]];
+                if (q >= 0) t = ntoken[ex[q] - tree_base];
                 else {
                     const int p = base + q;
                     t = p >= 0 ? committed[p] : -1;
@@ -118,8 +127,12 @@ __global__ void draft_rows_kernel(card_engine_state* E, const card_cache_state* 
             }
         }
     }
-    *R.n_out = nf;
-    *R.M = m;
+    __syncthreads();
+    if (tid == 0) {
+        *R.n_out = nf;
+        *R.M = n_catch + nf;
+        if (Pd < base) E->Pd = base;
+    }
 }
 
 __global__ void target_rows_kernel(card_engine_state* E, const card_cache_state* S, const int32_t* __restrict__ q_tok,
@@ -518,7 +531,7 @@ int card_draft_rows(card_engine_state* E, card_cache* h, const int32_t* committe
     const int rm = rows_max;
     CardRows R = make_rows(rows, rows + 1, rows + 2, rows + 2 + rm, rows + 2 + 2 * rm, rows + 2 + 3 * rm,
                            rows + 2 + 4 * rm, rows + 2 + 6 * rm, rows + 2 + 5 * rm, rm, extra_max);
-    draft_rows_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(E, S, tok, par, lay, fr, committed, R, tree_base, ctx_tail,
+    draft_rows_kernel<<<1, 128, 0, (cudaStream_t)stream>>>(E, S, tok, par, lay, fr, committed, R, tree_base, ctx_tail,
                                                          order);
     CARD_LAUNCH_CHECK();
     return CARD_OK;

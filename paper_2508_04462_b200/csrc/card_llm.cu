@@ -490,6 +490,34 @@ __global__ void attn_combine_kernel(const int32_t* dM, const int32_t* __restrict
     }
 }
 
+// ---------------------------------------------------------------- k-gram logit bias (agreement knob)
+// logits[r][i] + sharp * (u1_i + mixw * u2_i): the splitmix64 k-gram stream of
+// (seed, context tail of row r), _kernels.pyx:26-41.  Applied on the fly by
+// the top-k / argmax readers (one read of the logits instead of a separate
+// read-modify-write pass); same fp32 arithmetic as logit_bias_kernel.
+struct KgBias {
+    const int32_t* tail;
+    int order, stride;
+    uint64_t seed, seed2;
+    float mixw, sharp;
+};
+__device__ __forceinline__ void kg_row_state(const KgBias& b, int r, uint64_t& s1, uint64_t& s2) {
+    s1 = mix64(b.seed + kSeedSalt);
+    s2 = mix64(b.seed2 + kSeedSalt);
+    for (int j = 0; j < b.order; ++j) {
+        const int t = b.tail[(int64_t)r * b.stride + j];
+        if (t < 0) continue;
+        s1 = mix64(s1 ^ mix64((uint64_t)t + 1));
+        s2 = mix64(s2 ^ mix64((uint64_t)t + 1));
+    }
+}
+__device__ __forceinline__ float kg_apply(const KgBias& b, float logit, int i, uint64_t s1, uint64_t s2) {
+    const uint64_t step = (uint64_t)(i + 1) * kGamma;
+    float u = (float)to_unit(mix64(s1 + step));
+    if (b.mixw != 0.f) u += b.mixw * (float)to_unit(mix64(s2 + step));
+    return logit + b.sharp * u;
+}
+
 // ---------------------------------------------------------------- lm_head epilogues (split over the vocab)
 // Stage 1: CTA (row, split) scans a vocab slice: online max / sum-exp and a
 // register-resident sorted top-KT (static indices, bubble insertion).
@@ -498,11 +526,15 @@ __device__ __forceinline__ bool lbefore(float a, int ta, float b, int tb) { retu
 
 template <int KT>
 __global__ void __launch_bounds__(256) topk_partial_kernel(const float* __restrict__ logits, const int32_t* dM, int V,
-                                                           int S, float inv_temp, float* __restrict__ work) {
+                                                           int S, float inv_temp, float* __restrict__ work, KgBias kb) {
     pdl_wait();     // predecessor outputs visible from here
     pdl_trigger();  // let the next kernel start its prologue
     const int r = blockIdx.x, sp = blockIdx.y;
     if (r >= *dM) return;
+    const bool biased = kb.sharp != 0.f;
+    uint64_t ks1 = 0, ks2 = 0;
+    if (biased) kg_row_state(kb, r, ks1, ks2);
+    auto lg = [&](float v, int i) { return biased ? kg_apply(kb, v, i, ks1, ks2) : v; };
     // split boundaries on 4-element multiples so slices stay float4-aligned
     const int lo = (int)(((int64_t)V * sp / S) & ~3LL);
     const int hi = sp == S - 1 ? V : (int)(((int64_t)V * (sp + 1) / S) & ~3LL);
@@ -550,24 +582,24 @@ __global__ void __launch_bounds__(256) topk_partial_kernel(const float* __restri
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 const int i = lo + 4 * (vi + u * blockDim.x);
-                consume(q[u].x * inv_temp, i);
-                consume(q[u].y * inv_temp, i + 1);
-                consume(q[u].z * inv_temp, i + 2);
-                consume(q[u].w * inv_temp, i + 3);
+                consume(lg(q[u].x, i) * inv_temp, i);
+                consume(lg(q[u].y, i + 1) * inv_temp, i + 1);
+                consume(lg(q[u].z, i + 2) * inv_temp, i + 2);
+                consume(lg(q[u].w, i + 3) * inv_temp, i + 3);
             }
         }
         for (; vi < nv; vi += blockDim.x) {
             const float4 q = __ldg(l4 + vi);
             const int i = lo + 4 * vi;
-            consume(q.x * inv_temp, i);
-            consume(q.y * inv_temp, i + 1);
-            consume(q.z * inv_temp, i + 2);
-            consume(q.w * inv_temp, i + 3);
+            consume(lg(q.x, i) * inv_temp, i);
+            consume(lg(q.y, i + 1) * inv_temp, i + 1);
+            consume(lg(q.z, i + 2) * inv_temp, i + 2);
+            consume(lg(q.w, i + 3) * inv_temp, i + 3);
         }
         a0 = lo + 4 * nv;
         a1 = hi;
     }
-    for (int i = a0 + threadIdx.x; i < a1; i += blockDim.x) consume(lr[i] * inv_temp, i);
+    for (int i = a0 + threadIdx.x; i < a1; i += blockDim.x) consume(lg(lr[i], i) * inv_temp, i);
     // block reduction: max/sum then KT rounds of arg-best
     __shared__ float sm_m[8], sm_s[8], bv[8];
     __shared__ int bt[8], bw[8];
@@ -687,11 +719,14 @@ __global__ void topk_merge_kernel(const int32_t* dM, int S, int k, int V, const 
 
 // greedy: first maximum per row, split over the vocab then merged
 __global__ void __launch_bounds__(256) argmax_partial_kernel(const float* __restrict__ logits, const int32_t* dM,
-                                                             int V, int S, float* __restrict__ work) {
+                                                             int V, int S, float* __restrict__ work, KgBias kb) {
     pdl_wait();     // predecessor outputs visible from here
     pdl_trigger();  // let the next kernel start its prologue
     const int r = blockIdx.x, sp = blockIdx.y;
     if (r >= *dM) return;
+    const bool biased = kb.sharp != 0.f;
+    uint64_t ks1 = 0, ks2 = 0;
+    if (biased) kg_row_state(kb, r, ks1, ks2);
     // split boundaries on 4-element multiples so slices stay float4-aligned
     const int lo = (int)(((int64_t)V * sp / S) & ~3LL);
     const int hi = sp == S - 1 ? V : (int)(((int64_t)V * (sp + 1) / S) & ~3LL);
@@ -699,6 +734,7 @@ __global__ void __launch_bounds__(256) argmax_partial_kernel(const float* __rest
     float bv = -INFINITY;
     int bi = 0x7fffffff;
     auto take = [&](float v, int i) {
+        if (biased) v = kg_apply(kb, v, i, ks1, ks2);
         if (v > bv || (v == bv && i < bi)) {
             bv = v;
             bi = i;
@@ -962,8 +998,11 @@ static int vocab_splits(int m_max) {
 int card_lmhead_work_floats(int m_max, int k) { return m_max * vocab_splits(m_max) * (2 + 2 * 8); }
 
 int card_topk_logits(const float* logits, const int32_t* dM, int m_max, int V, int k, double inv_temp,
-                     int32_t* out_tok, double* out_logp, int32_t* out_cnt, float* work, void* stream) {
+                     int32_t* out_tok, double* out_logp, int32_t* out_cnt, float* work, const int32_t* ctx_tail,
+                     int order, int stride, uint64_t seed, uint64_t seed2, float mix_weight, float sharpness,
+                     void* stream) {
     if (k < 1 || k > 8) return CARD_E_CONFIG;
+    const KgBias kb{ctx_tail, order, stride, seed, seed2, mix_weight, ctx_tail ? sharpness : 0.f};
     cudaStream_t s = (cudaStream_t)stream;
     const int S = vocab_splits(m_max);
     dim3 g(m_max, S);
@@ -971,7 +1010,7 @@ int card_topk_logits(const float* logits, const int32_t* dM, int m_max, int V, i
     switch (k) {
 #define CARD_TOPK_CASE(KT)                                                                                   \
     case KT:                                                                                                 \
-        CARD_PDL((topk_partial_kernel<KT>), dim3(g), dim3(256), 0, s, logits, dM, V, S, it, work);                                \
+        CARD_PDL((topk_partial_kernel<KT>), dim3(g), dim3(256), 0, s, logits, dM, V, S, it, work, kb);                                \
         CARD_PDL((topk_merge_kernel<KT>), dim3((m_max + 7) / 8), dim3(256), 0, s, dM, S, k, V, work, out_tok, out_logp, out_cnt); \
         break;
         CARD_TOPK_CASE(1)
@@ -989,10 +1028,12 @@ int card_topk_logits(const float* logits, const int32_t* dM, int m_max, int V, i
 }
 
 int card_argmax_logits(const float* logits, const int32_t* dM, int m_max, int V, int32_t* out, float* work,
-                       void* stream) {
+                       const int32_t* ctx_tail, int order, int stride, uint64_t seed, uint64_t seed2, float mix_weight,
+                       float sharpness, void* stream) {
     cudaStream_t s = (cudaStream_t)stream;
     const int S = vocab_splits(m_max);
-    CARD_PDL((argmax_partial_kernel), dim3(m_max, S), dim3(256), 0, s, logits, dM, V, S, work);
+    const KgBias kb{ctx_tail, order, stride, seed, seed2, mix_weight, ctx_tail ? sharpness : 0.f};
+    CARD_PDL((argmax_partial_kernel), dim3(m_max, S), dim3(256), 0, s, logits, dM, V, S, work, kb);
     CARD_PDL((argmax_merge_kernel), dim3((m_max + 7) / 8), dim3(256), 0, s, dM, S, work, out);
     CARD_LAUNCH_CHECK();
     return CARD_OK;

@@ -236,15 +236,25 @@ class _LlamaAdapter:
             self.scratch_ptrs = torch.tensor([self.scratch_k.data_ptr(), self.scratch_v.data_ptr()],
                                              dtype=torch.int64, device=dev)
 
-    def _bias(self, rt_tail: _RowsAndTail):
+    def _bias_args(self, rt_tail: _RowsAndTail) -> tuple:
+        """(ctx_tail, order, stride, seed, seed2, mix, sharpness) of the k-gram
+        logit bias, applied on the fly by the top-k / argmax readers."""
         b = self.m.bias
         if b.sharpness == 0.0:
-            return
+            return (None, 0, 0, 0, 0, 0.0, 0.0)
         M64 = (1 << 64) - 1
         tails = ctypes.c_void_p(rt_tail.tail.data_ptr() + 4 * (rt_tail.order - b.order))
+        return (tails, b.order, rt_tail.order, b.seed & M64, b.mix_seed & M64, float(b.mix_weight),
+                float(b.sharpness))
+
+    def _bias(self, rt_tail: _RowsAndTail):
+        """In-place bias of the logits (fp64 sampling path)."""
+        tails, order, stride, seed, seed2, mix, sharp = self._bias_args(rt_tail)
+        if sharp == 0.0:
+            return
         raise_for_status(lib().card_logit_bias(ptr(self.rt.logits), ptr(rt_tail.rows.n_out), self.rows_max, self.V,
-                                               tails, b.order, rt_tail.order, b.seed & M64, b.mix_seed & M64,
-                                               float(b.mix_weight), float(b.sharpness), stream_ptr()), "logit_bias")
+                                               tails, order, stride, seed, seed2, mix, sharp, stream_ptr()),
+                         "logit_bias")
 
     def prefill(self, run, tokens):
         """Causal forward of tokens[0..n) into KV slots 0..n-1 (no outputs used)."""
@@ -262,25 +272,26 @@ class _LlamaAdapter:
     def draft(self, run):
         rows = run.drt.rows
         self.rt.forward(rows, self.rows_max)
-        self._bias(run.drt)
         raise_for_status(lib().card_topk_logits(ptr(self.rt.logits), ptr(rows.n_out), self.rows_max, self.V, self.k,
                                                 1.0 / run.t_score, ptr(self.tok), ptr(self.logp), ptr(self.cnt),
-                                                ptr(self.lm_work), stream_ptr()), "topk_logits")
+                                                ptr(self.lm_work), *self._bias_args(run.drt), stream_ptr()),
+                         "topk_logits")
         return self.tok, self.logp, self.cnt, 0
 
     def target(self, run):
         rows = run.trt.rows
         self.rt.forward(rows, self.rows_max)
-        self._bias(run.trt)
         L_ = lib()
         if run.sampling:
+            self._bias(run.trt)
             raise_for_status(L_.card_softmax64(ptr(self.rt.logits), ptr(rows.n_out), self.rows_max, self.V,
                                                1.0 / run.t_score, ptr(self.probs), stream_ptr()), "softmax64")
             raise_for_status(L_.card_verify_probs(run.E_ptr, run.q_tok_ptr, ptr(self.probs), self.V, None,
                                                   ptr(run.uni), stream_ptr()), "verify_probs")
         else:
             raise_for_status(L_.card_argmax_logits(ptr(self.rt.logits), ptr(rows.n_out), self.rows_max, self.V,
-                                                   ptr(self.amax), ptr(self.lm_work), stream_ptr()), "argmax")
+                                                   ptr(self.amax), ptr(self.lm_work), *self._bias_args(run.trt),
+                                                   stream_ptr()), "argmax")
             raise_for_status(L_.card_verify_argmax(run.E_ptr, run.q_tok_ptr, ptr(self.amax), stream_ptr()),
                              "verify_argmax")
 
