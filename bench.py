@@ -45,6 +45,7 @@ def parse():
     ap.add_argument("--k", type=int, default=3)
     ap.add_argument("--ratio", type=int, default=7)
     ap.add_argument("--temperature", type=float, default=0.0)
+    ap.add_argument("--mode", default="serial_sim", choices=["serial_sim", "concurrent"])
     ap.add_argument("--bias-sharpness", type=float, default=float(os.environ.get("CARD_BIAS", "1e6")))
     ap.add_argument("--bias-mix", type=float, default=0.0)
     ap.add_argument("--draft", default="llama-3.2-1b")
@@ -259,7 +260,7 @@ def main():
     torch.cuda.synchronize()
     init_s = time.perf_counter() - t_init
     cfg = card.EngineConfig(K=args.K, k=args.k, ratio=args.ratio, temperature=args.temperature,
-                            max_new_tokens=args.new_tokens, seed=0)
+                            max_new_tokens=args.new_tokens, seed=0, mode=args.mode)
     P = prompts(args.warmup + args.steps, tcfg.vocab_size, args.prompt_len, rank)
 
     def barrier():
@@ -330,7 +331,7 @@ def main():
         "config": {"workload": f"CARD {args.draft} draft + {args.target} target, 1 request/GPU (time-shared)",
                    "model": f"{args.draft}+{args.target}", "global_batch": world, "seq_len": args.prompt_len,
                    "new_tokens": args.new_tokens, "K": args.K, "k": args.k, "ratio": args.ratio,
-                   "temperature": args.temperature, "parallelism": f"dp{world} replicas",
+                   "temperature": args.temperature, "mode": args.mode, "parallelism": f"dp{world} replicas",
                    "agreement_knob": {"kgram_logit_bias_sharpness": args.bias_sharpness, "mix_weight": args.bias_mix},
                    "l2": "weights 17.5 GB >> 126 MB L2: streamed from HBM every step (no flush needed)"},
         "speedup_vs_ar": round(value / ar_value, 3),

@@ -259,6 +259,10 @@ int card_draft_promote(card_engine_state* E, card_cache* h, void** k_layers, voi
 int card_kv_compact(card_engine_state* E, card_cache* h, void** k_layers, void** v_layers, int n_layers,
                     int row_elems, int esize, int tree_base, void** scratch_kv, int capacity, void* stream);
 int card_cycle_end(card_engine_state* E, card_cache* h, void* stream);
+/* mode="concurrent": copy the target state's commit outcome (C, accepted
+ * tokens, correction, done) into the draft-side state before the correction
+ * is applied on the draft stream (engine.py:320-389 lock + epoch protocol). */
+int card_engine_handoff(const card_engine_state* target_state, card_engine_state* draft_state, void* stream);
 
 #ifdef __cplusplus
 }

@@ -86,6 +86,7 @@ SIGNATURES = {
     "card_draft_promote": (c_int, [_P, _P, _P, _P, c_int, c_int, c_int, c_int, c_int, _P]),
     "card_kv_compact": (c_int, [_P, _P, _P, _P, c_int, c_int, c_int, c_int, _P, c_int, _P]),
     "card_cycle_end": (c_int, [_P, _P, _P]),
+    "card_engine_handoff": (c_int, [_P, _P, _P]),
 }
 
 
@@ -108,7 +109,7 @@ LAUNCHES = {
     "card_topk_logits": 2, "card_argmax_logits": 2, "card_softmax64": 1, "card_logit_bias": 1,
     "card_draft_rows": 1, "card_target_rows": 1, "card_eos_fix": 1, "card_record_width": 1,
     "card_verify_argmax": 1, "card_verify_probs": 1, "card_commit": 1, "card_draft_promote": 2,
-    "card_kv_compact": 2, "card_cycle_end": 1,
+    "card_kv_compact": 2, "card_cycle_end": 1, "card_engine_handoff": 1,
 }
 launch_count = [0]
 

@@ -481,6 +481,22 @@ __global__ void kv_compact_scatter_kernel(const card_engine_state* E, const card
     }
 }
 
+// concurrent mode: the target's commit outcome -> the draft-side state (the
+// correction signal of engine.py:264-272; the draft keeps its own Pd)
+__global__ void handoff_kernel(const card_engine_state* T, card_engine_state* D) {
+    if (threadIdx.x != 0) return;
+    D->C = T->C;
+    D->C_prev = T->C_prev;
+    D->base_len = T->base_len;
+    D->done = T->done;
+    D->out_len = T->out_len;
+    D->n_acc = T->n_acc;
+    D->corr = T->corr;
+    for (int i = 0; i < 64; ++i) D->acc[i] = T->acc[i];
+    D->stop = 0;
+    D->n_widths = 0;
+}
+
 __global__ void cycle_end_kernel(card_engine_state* E, const card_cache_state* S, const int32_t* layer,
                                  const int32_t* frontier) {
     if (threadIdx.x != 0) return;
@@ -612,6 +628,12 @@ int card_kv_compact(card_engine_state* E, card_cache* h, void** k_layers, void**
     dim3 g(n_layers, capacity < 128 ? capacity : 128);
     kv_compact_gather_kernel<<<g, 128, 0, (cudaStream_t)stream>>>(E, S, remap, P, X, tree_base);
     kv_compact_scatter_kernel<<<g, 128, 0, (cudaStream_t)stream>>>(E, S, P, X, tree_base);
+    CARD_LAUNCH_CHECK();
+    return CARD_OK;
+}
+
+int card_engine_handoff(const card_engine_state* target_state, card_engine_state* draft_state, void* stream) {
+    handoff_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(target_state, draft_state);
     CARD_LAUNCH_CHECK();
     return CARD_OK;
 }

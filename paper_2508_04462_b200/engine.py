@@ -302,10 +302,10 @@ class _LlamaAdapter:
         rt = self.rt
         L_ = lib()
         nL = self.m.cfg.n_layers
-        raise_for_status(L_.card_draft_promote(run.E_ptr, run.cache.handle, ptr(rt.k_ptrs), ptr(rt.v_ptrs), nL,
+        raise_for_status(L_.card_draft_promote(run.Ed_ptr, run.cache.handle, ptr(rt.k_ptrs), ptr(rt.v_ptrs), nL,
                                                rt.kv_row_elems(), rt.kv_esize(), rt.tree_base, run.cfg.max_depth + 2,
                                                stream_ptr()), "draft_promote")
-        raise_for_status(L_.card_kv_compact(run.E_ptr, run.cache.handle, ptr(rt.k_ptrs), ptr(rt.v_ptrs), nL,
+        raise_for_status(L_.card_kv_compact(run.Ed_ptr, run.cache.handle, ptr(rt.k_ptrs), ptr(rt.v_ptrs), nL,
                                             rt.kv_row_elems(), rt.kv_esize(), rt.tree_base, ptr(self.scratch_ptrs),
                                             run.cache_capacity, stream_ptr()), "kv_compact")
 
@@ -372,8 +372,15 @@ class DeviceRun:
         st.n_uni = n_uni
         self.E = torch.frombuffer(bytearray(bytes(st)), dtype=torch.int32).to(self.dev)
         self.E_ptr = ptr(self.E)
+        # draft-side state: the same buffer in the lockstep drivers; a separate
+        # copy in mode="concurrent" (the draft stream never reads the target's
+        # in-flight commit; card_engine_handoff passes it over after each verify)
+        self.concurrent = config.mode == "concurrent"
+        self.Ed = self.E.clone() if self.concurrent else self.E
+        self.Ed_ptr = ptr(self.Ed)
         self.q_tok_ptr = ctypes.c_void_p(self.cache._qbufs[1])
         self._host = torch.empty(self.E.numel(), dtype=torch.int32, pin_memory=True)
+        self._host_d = torch.empty(self.E.numel(), dtype=torch.int32, pin_memory=True)
         self.da = _adapter(draft, "draft", self, self.d_rows_max)
         self.ta = _adapter(target, "target", self, self.t_rows_max)
         self._field = {name: getattr(EngineState, name).offset // 4 for name, _ in EngineState._fields_}
@@ -383,8 +390,9 @@ class DeviceRun:
         self.timing = {}
 
     # ---------------------------------------------------------------- state io
-    def _fptr(self, name: str) -> ctypes.c_void_p:
-        return ctypes.c_void_p(self.E.data_ptr() + 4 * self._field[name])
+    def _fptr(self, name: str, draft: bool = False) -> ctypes.c_void_p:
+        buf = self.Ed if draft else self.E
+        return ctypes.c_void_p(buf.data_ptr() + 4 * self._field[name])
 
     def read_state(self) -> EngineState:
         self._host.copy_(self.E, non_blocking=True)
@@ -393,6 +401,8 @@ class DeviceRun:
 
     def _set_field(self, name: str, value: int):
         self.E[self._field[name]] = int(value)
+        if self.Ed is not self.E:
+            self.Ed[self._field[name]] = int(value)
 
     def prefill(self):
         """Prompt KV for both models: target gets prompt[:-1] (its last token is
@@ -406,19 +416,20 @@ class DeviceRun:
     def launch_draft_step(self):
         L_ = lib()
         s = stream_ptr()
-        raise_for_status(L_.card_draft_rows(self.E_ptr, self.cache.handle, ptr(self.committed), ptr(self.drt.rows.block),
+        raise_for_status(L_.card_draft_rows(self.Ed_ptr, self.cache.handle, ptr(self.committed), ptr(self.drt.rows.block),
                                             self.d_rows_max, self.drt.rows.extra_max,
                                             getattr(self.da, "rt", None).tree_base if hasattr(self.da, "rt") else 0,
                                             ptr(self.drt.tail), self.drt.order, s), "draft_rows")
         tok, val, cnt, probs = self.da.draft(self)
         raise_for_status(L_.card_cache_expand_topk(self.cache.handle, ptr(tok), ptr(val), ptr(cnt), -1, probs,
-                                                   self._fptr("stop"), s), "expand")
-        raise_for_status(L_.card_record_width(self.E_ptr, self.cache.handle, ptr(self.drt.rows.n_out), s), "record")
+                                                   self._fptr("stop", True), s), "expand")
+        raise_for_status(L_.card_record_width(self.Ed_ptr, self.cache.handle, ptr(self.drt.rows.n_out), s), "record")
 
-    def launch_target_step(self, with_correct: bool = True, readback: bool = True):
+    def launch_target_step(self, with_correct: bool = True, readback: bool = True, with_query: bool = True):
         L_ = lib()
         s = stream_ptr()
-        raise_for_status(L_.card_cache_query(self.cache.handle, self.cfg.query_depth, s), "query")
+        if with_query:
+            raise_for_status(L_.card_cache_query(self.cache.handle, self.cfg.query_depth, s), "query")
         raise_for_status(L_.card_target_rows(self.E_ptr, self.cache.handle, ptr(self.committed),
                                              ptr(self.trt.rows.block), self.t_rows_max, 1, ptr(self.trt.tail),
                                              self.trt.order, s), "target_rows")
@@ -426,7 +437,8 @@ class DeviceRun:
         raise_for_status(L_.card_commit(self.E_ptr, ptr(self.committed), s), "commit")
         if with_correct:
             self.launch_correct()
-        raise_for_status(L_.card_cycle_end(self.E_ptr, self.cache.handle, s), "cycle_end")
+        raise_for_status(L_.card_cycle_end(self.E_ptr, None if self.concurrent else self.cache.handle, s),
+                         "cycle_end")
         if readback:
             self._host.copy_(self.E, non_blocking=True)
 
@@ -463,8 +475,8 @@ class DeviceRun:
     def launch_correct(self):
         L_ = lib()
         s = stream_ptr()
-        raise_for_status(L_.card_cache_correct(self.cache.handle, self._fptr("acc"), self._fptr("n_acc"),
-                                               self._fptr("corr"), self._fptr("done"), s), "correct")
+        raise_for_status(L_.card_cache_correct(self.cache.handle, self._fptr("acc", True), self._fptr("n_acc", True),
+                                               self._fptr("corr", True), self._fptr("done", True), s), "correct")
         self.da.post_correct(self)
 
     def correct_sync(self):
@@ -601,6 +613,129 @@ class DeviceRun:
         return cycles
 
 
+class _ConcurrentDriver:
+    """mode="concurrent" (engine.py:320-389) on one GPU: the draft expands the
+    tree on its own stream while the target verifies on another.  The
+    reference's lock + epoch protocol becomes stream order plus a hand-off:
+
+      draft stream  : [draft step]* ... wait(V) [handoff E->Ed, correct,
+                      draft-KV roll-forward, query] -> event Q ... [draft step]*
+      target stream : wait(Q) [target rows, verify forward, accept, commit,
+                      record -> host] -> event V
+
+    The cache is only mutated on the draft stream, so corrections and
+    expansions never race (the reference discards stale expansions by epoch,
+    engine.py:359-360; here they are ordered).  At most one draft step is in
+    flight so a correction waits for at most one.  Greedy output is
+    schedule-invariant (lossless); the trace carries wall-clock times."""
+
+    def __init__(self, run: "DeviceRun"):
+        from . import _lib
+
+        self.run = run
+        self.D, self.T = torch.cuda.Stream(), torch.cuda.Stream()
+        cap = torch.cuda.Stream()
+        cap.wait_stream(torch.cuda.current_stream())
+        self.g_d, self.g_q, self.g_t, self.g_c = (torch.cuda.CUDAGraph() for _ in range(4))
+        with torch.cuda.stream(cap):
+            c = [_lib.launch_count[0]]
+            with torch.cuda.graph(self.g_d, stream=cap):
+                run.launch_draft_step()
+                run._host_d.copy_(run.Ed, non_blocking=True)
+            c.append(_lib.launch_count[0])
+            with torch.cuda.graph(self.g_q, stream=cap):
+                raise_for_status(lib().card_cache_query(run.cache.handle, run.cfg.query_depth, stream_ptr()), "query")
+            c.append(_lib.launch_count[0])
+            with torch.cuda.graph(self.g_t, stream=cap):
+                run.launch_target_step(with_correct=False, readback=True, with_query=False)
+            c.append(_lib.launch_count[0])
+            with torch.cuda.graph(self.g_c, stream=cap):
+                raise_for_status(lib().card_engine_handoff(run.E_ptr, run.Ed_ptr, stream_ptr()), "handoff")
+                run.launch_correct()
+                raise_for_status(lib().card_cache_query(run.cache.handle, run.cfg.query_depth, stream_ptr()), "query")
+            c.append(_lib.launch_count[0])
+        torch.cuda.current_stream().wait_stream(cap)
+        self.per_graph = [c[i + 1] - c[i] for i in range(4)]
+        self.replays = [0, 0, 0, 0]
+
+    def _draft(self):
+        with torch.cuda.stream(self.D):
+            self.g_d.replay()
+            ev = torch.cuda.Event()
+            ev.record(self.D)
+        self.replays[0] += 1
+        return ev
+
+    def _draft_done(self, t0):
+        """Read the finished draft step's record: width (trace) and stop flag."""
+        run = self.run
+        Ed = EngineState.from_buffer_copy(run._host_d.numpy().tobytes())
+        n = Ed.n_widths
+        w = Ed.widths[n - 1] if 0 < n <= 64 else 0
+        if w > 0:
+            run._emit(time.perf_counter() - t0, False, w, 0, 0, "draft_expand")
+        return bool(Ed.stop)
+
+    def run_loop(self):
+        run, cfg = self.run, self.run.cfg
+        t0 = time.perf_counter()
+        torch.cuda.current_stream().synchronize()
+        self.D.wait_stream(torch.cuda.current_stream())
+        self.T.wait_stream(torch.cuda.current_stream())
+        # warm-up: query_depth expansions before the first target step (engine.py:377)
+        paused = False
+        for _ in range(min(cfg.query_depth, cfg.max_depth)):
+            ev = self._draft()
+            ev.synchronize()
+            if self._draft_done(t0):
+                paused = True
+                break
+        with torch.cuda.stream(self.D):
+            self.g_q.replay()
+            q_ev = torch.cuda.Event()
+            q_ev.record(self.D)
+        self.replays[1] += 1
+        d_ev = None
+        done = False
+        while not done:
+            self.T.wait_event(q_ev)
+            with torch.cuda.stream(self.T):
+                self.g_t.replay()
+                v_ev = torch.cuda.Event()
+                v_ev.record(self.T)
+            self.replays[2] += 1
+            while not v_ev.query():
+                if d_ev is not None and d_ev.query():
+                    paused = self._draft_done(t0)
+                    d_ev = None
+                if d_ev is None and not paused:
+                    d_ev = self._draft()
+            E = EngineState.from_buffer_copy(run._host.numpy().tobytes())
+            now = time.perf_counter() - t0
+            hit = bool(E.rec_hit)
+            run.output.extend(E.committed_now[i] for i in range(E.n_commit))
+            run._emit_target(now, hit, E)
+            done = bool(E.rec_done)
+            if done:
+                break
+            if d_ev is not None:   # the correction follows the in-flight draft step on its stream
+                d_ev.synchronize()
+                self._draft_done(t0)
+                d_ev = None
+            self.D.wait_event(v_ev)
+            with torch.cuda.stream(self.D):
+                self.g_c.replay()
+                q_ev = torch.cuda.Event()
+                q_ev.record(self.D)
+            self.replays[3] += 1
+            paused = False
+            run._emit(time.perf_counter() - t0, hit, 0, 0, 0, "correct")
+        torch.cuda.synchronize()
+
+    def launches(self) -> int:
+        return sum(r * n for r, n in zip(self.replays, self.per_graph))
+
+
 def _validate_run_config(draft, target, config):
     if config.max_depth > 30:
         raise ConfigError("max_depth > 30 is not supported by the device tree attention")
@@ -625,6 +760,24 @@ def run_speculative(draft, target, prompt: Sequence[TokenId], config: EngineConf
         use_graphs = "llama" in kinds and config.correction_enabled
     if trace_alive is None:
         trace_alive = not use_graphs
+    concurrent = config.mode == "concurrent" and config.correction_enabled and use_graphs
+    if concurrent:
+        run = DeviceRun(draft, target, prompt, config, trace_alive=False)
+        t0 = time.perf_counter()
+        run.prefill()
+        drv = _ConcurrentDriver(run)
+        torch.cuda.synchronize()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record()
+        drv.run_loop()
+        ev1.record()
+        ev1.synchronize()
+        run.timing["decode_ms"] = ev0.elapsed_time(ev1)
+        run.timing["gpu_launches"] = drv.launches()
+        run.timing["draft_steps"], run.timing["target_steps"] = drv.replays[0], drv.replays[2]
+        run.timing["wall_s"] = time.perf_counter() - t0
+        return RunResult(output=run.output, metrics=finalize(run.trace, target.spec, draft.spec), trace=run.trace,
+                         wall=run.timing)
     run = DeviceRun(draft, target, prompt, config, trace_alive=trace_alive)
     t0 = time.perf_counter()
     if use_graphs:

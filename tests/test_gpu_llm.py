@@ -170,3 +170,23 @@ def test_card_greedy_lossless_high_acceptance_bf16(card):
     res = card.run_speculative(d, t, prompt, cfg, use_graphs=True)
     assert res.metrics.mean_acceptance_length > 2.5, res.metrics.mean_acceptance_length
     assert res.output == van.output
+
+
+@pytest.mark.parametrize("dtype", ["fp32", "bf16"])
+def test_concurrent_mode_is_lossless(card, dtype):
+    """mode="concurrent" (engine.py:320-389): draft and target on two streams
+    with the device hand-off; greedy tokens equal autoregressive decoding."""
+    from paper_2508_04462_b200.lm import LogitBias
+
+    preset = ("tiny-target", "tiny-draft") if dtype == "fp32" else ("small-target", "small-draft")
+    sharp = 30.0 if dtype == "fp32" else 4000.0
+    bias = LogitBias(seed=11, order=2, sharpness=sharp, mix_seed=131, mix_weight=0.0)
+    d, t, *_ = _tiny_pair(card, dtype, *preset, bias=bias)
+    prompt = [int(x) for x in np.random.default_rng(7).integers(0, t.vocab.size, 48)]
+    cfg = card.EngineConfig(K=16, k=3, ratio=5, max_new_tokens=160, mode="concurrent")
+    van = card.run_vanilla(t, prompt, cfg)
+    res = card.run_speculative(d, t, prompt, cfg, use_graphs=True)
+    assert res.output == van.output
+    assert res.wall["target_steps"] < len(res.output)   # more than one token per verify on average
+    events = {e.event for e in res.trace}
+    assert {"verify", "correct"} <= events
