@@ -64,6 +64,7 @@ SIGNATURES = {
     "card_rmsnorm": (c_int, [_P, _P, c_int, ctypes.c_float, _P, c_int, _P, _P, c_int, _P]),
     "card_rope_kv": (c_int, [_P, _P, c_int, _P, _P, _P, _P, c_int, c_int, c_int, _P, _P, _P, c_int, _P]),
     "card_attention_work_floats": (c_int, [c_int, c_int, c_int, c_int]),
+    "card_attention_trace": (c_int, [_P]),
     "card_attention": (c_int, [_P, _P, c_int, _P, _P, _P, c_int, _P, _P, c_int, c_int, c_int, c_int, c_int, _P,
                                _P, c_int, _P]),
     "card_lmhead_work_floats": (c_int, [c_int, c_int]),

@@ -80,9 +80,19 @@ __device__ __forceinline__ void st_cl_v2(uint32_t addr, float a, float b) {
     asm volatile("st.shared::cluster.v2.f32 [%0], {%1, %2};" ::"r"(addr), "f"(a), "f"(b) : "memory");
 }
 
+__device__ unsigned long long* g_attn_trace = nullptr;   // tuning: [grid][8] %globaltimer stamps
+__device__ __forceinline__ void at_stamp(int k) {
+    if (g_attn_trace && threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        const int cta = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+        g_attn_trace[cta * 8 + k] = t;
+    }
+}
+
 }  // namespace
 
-// smem: K[kCh][HD+8] bf16 | V[kCh][HD+8] bf16 | recv[S][kQT/S][HD+2] f32
+// smem: 2 x (K[kCh][HD+8] bf16 | V[kCh][HD+8] bf16) | recv[S][kQT/S][HD+2] f32
 template <int HD>
 __global__ void __launch_bounds__(kThreads) attn_fused_kernel(const float* __restrict__ q, const int32_t* dM,
                                                              const int32_t* __restrict__ plen,
@@ -94,12 +104,14 @@ __global__ void __launch_bounds__(kThreads) attn_fused_kernel(const float* __res
     constexpr int LD = HD + 8;   // padded bf16 row: 16-byte aligned, conflict-free 32-bit fragment loads
     constexpr int PW = HD + 2;   // partial record: m, l, o[HD]
     extern __shared__ __align__(16) uint8_t smem[];
-    __nv_bfloat16* Ks = reinterpret_cast<__nv_bfloat16*>(smem);
-    __nv_bfloat16* Vs = Ks + kCh * LD;
-    float* recv = reinterpret_cast<float*>(Vs + kCh * LD);
+    __nv_bfloat16* Ks = reinterpret_cast<__nv_bfloat16*>(smem);   // [2][kCh][LD] (double buffer)
+    __nv_bfloat16* Vs = Ks + 2 * kCh * LD;                         // [2][kCh][LD]
+    float* recv = reinterpret_cast<float*>(Vs + 2 * kCh * LD);
 
+    at_stamp(0);
     pdl_wait();
     pdl_trigger();
+    at_stamp(1);
     const int S = gridDim.x;
     const int rank = (int)cl_rank();
     const int qt = blockIdx.y, g = blockIdx.z;
@@ -112,6 +124,24 @@ __global__ void __launch_bounds__(kThreads) attn_fused_kernel(const float* __res
     const int warp = warp_id(), lane = lane_id();
     const int gq = lane >> 2, tq = lane & 3;
 
+    // chunk `rank` is a prefix chunk when rank*64 < plen of the tile's last row
+    // (plen never decreases along the rows the builders emit): start staging it
+    // now so its latency overlaps the prologue (double buffer 0)
+    const int early_kmax = plen[min(M - 1, (q0 + kQT - 1) / G)];
+    const uint32_t ks_base = s_u32(Ks), vs_base = s_u32(Vs);
+    auto stage_rows = [&](int c, int b, auto slot_of) {
+        const int ks0 = c * kCh;
+        const uint32_t kb = ks_base + (uint32_t)(b * kCh * LD * 2), vb = vs_base + (uint32_t)(b * kCh * LD * 2);
+        for (int idx = threadIdx.x; idx < kCh * HD / 8; idx += kThreads) {
+            const int j = idx / (HD / 8), d8 = (idx % (HD / 8)) * 8;
+            const int64_t src = (slot_of(ks0 + j) * nkv + g) * HD + d8;
+            cp_async16(kb + (uint32_t)((j * LD + d8) * 2), kc + src);
+            cp_async16(vb + (uint32_t)((j * LD + d8) * 2), vc + src);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    const bool prestaged = rank * kCh < early_kmax;
+    if (prestaged) stage_rows(rank, 0, [](int k) { return (int64_t)k; });
     // keys needed by this tile: max plen over its rows (prefix chunks), and
     // the tile rows' extra slots concatenated row by row (extra chunks: row
     // i's keys are [xoff[i], xoff[i] + xne[i]) of the gathered list)
@@ -119,19 +149,31 @@ __global__ void __launch_bounds__(kThreads) attn_fused_kernel(const float* __res
     __shared__ int xoff[kMaxTileRows], xne[kMaxTileRows];
     __shared__ int xs[kMaxExtra];
     const int r0 = q0 / G, r1 = min(M - 1, (q0 + kQT - 1) / G);
-    if (threadIdx.x == 0) {
-        int kmax = 0, off = 0;
-        for (int i = 0; i <= r1 - r0; ++i) {
-            const int r = r0 + i;
-            kmax = max(kmax, plen[r]);
-            int ne = min(n_extra[r], extra_max);
-            ne = max(0, min(ne, kMaxExtra - off));
-            xoff[i] = off;
-            xne[i] = ne;
-            off += ne;
+    const int nrows = r1 - r0 + 1;   // <= kMaxTileRows
+    // one thread per tile row loads (plen, n_extra); warp 0 scans the extra
+    // counts (a serial single-thread loop of dependent loads cost ~10 us)
+    if (threadIdx.x == 0) s_kmax = 0;
+    for (int i = threadIdx.x; i < nrows; i += kThreads) xne[i] = max(0, min(n_extra[r0 + i], extra_max));
+    __syncthreads();
+    for (int i = threadIdx.x; i < nrows; i += kThreads) atomicMax(&s_kmax, plen[r0 + i]);
+    if (warp_id() == 0) {
+        int carry = 0;
+        for (int b0 = 0; b0 < nrows; b0 += 32) {
+            const int i = b0 + lane_id();
+            const int v = i < nrows ? xne[i] : 0;
+            int x = v;
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane_id() >= o) x += y;
+            }
+            if (i < nrows) {
+                const int off = carry + x - v;
+                xoff[i] = off;
+                xne[i] = max(0, min(v, kMaxExtra - off));   // clip to the gathered-list capacity
+            }
+            carry += __shfl_sync(0xffffffffu, x, 31);
         }
-        s_kmax = kmax;
-        s_nx = off;
+        if (lane_id() == 0) s_nx = min(carry, kMaxExtra);
     }
     __syncthreads();
     for (int i = 0; i <= r1 - r0; ++i)
@@ -171,22 +213,35 @@ __global__ void __launch_bounds__(kThreads) attn_fused_kernel(const float* __res
     for (int n = 0; n < HD / 8; ++n) oacc[n][0] = oacc[n][1] = oacc[n][2] = oacc[n][3] = 0.f;
     float ma = -INFINITY, mb = -INFINITY, la = 0.f, lb = 0.f;
 
-    const uint32_t ks_base = s_u32(Ks), vs_base = s_u32(Vs);
     __syncthreads();   // xs complete
-    for (int c = rank; c < n_all; c += S) {
+    at_stamp(2);
+    // stage chunk c into buffer b (cp.async, one commit group per chunk)
+    // gathered padding rows read slot xs[0] (finite data: 0 * V must stay 0)
+    const int nx = s_nx;
+    auto stage = [&](int c, int b) {
+        if (c >= n_ch)
+            stage_rows(c - n_ch, b, [&](int k) { return (int64_t)xs[k < nx ? k : 0]; });
+        else
+            stage_rows(c, b, [](int k) { return (int64_t)k; });
+    };
+    if (rank < n_all && !prestaged) stage(rank, 0);
+    int buf = 0;
+    for (int c = rank; c < n_all; c += S, buf ^= 1) {
         const bool xc = c >= n_ch;   // extra (gathered) chunk
         const int k0 = (xc ? c - n_ch : c) * kCh;
-        __syncthreads();   // previous chunk fully consumed
-        for (int idx = threadIdx.x; idx < kCh * HD / 8; idx += kThreads) {
-            const int j = idx / (HD / 8), d8 = (idx % (HD / 8)) * 8;
-            // gathered padding rows read slot xs[0] (finite data: 0 * V must stay 0)
-            const int64_t slot = xc ? (int64_t)xs[(k0 + j < s_nx) ? k0 + j : 0] : (int64_t)(k0 + j);
-            const int64_t src = (slot * nkv + g) * HD + d8;
-            cp_async16(ks_base + (uint32_t)((j * LD + d8) * 2), kc + src);
-            cp_async16(vs_base + (uint32_t)((j * LD + d8) * 2), vc + src);
+        __syncthreads();   // the other buffer (chunk c - S) is fully consumed
+        // prefetch the next chunk into the other buffer while this one is used
+        if (c + S < n_all) {
+            stage(c + S, buf ^ 1);
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
         }
-        cp_async_wait_all();
-        __syncthreads();
+        __syncthreads();   // chunk c visible to every warp
+        if (c == rank) at_stamp(3);
+        const uint32_t kcur = ks_base + (uint32_t)(buf * kCh * LD * 2);
+        const uint32_t vcur = vs_base + (uint32_t)(buf * kCh * LD * 2);
+        const __nv_bfloat16* Kc = Ks + buf * kCh * LD;
         if (!warp_live) continue;
         // visible chunk keys of rows a / b: [loa, hia) / [lob, hib)
         int loa = 0, hia = pla - k0, lob = 0, hib = plb - k0;
@@ -204,7 +259,7 @@ __global__ void __launch_bounds__(kThreads) attn_fused_kernel(const float* __res
         for (int ks = 0; ks < HD / 16; ++ks)
 #pragma unroll
             for (int n = 0; n < kCh / 8; ++n) {
-                const __nv_bfloat16* kr = Ks + (n * 8 + gq) * LD + ks * 16 + 2 * tq;
+                const __nv_bfloat16* kr = Kc + (n * 8 + gq) * LD + ks * 16 + 2 * tq;
                 uint32_t b[2];
                 b[0] = *reinterpret_cast<const uint32_t*>(kr);
                 b[1] = *reinterpret_cast<const uint32_t*>(kr + 8);
@@ -269,13 +324,14 @@ __global__ void __launch_bounds__(kThreads) attn_fused_kernel(const float* __res
                 const int key = kk * 16 + (mat & 1) * 8 + mrow;
                 const int dim = (nd + (mat >> 1)) * 8;
                 uint32_t b0, b1, b2, b3;
-                ldsm_x4_trans(vs_base + (uint32_t)((key * LD + dim) * 2), b0, b1, b2, b3);
+                ldsm_x4_trans(vcur + (uint32_t)((key * LD + dim) * 2), b0, b1, b2, b3);
                 const uint32_t bA[2] = {b0, b1}, bB[2] = {b2, b3};
                 mma16816(oacc[nd], p[kk], bA);
                 mma16816(oacc[nd + 1], p[kk], bB);
             }
     }
 
+    at_stamp(4);
     // push this rank's partial (m, l, o) for its 64 query-heads to the owners
     const uint32_t recv_base = s_u32(recv);
     if (warp_live) {
@@ -294,28 +350,45 @@ __global__ void __launch_bounds__(kThreads) attn_fused_kernel(const float* __res
             st_cl_v2(db + (uint32_t)((2 + d) * 4), oacc[nd][2], oacc[nd][3]);
         }
     }
+    at_stamp(5);
     cl_sync();   // every partial has landed in its owner's smem
-    // owner merge: query-heads [rank*QO, rank*QO + QO), S partials in rank order
+    at_stamp(6);
+    // owner merge: query-heads [rank*QO, rank*QO + QO), S partials in rank
+    // order.  Per query-head weights w_s / L first (one thread each), then
+    // every output element is S independent loads.
+    __shared__ float s_w[kQT][8];
+    if (threadIdx.x < QO) {
+        const int ql = threadIdx.x;
+        float Mx = -INFINITY;
+        for (int s = 0; s < S; ++s) Mx = fmaxf(Mx, recv[(s * QO + ql) * PW]);
+        const float Ms = Mx == -INFINITY ? 0.f : Mx;
+        float w[8], L = 0.f;
+        for (int s = 0; s < S; ++s) {
+            const float* rec = recv + (s * QO + ql) * PW;
+            w[s] = rec[0] == -INFINITY ? 0.f : __expf(rec[0] - Ms);
+            L += w[s] * rec[1];
+        }
+        const float invL = L > 0.f ? 1.0f / L : 0.f;
+        for (int s = 0; s < S; ++s) s_w[ql][s] = w[s] * invL;
+    }
+    __syncthreads();
     for (int e = threadIdx.x; e < QO * HD; e += kThreads) {
         const int ql = e / HD, d = e - ql * HD;
         const int qi = q0 + rank * QO + ql;
         if (qi >= nq) break;
-        float Mx = -INFINITY;
-        for (int s = 0; s < S; ++s) Mx = fmaxf(Mx, recv[(s * QO + ql) * PW]);
-        const float Ms = Mx == -INFINITY ? 0.f : Mx;
-        float L = 0.f, acc = 0.f;
-        for (int s = 0; s < S; ++s) {
-            const float* rec = recv + (s * QO + ql) * PW;
-            const float w = rec[0] == -INFINITY ? 0.f : __expf(rec[0] - Ms);
-            L += w * rec[1];
-            acc += w * rec[2 + d];
-        }
+        float acc = 0.f;
+        for (int s = 0; s < S; ++s) acc += s_w[ql][s] * recv[(s * QO + ql) * PW + 2 + d];
         const int r = qi / G, h = g * G + qi % G;
-        o_out[((int64_t)r * nh + h) * HD + d] = __float2bfloat16(L > 0.f ? acc / L : 0.f);
+        o_out[((int64_t)r * nh + h) * HD + d] = __float2bfloat16(acc);
     }
+    at_stamp(7);
 }
 
-int attn_fused_smem(int hd, int S) { return 2 * kCh * (hd + 8) * 2 + S * (kQT / S) * (hd + 2) * 4; }
+int attn_set_trace(unsigned long long* buf) {
+    return cudaMemcpyToSymbol(g_attn_trace, &buf, sizeof(buf)) == cudaSuccess ? CARD_OK : CARD_E_CUDA;
+}
+
+int attn_fused_smem(int hd, int S) { return 4 * kCh * (hd + 8) * 2 + S * (kQT / S) * (hd + 2) * 4; }
 
 int launch_attn_fused(const float* q, const int32_t* dM, int m_max, const int32_t* plen, const int32_t* n_extra,
                       const int32_t* extra, int extra_max, const void* kc, const void* vc, int nh, int nkv, int hd,

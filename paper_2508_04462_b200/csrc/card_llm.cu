@@ -943,6 +943,8 @@ int card_rope_kv(const float* qkv, const int32_t* dM, int m_max, const int32_t* 
     return CARD_OK;
 }
 
+int card_attention_trace(unsigned long long* buf) { return attn_set_trace(buf); }
+
 int card_attention_work_floats(int m_max, int nh, int hd, int max_plen) {
     const int n_splits = (max_plen + kChunk - 1) / kChunk;
     return m_max * nh * (n_splits + 1) * (hd + 2);

@@ -11,6 +11,7 @@ namespace card {
 int launch_attn_fused(const float* q, const int32_t* dM, int m_max, const int32_t* plen, const int32_t* n_extra,
                       const int32_t* extra, int extra_max, const void* kc, const void* vc, int nh, int nkv, int hd,
                       int max_plen, void* o, cudaStream_t s);
+int attn_set_trace(unsigned long long* buf);
 }  // namespace card
 
 // GEMM epilogues (card_gemm.cu)
