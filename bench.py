@@ -116,6 +116,21 @@ def prompts(n, V, L, rank=0):
     return [[int(x) for x in np.random.default_rng(1000 + i + 10000 * rank).integers(0, V, L)] for i in range(n)]
 
 
+def aggregate_ranks(tokens, dec_ms, e2e_s, world, device):
+    """DP replicas (weak scaling, no data-path collective): total tokens over
+    all ranks, and the slowest rank's device / end-to-end time."""
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([float(tokens), float(dec_ms), float(e2e_s)], dtype=torch.float64, device=device)
+    if world <= 1:
+        return float(tokens), float(dec_ms), float(e2e_s)
+    tot, mx = t.clone(), t.clone()
+    dist.all_reduce(tot, op=dist.ReduceOp.SUM)
+    dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+    return tot[0].item(), mx[1].item(), mx[2].item()
+
+
 def traffic_from_profiles():
     p = os.path.join(ROOT, "profiles", "traffic.json")
     try:
@@ -297,15 +312,7 @@ def main():
     barrier()
     clk = clocks.stop()
     # whole-job aggregate: tokens over all ranks / max device time over ranks
-    tok_t = torch.tensor([float(tokens), dec_ms, e2e_s], dtype=torch.float64, device="cuda")
-    if world > 1:
-        tot = tok_t.clone()
-        dist.all_reduce(tot, op=dist.ReduceOp.SUM)
-        mx = tok_t.clone()
-        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-        all_tokens, max_ms, max_e2e = tot[0].item(), mx[1].item(), mx[2].item()
-    else:
-        all_tokens, max_ms, max_e2e = float(tokens), dec_ms, e2e_s
+    all_tokens, max_ms, max_e2e = aggregate_ranks(tokens, dec_ms, e2e_s, world, "cuda")
     value = all_tokens / (max_ms / 1000.0)
     # same-box GPU autoregressive baseline (same kernels; M = 1 rows)
     ar_tok = 0
