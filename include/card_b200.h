@@ -204,7 +204,9 @@ int card_rope_kv(const float* qkv, const int32_t* dM, int m_max, const int32_t* 
 int card_attention_work_floats(int m_max, int nh, int hd, int max_plen);
 /* tuning: per-CTA %globaltimer stamps [grid][8] of the fused attention (NULL disables) */
 int card_attention_trace(unsigned long long* buf);
-int card_attention(const float* q, const int32_t* dM, int m_max, const int32_t* plen,
+/* slot: the rows' KV slots (row block), lets the fused bf16 kernel start on old
+ * KV before the QKV GEMM that writes the new rows has finished */
+int card_attention(const float* q, const int32_t* dM, int m_max, const int32_t* plen, const int32_t* slot,
                    const int32_t* n_extra, const int32_t* extra, int extra_max, const void* k_cache,
                    const void* v_cache, int kvdtype, int nh, int nkv, int hd, int max_plen, float* work,
                    void* o, int odtype, void* stream);

@@ -65,7 +65,7 @@ SIGNATURES = {
     "card_rope_kv": (c_int, [_P, _P, c_int, _P, _P, _P, _P, c_int, c_int, c_int, _P, _P, _P, c_int, _P]),
     "card_attention_work_floats": (c_int, [c_int, c_int, c_int, c_int]),
     "card_attention_trace": (c_int, [_P]),
-    "card_attention": (c_int, [_P, _P, c_int, _P, _P, _P, c_int, _P, _P, c_int, c_int, c_int, c_int, c_int, _P,
+    "card_attention": (c_int, [_P, _P, c_int, _P, _P, _P, _P, c_int, _P, _P, c_int, c_int, c_int, c_int, c_int, _P,
                                _P, c_int, _P]),
     "card_lmhead_work_floats": (c_int, [c_int, c_int]),
     "card_topk_logits": (c_int, [_P, _P, c_int, c_int, c_int, c_double, _P, _P, _P, _P, _P, c_int, c_int, c_uint64,
@@ -106,7 +106,7 @@ LAUNCHES = {
     "card_kgram_dist": 1, "card_rows_topk": 1, "card_log_cr": 1, "card_exp_cr": 1,
     "card_cache_reset": 2, "card_cache_expand": 2, "card_cache_expand_topk": 1, "card_cache_pool": 2,
     "card_cache_query": 1, "card_cache_correct": 1, "card_cache_advance_root": 1, "card_cache_count_alive": 1,
-    "card_cache_clear_status": 1, "card_embed": 1, "card_rmsnorm": 1, "card_rope_kv": 1, "card_attention": lambda a: 1 if (a[9] == 0 and a[16] == 0 and a[12] in (64, 128)) else 3,
+    "card_cache_clear_status": 1, "card_embed": 1, "card_rmsnorm": 1, "card_rope_kv": 1, "card_attention": lambda a: 1 if (a[10] == 0 and a[17] == 0 and a[13] in (64, 128) and a[4]) else 3,
     "card_topk_logits": 2, "card_argmax_logits": 2, "card_softmax64": 1, "card_logit_bias": 1,
     "card_draft_rows": 1, "card_target_rows": 1, "card_eos_fix": 1, "card_record_width": 1,
     "card_verify_argmax": 1, "card_verify_probs": 1, "card_commit": 1, "card_draft_promote": 2,

@@ -96,6 +96,7 @@ __device__ __forceinline__ void at_stamp(int k) {
 template <int HD>
 __global__ void __launch_bounds__(kThreads) attn_fused_kernel(const float* __restrict__ q, const int32_t* dM,
                                                              const int32_t* __restrict__ plen,
+                                                             const int32_t* __restrict__ slot,
                                                              const int32_t* __restrict__ n_extra,
                                                              const int32_t* __restrict__ extra, int extra_max,
                                                              const __nv_bfloat16* __restrict__ kc,
@@ -109,9 +110,9 @@ __global__ void __launch_bounds__(kThreads) attn_fused_kernel(const float* __res
     float* recv = reinterpret_cast<float*>(Vs + 2 * kCh * LD);
 
     at_stamp(0);
-    pdl_wait();
-    pdl_trigger();
-    at_stamp(1);
+    // Everything up to the first K/V chunk reads only the row block and old KV
+    // slots, written before the previous kernel (the QKV GEMM) started; it runs
+    // before griddepcontrol.wait and overlaps the GEMM's tail.
     const int S = gridDim.x;
     const int rank = (int)cl_rank();
     const int qt = blockIdx.y, g = blockIdx.z;
@@ -124,10 +125,6 @@ __global__ void __launch_bounds__(kThreads) attn_fused_kernel(const float* __res
     const int warp = warp_id(), lane = lane_id();
     const int gq = lane >> 2, tq = lane & 3;
 
-    // chunk `rank` is a prefix chunk when rank*64 < plen of the tile's last row
-    // (plen never decreases along the rows the builders emit): start staging it
-    // now so its latency overlaps the prologue (double buffer 0)
-    const int early_kmax = plen[min(M - 1, (q0 + kQT - 1) / G)];
     const uint32_t ks_base = s_u32(Ks), vs_base = s_u32(Vs);
     auto stage_rows = [&](int c, int b, auto slot_of) {
         const int ks0 = c * kCh;
@@ -140,8 +137,6 @@ __global__ void __launch_bounds__(kThreads) attn_fused_kernel(const float* __res
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
-    const bool prestaged = rank * kCh < early_kmax;
-    if (prestaged) stage_rows(rank, 0, [](int k) { return (int64_t)k; });
     // keys needed by this tile: max plen over its rows (prefix chunks), and
     // the tile rows' extra slots concatenated row by row (extra chunks: row
     // i's keys are [xoff[i], xoff[i] + xne[i]) of the gathered list)
@@ -181,6 +176,14 @@ __global__ void __launch_bounds__(kThreads) attn_fused_kernel(const float* __res
     const int n_ch = (s_kmax + kCh - 1) / kCh;
     const int n_xch = (s_nx + kCh - 1) / kCh;
     const int n_all = n_ch + n_xch;
+    // this rank's first chunk can be staged before the wait when it is a
+    // prefix chunk below every KV slot this forward writes (slot[0] is the
+    // lowest: catch-up / chain rows come first, tree slots lie above the prefix)
+    const bool prestaged = rank < n_ch && (rank + 1) * kCh <= slot[0];
+    if (prestaged) stage_rows(rank, 0, [](int k) { return (int64_t)k; });
+    pdl_wait();
+    pdl_trigger();
+    at_stamp(1);
 
     // this warp's 16 query-heads: rows a = gq, b = gq + 8
     const int qa = q0 + warp * 16 + gq, qb = qa + 8;
@@ -390,7 +393,8 @@ int attn_set_trace(unsigned long long* buf) {
 
 int attn_fused_smem(int hd, int S) { return 4 * kCh * (hd + 8) * 2 + S * (kQT / S) * (hd + 2) * 4; }
 
-int launch_attn_fused(const float* q, const int32_t* dM, int m_max, const int32_t* plen, const int32_t* n_extra,
+int launch_attn_fused(const float* q, const int32_t* dM, int m_max, const int32_t* plen, const int32_t* slot,
+                      const int32_t* n_extra,
                       const int32_t* extra, int extra_max, const void* kc, const void* vc, int nh, int nkv, int hd,
                       int max_plen, void* o, cudaStream_t s) {
     const int G = nh / nkv;
@@ -420,7 +424,7 @@ int launch_attn_fused(const float* q, const int32_t* dM, int m_max, const int32_
             cudaFuncSetAttribute(attn_fused_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
             a64 = true;
         }
-        e = cudaLaunchKernelEx(&cfg, attn_fused_kernel<64>, q, dM, plen, n_extra, extra, extra_max,
+        e = cudaLaunchKernelEx(&cfg, attn_fused_kernel<64>, q, dM, plen, slot, n_extra, extra, extra_max,
                                (const __nv_bfloat16*)kc, (const __nv_bfloat16*)vc, nh, nkv, (__nv_bfloat16*)o);
     } else {
         static bool a128 = false;
@@ -428,7 +432,7 @@ int launch_attn_fused(const float* q, const int32_t* dM, int m_max, const int32_
             cudaFuncSetAttribute(attn_fused_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
             a128 = true;
         }
-        e = cudaLaunchKernelEx(&cfg, attn_fused_kernel<128>, q, dM, plen, n_extra, extra, extra_max,
+        e = cudaLaunchKernelEx(&cfg, attn_fused_kernel<128>, q, dM, plen, slot, n_extra, extra, extra_max,
                                (const __nv_bfloat16*)kc, (const __nv_bfloat16*)vc, nh, nkv, (__nv_bfloat16*)o);
     }
     if (e != cudaSuccess) {

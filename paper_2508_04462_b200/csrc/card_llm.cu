@@ -950,7 +950,8 @@ int card_attention_work_floats(int m_max, int nh, int hd, int max_plen) {
     return m_max * nh * (n_splits + 1) * (hd + 2);
 }
 
-int card_attention(const float* q, const int32_t* dM, int m_max, const int32_t* plen, const int32_t* n_extra,
+int card_attention(const float* q, const int32_t* dM, int m_max, const int32_t* plen, const int32_t* slot,
+                   const int32_t* n_extra,
                    const int32_t* extra, int extra_max, const void* kc, const void* vc, int kvdtype, int nh, int nkv,
                    int hd, int max_plen, float* work, void* o, int odtype, void* stream) {
     cudaStream_t s = (cudaStream_t)stream;
@@ -964,7 +965,8 @@ int card_attention(const float* q, const int32_t* dM, int m_max, const int32_t* 
         attr = true;
     }
     if (kvdtype == 0 && odtype == 0 && (hd == 64 || hd == 128) && !getenv("CARD_ATTN_SPLITKV"))
-        return launch_attn_fused(q, dM, m_max, plen, n_extra, extra, extra_max, kc, vc, nh, nkv, hd, max_plen, o, s);
+        if (slot) return launch_attn_fused(q, dM, m_max, plen, slot, n_extra, extra, extra_max, kc, vc, nh, nkv, hd,
+                                           max_plen, o, s);
     dim3 g1(nkv, n_splits);
     const int ew = (m_max * nh + 7) / 8;
     if (kvdtype == 0) {

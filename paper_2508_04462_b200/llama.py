@@ -401,7 +401,7 @@ class DeviceLlama:
             chk(L_.card_rope_kv(ptr(self.qkv), ptr(dM), mm, ptr(rows.pos), ptr(rows.slot), ptr(self.cos),
                                 ptr(self.sin), c.n_heads, c.n_kv_heads, hd, ptr(self.q), ptr(self.k_cache[li]),
                                 ptr(self.v_cache[li]), self.code, s), "rope_kv")
-            chk(L_.card_attention(ptr(self.q), ptr(dM), mm, ptr(rows.plen), ptr(rows.n_extra), ptr(rows.extra),
+            chk(L_.card_attention(ptr(self.q), ptr(dM), mm, ptr(rows.plen), ptr(rows.slot), ptr(rows.n_extra), ptr(rows.extra),
                                   rows.extra_max, ptr(self.k_cache[li]), ptr(self.v_cache[li]), self.code,
                                   c.n_heads, c.n_kv_heads, hd, self.prefix_slots, ptr(self.work), ptr(self.o),
                                   self.code, s), "attention")
@@ -426,7 +426,7 @@ class DeviceLlama:
                           ptr(self.ssq), self.mpad, s), "embed")
         for li, P in enumerate(plan["layers"]):
             P["qkv"].run(dM)
-            chk(L_.card_attention(ptr(self.q), ptr(dM), mm, ptr(rows.plen), ptr(rows.n_extra), ptr(rows.extra),
+            chk(L_.card_attention(ptr(self.q), ptr(dM), mm, ptr(rows.plen), ptr(rows.slot), ptr(rows.n_extra), ptr(rows.extra),
                                   rows.extra_max, ptr(self.k_cache[li]), ptr(self.v_cache[li]), self.code,
                                   c.n_heads, c.n_kv_heads, c.head_dim, self.prefix_slots, ptr(self.work), ptr(self.o),
                                   self.code, s), "attention")

@@ -28,7 +28,7 @@ L = lib()
 from paper_2508_04462_b200._device import ptr, stream_ptr
 c = cfg
 def run():
-    L.card_attention(ptr(rt.q), ptr(rows.M), m, ptr(rows.plen), ptr(rows.n_extra), ptr(rows.extra), rows.extra_max,
+    L.card_attention(ptr(rt.q), ptr(rows.M), m, ptr(rows.plen), ptr(rows.slot), ptr(rows.n_extra), ptr(rows.extra), rows.extra_max,
                      ptr(rt.k_cache[0]), ptr(rt.v_cache[0]), 0, c.n_heads, c.n_kv_heads, c.head_dim, rt.prefix_slots,
                      ptr(rt.work), ptr(rt.o), 0, stream_ptr())
 run(); torch.cuda.synchronize()

@@ -63,7 +63,7 @@ def bench_model(name, preset, m_rows, ctx_len):
     print(f"  all GEMMs: {total_t:.3f} ms  {total_b/total_t/1e6:.0f} GB/s")
     L = _lib.lib()
     c = cfg
-    t_att = timeit(lambda: L.card_attention(ptr(rt.q), ptr(dM), rt.mpad, ptr(rows.plen), ptr(rows.n_extra),
+    t_att = timeit(lambda: L.card_attention(ptr(rt.q), ptr(dM), rt.mpad, ptr(rows.plen), ptr(rows.slot), ptr(rows.n_extra),
                                              ptr(rows.extra), rows.extra_max, ptr(rt.k_cache[0]), ptr(rt.v_cache[0]),
                                              0, c.n_heads, c.n_kv_heads, c.head_dim, rt.prefix_slots, ptr(rt.work),
                                              ptr(rt.o), 0, stream_ptr()))
