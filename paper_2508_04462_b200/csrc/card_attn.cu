@@ -34,9 +34,7 @@ namespace card {
 namespace {
 
 constexpr int kCh = 64;      // keys per chunk
-constexpr int kQT = 64;      // query-heads per CTA (4 warps x 16)
-constexpr int kThreads = 128;
-constexpr int kMaxTileRows = 72;   // rows per tile of 64 query-heads (GQA group >= 1)
+constexpr int kMaxTileRows = 136;  // rows per tile of <= 128 query-heads (GQA group >= 1)
 constexpr int kMaxExtra = 1024;    // gathered extra slots per tile
 
 __device__ __forceinline__ uint32_t s_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
@@ -93,8 +91,10 @@ __device__ __forceinline__ void at_stamp(int k) {
 }  // namespace
 
 // smem: 2 x (K[kCh][HD+8] bf16 | V[kCh][HD+8] bf16) | recv[S][kQT/S][HD+2] f32
-template <int HD>
-__global__ void __launch_bounds__(kThreads) attn_fused_kernel(const float* __restrict__ q, const int32_t* dM,
+// QT query-heads per CTA: 64 (4 warps) for the verify, 128 (8 warps) for the
+// wide draft tree (more queries per staged K/V chunk, half the tiles)
+template <int HD, int QT>
+__global__ void __launch_bounds__(QT * 2) attn_fused_kernel(const float* __restrict__ q, const int32_t* dM,
                                                              const int32_t* __restrict__ plen,
                                                              const int32_t* __restrict__ slot,
                                                              const int32_t* __restrict__ n_extra,
@@ -102,6 +102,7 @@ __global__ void __launch_bounds__(kThreads) attn_fused_kernel(const float* __res
                                                              const __nv_bfloat16* __restrict__ kc,
                                                              const __nv_bfloat16* __restrict__ vc, int nh, int nkv,
                                                              __nv_bfloat16* __restrict__ o_out) {
+    constexpr int kThr = QT * 2;
     constexpr int LD = HD + 8;   // padded bf16 row: 16-byte aligned, conflict-free 32-bit fragment loads
     constexpr int PW = HD + 2;   // partial record: m, l, o[HD]
     extern __shared__ __align__(16) uint8_t smem[];
@@ -119,9 +120,9 @@ __global__ void __launch_bounds__(kThreads) attn_fused_kernel(const float* __res
     const int M = *dM;
     const int G = nh / nkv;
     const int nq = M * G;
-    const int q0 = qt * kQT;
+    const int q0 = qt * QT;
     if (q0 >= nq) return;   // the whole cluster shares qt: consistent early exit
-    const int QO = kQT / S;   // query-heads owned per rank in the combine
+    const int QO = QT / S;   // query-heads owned per rank in the combine
     const int warp = warp_id(), lane = lane_id();
     const int gq = lane >> 2, tq = lane & 3;
 
@@ -129,7 +130,7 @@ __global__ void __launch_bounds__(kThreads) attn_fused_kernel(const float* __res
     auto stage_rows = [&](int c, int b, auto slot_of) {
         const int ks0 = c * kCh;
         const uint32_t kb = ks_base + (uint32_t)(b * kCh * LD * 2), vb = vs_base + (uint32_t)(b * kCh * LD * 2);
-        for (int idx = threadIdx.x; idx < kCh * HD / 8; idx += kThreads) {
+        for (int idx = threadIdx.x; idx < kCh * HD / 8; idx += kThr) {
             const int j = idx / (HD / 8), d8 = (idx % (HD / 8)) * 8;
             const int64_t src = (slot_of(ks0 + j) * nkv + g) * HD + d8;
             cp_async16(kb + (uint32_t)((j * LD + d8) * 2), kc + src);
@@ -143,14 +144,14 @@ __global__ void __launch_bounds__(kThreads) attn_fused_kernel(const float* __res
     __shared__ int s_kmax, s_nx;
     __shared__ int xoff[kMaxTileRows], xne[kMaxTileRows];
     __shared__ int xs[kMaxExtra];
-    const int r0 = q0 / G, r1 = min(M - 1, (q0 + kQT - 1) / G);
+    const int r0 = q0 / G, r1 = min(M - 1, (q0 + QT - 1) / G);
     const int nrows = r1 - r0 + 1;   // <= kMaxTileRows
     // one thread per tile row loads (plen, n_extra); warp 0 scans the extra
     // counts (a serial single-thread loop of dependent loads cost ~10 us)
     if (threadIdx.x == 0) s_kmax = 0;
-    for (int i = threadIdx.x; i < nrows; i += kThreads) xne[i] = max(0, min(n_extra[r0 + i], extra_max));
+    for (int i = threadIdx.x; i < nrows; i += kThr) xne[i] = max(0, min(n_extra[r0 + i], extra_max));
     __syncthreads();
-    for (int i = threadIdx.x; i < nrows; i += kThreads) atomicMax(&s_kmax, plen[r0 + i]);
+    for (int i = threadIdx.x; i < nrows; i += kThr) atomicMax(&s_kmax, plen[r0 + i]);
     if (warp_id() == 0) {
         int carry = 0;
         for (int b0 = 0; b0 < nrows; b0 += 32) {
@@ -172,7 +173,7 @@ __global__ void __launch_bounds__(kThreads) attn_fused_kernel(const float* __res
     }
     __syncthreads();
     for (int i = 0; i <= r1 - r0; ++i)
-        for (int j = threadIdx.x; j < xne[i]; j += kThreads) xs[xoff[i] + j] = extra[(int64_t)(r0 + i) * extra_max + j];
+        for (int j = threadIdx.x; j < xne[i]; j += kThr) xs[xoff[i] + j] = extra[(int64_t)(r0 + i) * extra_max + j];
     const int n_ch = (s_kmax + kCh - 1) / kCh;
     const int n_xch = (s_nx + kCh - 1) / kCh;
     const int n_all = n_ch + n_xch;
@@ -359,7 +360,7 @@ __global__ void __launch_bounds__(kThreads) attn_fused_kernel(const float* __res
     // owner merge: query-heads [rank*QO, rank*QO + QO), S partials in rank
     // order.  Per query-head weights w_s / L first (one thread each), then
     // every output element is S independent loads.
-    __shared__ float s_w[kQT][8];
+    __shared__ float s_w[QT][8];
     if (threadIdx.x < QO) {
         const int ql = threadIdx.x;
         float Mx = -INFINITY;
@@ -375,7 +376,7 @@ __global__ void __launch_bounds__(kThreads) attn_fused_kernel(const float* __res
         for (int s = 0; s < S; ++s) s_w[ql][s] = w[s] * invL;
     }
     __syncthreads();
-    for (int e = threadIdx.x; e < QO * HD; e += kThreads) {
+    for (int e = threadIdx.x; e < QO * HD; e += kThr) {
         const int ql = e / HD, d = e - ql * HD;
         const int qi = q0 + rank * QO + ql;
         if (qi >= nq) break;
@@ -391,21 +392,35 @@ int attn_set_trace(unsigned long long* buf) {
     return cudaMemcpyToSymbol(g_attn_trace, &buf, sizeof(buf)) == cudaSuccess ? CARD_OK : CARD_E_CUDA;
 }
 
-int attn_fused_smem(int hd, int S) { return 4 * kCh * (hd + 8) * 2 + S * (kQT / S) * (hd + 2) * 4; }
+int attn_fused_smem(int hd, int S, int qt) { return 4 * kCh * (hd + 8) * 2 + S * (qt / S) * (hd + 2) * 4; }
+
+template <int HD, int QT>
+static cudaError_t launch_qt(cudaLaunchConfig_t& cfg, const float* q, const int32_t* dM, const int32_t* plen,
+                             const int32_t* slot, const int32_t* n_extra, const int32_t* extra, int extra_max,
+                             const void* kc, const void* vc, int nh, int nkv, void* o) {
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(attn_fused_kernel<HD, QT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        attr = true;
+    }
+    return cudaLaunchKernelEx(&cfg, attn_fused_kernel<HD, QT>, q, dM, plen, slot, n_extra, extra, extra_max,
+                              (const __nv_bfloat16*)kc, (const __nv_bfloat16*)vc, nh, nkv, (__nv_bfloat16*)o);
+}
 
 int launch_attn_fused(const float* q, const int32_t* dM, int m_max, const int32_t* plen, const int32_t* slot,
-                      const int32_t* n_extra,
-                      const int32_t* extra, int extra_max, const void* kc, const void* vc, int nh, int nkv, int hd,
-                      int max_plen, void* o, cudaStream_t s) {
+                      const int32_t* n_extra, const int32_t* extra, int extra_max, const void* kc, const void* vc,
+                      int nh, int nkv, int hd, int max_plen, void* o, cudaStream_t s) {
     const int G = nh / nkv;
-    const int n_qt = (m_max * G + kQT - 1) / kQT;
     const int n_ch = (max_plen + kCh - 1) / kCh;
-    int S = n_qt * nkv <= 37 ? 8 : 4;
+    // wide (draft tree) forwards: 128 query-heads per CTA; narrow: 64
+    const int QT = (m_max * G >= 512) ? 128 : 64;
+    const int n_qt = (m_max * G + QT - 1) / QT;
+    int S = n_qt * nkv <= 37 ? 8 : (QT == 128 ? 8 : 4);
     while (S > 1 && S > n_ch) S >>= 1;
-    const int smem = attn_fused_smem(hd, S);
+    const int smem = attn_fused_smem(hd, S, QT);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(S, n_qt, nkv);
-    cfg.blockDim = dim3(kThreads);
+    cfg.blockDim = dim3(QT * 2);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute attr[2];
@@ -418,23 +433,12 @@ int launch_attn_fused(const float* q, const int32_t* dM, int m_max, const int32_
     cfg.attrs = attr;
     cfg.numAttrs = 2;
     cudaError_t e;
-    if (hd == 64) {
-        static bool a64 = false;
-        if (!a64) {
-            cudaFuncSetAttribute(attn_fused_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-            a64 = true;
-        }
-        e = cudaLaunchKernelEx(&cfg, attn_fused_kernel<64>, q, dM, plen, slot, n_extra, extra, extra_max,
-                               (const __nv_bfloat16*)kc, (const __nv_bfloat16*)vc, nh, nkv, (__nv_bfloat16*)o);
-    } else {
-        static bool a128 = false;
-        if (!a128) {
-            cudaFuncSetAttribute(attn_fused_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-            a128 = true;
-        }
-        e = cudaLaunchKernelEx(&cfg, attn_fused_kernel<128>, q, dM, plen, slot, n_extra, extra, extra_max,
-                               (const __nv_bfloat16*)kc, (const __nv_bfloat16*)vc, nh, nkv, (__nv_bfloat16*)o);
-    }
+    if (hd == 64)
+        e = QT == 128 ? launch_qt<64, 128>(cfg, q, dM, plen, slot, n_extra, extra, extra_max, kc, vc, nh, nkv, o)
+                      : launch_qt<64, 64>(cfg, q, dM, plen, slot, n_extra, extra, extra_max, kc, vc, nh, nkv, o);
+    else
+        e = QT == 128 ? launch_qt<128, 128>(cfg, q, dM, plen, slot, n_extra, extra, extra_max, kc, vc, nh, nkv, o)
+                      : launch_qt<128, 64>(cfg, q, dM, plen, slot, n_extra, extra, extra_max, kc, vc, nh, nkv, o);
     if (e != cudaSuccess) {
         set_cuda_error(e);
         return CARD_E_CUDA;
