@@ -87,8 +87,11 @@ PRESETS = {
     # BASELINE.json configs[1]
     "llama-3.2-1b": LlamaConfig(128256, 2048, 16, 32, 8, 64, 8192, 500000.0, 1e-5, True, False, _LLAMA3_SCALING_1B),
     "llama-3.1-8b": LlamaConfig(128256, 4096, 32, 32, 8, 128, 14336, 500000.0, 1e-5, False, False, _LLAMA3_SCALING_8B),
-    # BASELINE.json configs[2]
-    "qwen2.5-0.5b": LlamaConfig(151936, 896, 24, 14, 2, 64, 4864, 1000000.0, 1e-6, True, True, None),
+    # BASELINE.json configs[2].  The two checkpoints pad their embedding tables
+    # differently (151936 vs 152064 rows) over one 151665-token tokenizer; the
+    # engine needs one vocabulary (engine.py:127-136), so the draft is padded
+    # to the target's 152064 rows (padding rows are never real tokens).
+    "qwen2.5-0.5b": LlamaConfig(152064, 896, 24, 14, 2, 64, 4864, 1000000.0, 1e-6, True, True, None),
     "qwen2.5-7b": LlamaConfig(152064, 3584, 28, 28, 4, 128, 18944, 1000000.0, 1e-6, False, True, None),
     # BASELINE.json configs[0]: the CPU-runnable tiny pair (FFN rounded to 704)
     "tiny-target": LlamaConfig(64, 256, 4, 4, 2, 64, 704, 10000.0, 1e-5, False, False, None),
