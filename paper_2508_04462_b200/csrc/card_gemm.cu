@@ -194,7 +194,7 @@ __device__ __forceinline__ void sts_f32(uint32_t addr, float v) {
 template <int EPI>
 __device__ __forceinline__ void epi_chunk(const TcArgs& a, int tile, int n_glob, int n_local, int m0, int mc,
                                           float* v, uint32_t xch, const float* invs, const int* tpos,
-                                          const int* tslot) {
+                                          const int* tslot, float* xch_ptr) {
     const float b = a.bias ? a.bias[n_glob] : 0.f;
     if (a.ssq_in)
 #pragma unroll
@@ -248,7 +248,10 @@ __device__ __forceinline__ void epi_chunk(const TcArgs& a, int tile, int n_glob,
         // rows [0,64) of a tile are gates, [64,128) the matching ups.  Gate
         // thread f and up thread 64+f swap halves of the chunk through xch
         // ([16][128] fp32) so all 128 threads share the SwiGLU: the gate thread
-        // finishes tokens 0..7, the up thread tokens 8..15 of feature f.
+        // finishes tokens 0..7, the up thread tokens 8..15 of feature f.  The
+        // bf16 results are staged as a [16][64] tile and written as 16-byte
+        // vectors (one 128-byte row per token): scattered 2-byte stores made
+        // this epilogue 4x slower.
         const int f = n_local & 63;
         const bool up = n_local >= 64;
 #pragma unroll
@@ -261,16 +264,24 @@ __device__ __forceinline__ void epi_chunk(const TcArgs& a, int tile, int n_glob,
 #pragma unroll
         for (int jj = 0; jj < 8; ++jj) o[jj] = lds_f32(other + (uint32_t)((jb + jj) * 128 * 4));
         named_bar(1, kEpiThreads);
-        const int fo = tile * 64 + f;
+        // stage bf16 outputs [16 tokens][64 features] in the (now free) front of xch
+        __nv_bfloat16* stg = reinterpret_cast<__nv_bfloat16*>(xch_ptr);
 #pragma unroll
         for (int jj = 0; jj < 8; ++jj) {
             const int j = jb + jj;
-            if (j < mc) {
-                const float g = up ? o[jj] : v[j] + b;
-                const float u = up ? v[j] + b : o[jj];
-                a.out_bf16[(int64_t)(m0 + j) * a.ldo + fo] = __float2bfloat16(silu(g) * u);
+            const float g = up ? o[jj] : v[j] + b;
+            const float u = up ? v[j] + b : o[jj];
+            stg[j * 64 + f] = __float2bfloat16(silu(g) * u);
+        }
+        named_bar(1, kEpiThreads);
+        {
+            const int row = n_local >> 3, piece = n_local & 7;   // 16 rows x 8 pieces of 16 B
+            if (row < mc) {
+                const uint4 val = *reinterpret_cast<const uint4*>(stg + row * 64 + piece * 8);
+                *reinterpret_cast<uint4*>(a.out_bf16 + (int64_t)(m0 + row) * a.ldo + tile * 64 + piece * 8) = val;
             }
         }
+        named_bar(1, kEpiThreads);
         return;
     }
     if (EPI == EPI_RESID_F32) {
@@ -527,7 +538,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
                 float v[16];
                 tmem_ld16(trow + (uint32_t)m0, v);
                 const int mc = (M - m0) < 16 ? (M - m0) : 16;
-                epi_chunk<EPI>(a, tile, n_glob, n_local, m0, mc, v, smem_u32(xch), invs, tpos, tslot);
+                epi_chunk<EPI>(a, tile, n_glob, n_local, m0, mc, v, smem_u32(xch), invs, tpos, tslot, xch);
             }
             tc_fence_before();
             __syncwarp();
