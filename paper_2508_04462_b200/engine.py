@@ -633,7 +633,12 @@ class _ConcurrentDriver:
         from . import _lib
 
         self.run = run
-        self.D, self.T = torch.cuda.Stream(), torch.cuda.Stream()
+        # the draft stream gets the higher priority: with the target verifying
+        # concurrently, accepted tokens per second track draft layers per
+        # second (each layer adds about one token of depth the next verify can
+        # accept), so the draft's kernels are scheduled first
+        self.D = torch.cuda.Stream(priority=-8)   # clamped to the highest priority
+        self.T = torch.cuda.Stream(priority=0)
         cap = torch.cuda.Stream()
         cap.wait_stream(torch.cuda.current_stream())
         self.g_d, self.g_q, self.g_t, self.g_c = (torch.cuda.CUDAGraph() for _ in range(4))
