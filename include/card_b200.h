@@ -267,6 +267,11 @@ int card_cycle_end(card_engine_state* E, card_cache* h, void* stream);
  * tokens, correction, done) into the draft-side state before the correction
  * is applied on the draft stream (engine.py:320-389 lock + epoch protocol). */
 int card_engine_handoff(const card_engine_state* target_state, card_engine_state* draft_state, void* stream);
+/* Two-GPU draft||target placement: enable P2P access both ways between the
+ * draft and the target device (the kernels of each side read the other's
+ * query result / commit outcome / committed tokens over NVLink).  Returns
+ * CARD_E_CONFIG when the devices cannot access each other. */
+int card_enable_peer_access(int dev_a, int dev_b);
 
 #ifdef __cplusplus
 }

@@ -88,6 +88,7 @@ SIGNATURES = {
     "card_kv_compact": (c_int, [_P, _P, _P, _P, c_int, c_int, c_int, c_int, _P, c_int, _P]),
     "card_cycle_end": (c_int, [_P, _P, _P]),
     "card_engine_handoff": (c_int, [_P, _P, _P]),
+    "card_enable_peer_access": (c_int, [c_int, c_int]),
 }
 
 

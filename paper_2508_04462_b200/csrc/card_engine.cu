@@ -632,6 +632,28 @@ int card_kv_compact(card_engine_state* E, card_cache* h, void** k_layers, void**
     return CARD_OK;
 }
 
+int card_enable_peer_access(int dev_a, int dev_b) {
+    if (dev_a == dev_b) return CARD_OK;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    int ok_ab = 0, ok_ba = 0;
+    cudaDeviceCanAccessPeer(&ok_ab, dev_a, dev_b);
+    cudaDeviceCanAccessPeer(&ok_ba, dev_b, dev_a);
+    if (!ok_ab || !ok_ba) return CARD_E_CONFIG;
+    for (int k = 0; k < 2; ++k) {
+        cudaSetDevice(k == 0 ? dev_a : dev_b);
+        cudaError_t e = cudaDeviceEnablePeerAccess(k == 0 ? dev_b : dev_a, 0);
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) {
+            set_cuda_error(e);
+            cudaSetDevice(prev);
+            return CARD_E_CUDA;
+        }
+        cudaGetLastError();
+    }
+    cudaSetDevice(prev);
+    return CARD_OK;
+}
+
 int card_engine_handoff(const card_engine_state* target_state, card_engine_state* draft_state, void* stream) {
     handoff_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(target_state, draft_state);
     CARD_LAUNCH_CHECK();

@@ -214,10 +214,13 @@ class _LlamaAdapter:
         self.rows_max = rows_max
         tree_slots = run.cache_capacity if role == "draft" else 0
         budgets = {rows_max, PREFILL_CHUNK}
-        self.rt = model.runtime(run.max_ctx, tree_slots, budgets)
+        dev = run.dev_d if role == "draft" else run.dev_t
+        with torch.cuda.device(dev):
+            self.rt = model.runtime(run.max_ctx, tree_slots, budgets)
+        if self.rt.dev != dev:
+            raise ConfigError(f"the {role} model lives on {self.rt.dev}, the run places it on {dev}")
         if self.rt.extra_max < run.cfg.max_depth + 1:
             raise ConfigError("max_depth too large for the tree-attention extra-slot budget")
-        dev = run.dev
         V = model.vocab.size
         self.V = V
         self.k = run.cfg.k
@@ -263,7 +266,7 @@ class _LlamaAdapter:
         if not tokens:
             return
         if self.prefill_rows is None:
-            self.prefill_rows = RowBlock(PREFILL_CHUNK, 1, run.dev)
+            self.prefill_rows = RowBlock(PREFILL_CHUNK, 1, self.rt.dev)
         for s in range(0, len(tokens), PREFILL_CHUNK):
             chunk = tokens[s:s + PREFILL_CHUNK]
             self.prefill_rows.set_chain(chunk, s)
@@ -331,11 +334,21 @@ def _order_of(model) -> int:
 class DeviceRun:
     """State of one decode on the device (engine.py:149-272)."""
 
-    def __init__(self, draft, target, prompt, config: EngineConfig, *, trace_alive: bool = True):
+    def __init__(self, draft, target, prompt, config: EngineConfig, *, trace_alive: bool = True,
+                 devices: tuple[int, int] | None = None):
         _check_pair(draft, target)
         self.draft_model, self.target_model = draft, target
         self.cfg = config
         self.dev = require_cuda()
+        # placement (mode="concurrent"): the candidate tree, the draft state and
+        # the draft rows live with the draft model; committed tokens, the target
+        # state and rows with the target.  Kernels of either side read the other
+        # side's small buffers (query result, commit outcome, committed tokens)
+        # directly — over NVLink P2P when the devices differ.
+        dd, td = devices if devices is not None else (self.dev.index, self.dev.index)
+        self.dev_d, self.dev_t = torch.device("cuda", dd), torch.device("cuda", td)
+        if dd != td:
+            enable_peer_access(dd, td)
         self.prompt = _check_prompt(prompt, target.vocab.size)
         self.t_score = config.temperature if config.temperature > 0.0 else 1.0
         self.sampling = config.temperature > 0.0
@@ -348,18 +361,19 @@ class DeviceRun:
             self.cache_capacity = 6 * cfg.K * (cfg.max_depth + 1) + 256
         else:   # the un-steered ablation never compacts (cache.py:415-437)
             self.cache_capacity = cfg.K * (cfg.max_new_tokens + cfg.max_depth + 2) * 2 + 256
-        self.cache = TreeCache(self.prompt[-1], CacheConfig(cfg.K, cfg.k, cfg.max_depth), eos_token=self.eos,
-                               capacity=self.cache_capacity)
+        with torch.cuda.device(self.dev_d):
+            self.cache = TreeCache(self.prompt[-1], CacheConfig(cfg.K, cfg.k, cfg.max_depth), eos_token=self.eos,
+                                   capacity=self.cache_capacity)
         order = max(_order_of(draft), _order_of(target))
         self.d_rows_max = cfg.K + cfg.max_depth + 2
         self.t_rows_max = cfg.query_depth + 1
-        self.drt = _RowsAndTail(self.d_rows_max, cfg.max_depth + 1, order, self.dev)
-        self.trt = _RowsAndTail(self.t_rows_max, 1, order, self.dev)
-        self.committed = torch.zeros(self.max_ctx + 8, dtype=torch.int32, device=self.dev)
+        self.drt = _RowsAndTail(self.d_rows_max, cfg.max_depth + 1, order, self.dev_d)
+        self.trt = _RowsAndTail(self.t_rows_max, 1, order, self.dev_t)
+        self.committed = torch.zeros(self.max_ctx + 8, dtype=torch.int32, device=self.dev_t)
         self.committed[:C0] = torch.tensor(self.prompt, dtype=torch.int32)
         rng = np.random.default_rng(cfg.seed)   # engine.py:162; the only randomness
         n_uni = (cfg.max_new_tokens + 2) * (cfg.query_depth + 2) + 16 if self.sampling else 1
-        self.uni = torch.from_numpy(rng.random(n_uni)).to(self.dev)
+        self.uni = torch.from_numpy(rng.random(n_uni)).to(self.dev_t)
         st = EngineState()
         st.C = C0
         st.Pd = 0
@@ -370,13 +384,15 @@ class DeviceRun:
         st.base_len = C0
         st.anchor_origin = int(not cfg.correction_enabled)
         st.n_uni = n_uni
-        self.E = torch.frombuffer(bytearray(bytes(st)), dtype=torch.int32).to(self.dev)
+        self.E = torch.frombuffer(bytearray(bytes(st)), dtype=torch.int32).to(self.dev_t)
         self.E_ptr = ptr(self.E)
         # draft-side state: the same buffer in the lockstep drivers; a separate
         # copy in mode="concurrent" (the draft stream never reads the target's
         # in-flight commit; card_engine_handoff passes it over after each verify)
         self.concurrent = config.mode == "concurrent"
-        self.Ed = self.E.clone() if self.concurrent else self.E
+        if dd != td and not self.concurrent:
+            raise ConfigError("separate draft/target devices need mode='concurrent'")
+        self.Ed = self.E.to(self.dev_d, copy=True) if self.concurrent else self.E
         self.Ed_ptr = ptr(self.Ed)
         self.q_tok_ptr = ctypes.c_void_p(self.cache._qbufs[1])
         self._host = torch.empty(self.E.numel(), dtype=torch.int32, pin_memory=True)
@@ -408,8 +424,10 @@ class DeviceRun:
         """Prompt KV for both models: target gets prompt[:-1] (its last token is
         the first verify input), the draft likewise (its flat step computes the root)."""
         body = self.prompt[:-1]
-        self.da.prefill(self, body)
-        self.ta.prefill(self, body)
+        with torch.cuda.device(self.dev_d):
+            self.da.prefill(self, body)
+        with torch.cuda.device(self.dev_t):
+            self.ta.prefill(self, body)
         self._set_field("Pd", len(body))
 
     # ---------------------------------------------------------------- sequences
@@ -633,33 +651,41 @@ class _ConcurrentDriver:
         from . import _lib
 
         self.run = run
+        dd, td = run.dev_d, run.dev_t
         # the draft stream gets the higher priority: with the target verifying
         # concurrently, accepted tokens per second track draft layers per
         # second (each layer adds about one token of depth the next verify can
         # accept), so the draft's kernels are scheduled first
-        self.D = torch.cuda.Stream(priority=-8)   # clamped to the highest priority
-        self.T = torch.cuda.Stream(priority=0)
-        cap = torch.cuda.Stream()
-        cap.wait_stream(torch.cuda.current_stream())
+        self.D = torch.cuda.Stream(device=dd, priority=-8)   # clamped to the highest priority
+        self.T = torch.cuda.Stream(device=td, priority=0)
         self.g_d, self.g_q, self.g_t, self.g_c = (torch.cuda.CUDAGraph() for _ in range(4))
-        with torch.cuda.stream(cap):
-            c = [_lib.launch_count[0]]
-            with torch.cuda.graph(self.g_d, stream=cap):
-                run.launch_draft_step()
-                run._host_d.copy_(run.Ed, non_blocking=True)
+        c = [_lib.launch_count[0]]
+
+        def capture(g, dev, fn):
+            with torch.cuda.device(dev):
+                cap = torch.cuda.Stream(device=dev)
+                cap.wait_stream(torch.cuda.current_stream(dev))
+                with torch.cuda.stream(cap), torch.cuda.graph(g, stream=cap):
+                    fn()
+                torch.cuda.current_stream(dev).wait_stream(cap)
             c.append(_lib.launch_count[0])
-            with torch.cuda.graph(self.g_q, stream=cap):
-                raise_for_status(lib().card_cache_query(run.cache.handle, run.cfg.query_depth, stream_ptr()), "query")
-            c.append(_lib.launch_count[0])
-            with torch.cuda.graph(self.g_t, stream=cap):
-                run.launch_target_step(with_correct=False, readback=True, with_query=False)
-            c.append(_lib.launch_count[0])
-            with torch.cuda.graph(self.g_c, stream=cap):
-                raise_for_status(lib().card_engine_handoff(run.E_ptr, run.Ed_ptr, stream_ptr()), "handoff")
-                run.launch_correct()
-                raise_for_status(lib().card_cache_query(run.cache.handle, run.cfg.query_depth, stream_ptr()), "query")
-            c.append(_lib.launch_count[0])
-        torch.cuda.current_stream().wait_stream(cap)
+
+        def draft_step():
+            run.launch_draft_step()
+            run._host_d.copy_(run.Ed, non_blocking=True)
+
+        def query():
+            raise_for_status(lib().card_cache_query(run.cache.handle, run.cfg.query_depth, stream_ptr()), "query")
+
+        def correct_query():
+            raise_for_status(lib().card_engine_handoff(run.E_ptr, run.Ed_ptr, stream_ptr()), "handoff")
+            run.launch_correct()
+            query()
+
+        capture(self.g_d, dd, draft_step)
+        capture(self.g_q, dd, query)
+        capture(self.g_t, td, lambda: run.launch_target_step(with_correct=False, readback=True, with_query=False))
+        capture(self.g_c, dd, correct_query)
         self.per_graph = [c[i + 1] - c[i] for i in range(4)]
         self.replays = [0, 0, 0, 0]
 
@@ -684,9 +710,9 @@ class _ConcurrentDriver:
     def run_loop(self):
         run, cfg = self.run, self.run.cfg
         t0 = time.perf_counter()
-        torch.cuda.current_stream().synchronize()
-        self.D.wait_stream(torch.cuda.current_stream())
-        self.T.wait_stream(torch.cuda.current_stream())
+        for dev, st in ((run.dev_d, self.D), (run.dev_t, self.T)):
+            torch.cuda.current_stream(dev).synchronize()
+            st.wait_stream(torch.cuda.current_stream(dev))
         # warm-up: query_depth expansions before the first target step (engine.py:377)
         paused = False
         for _ in range(min(cfg.query_depth, cfg.max_depth)):
@@ -735,7 +761,8 @@ class _ConcurrentDriver:
             self.replays[3] += 1
             paused = False
             run._emit(time.perf_counter() - t0, hit, 0, 0, 0, "correct")
-        torch.cuda.synchronize()
+        for dev in {run.dev_d, run.dev_t}:
+            torch.cuda.synchronize(dev)
 
     def launches(self) -> int:
         return sum(r * n for r, n in zip(self.replays, self.per_graph))
@@ -748,8 +775,14 @@ def _validate_run_config(draft, target, config):
         raise ConfigError("query_depth too large")
 
 
+def enable_peer_access(a: int, b: int):
+    """P2P loads/stores between two devices in both directions (NVLink)."""
+    raise_for_status(lib().card_enable_peer_access(a, b), "card_enable_peer_access")
+
+
 def run_speculative(draft, target, prompt: Sequence[TokenId], config: EngineConfig, *,
-                    use_graphs: bool | None = None, trace_alive: bool | None = None) -> RunResult:
+                    use_graphs: bool | None = None, trace_alive: bool | None = None,
+                    devices: tuple[int, int] | None = None) -> RunResult:
     """The generate() entry point (engine.py:275-287), on the device.
 
     ``use_graphs`` (default: True for transformer pairs with correction on)
@@ -766,16 +799,20 @@ def run_speculative(draft, target, prompt: Sequence[TokenId], config: EngineConf
     if trace_alive is None:
         trace_alive = not use_graphs
     concurrent = config.mode == "concurrent" and config.correction_enabled and use_graphs
+    if devices is not None and not concurrent:
+        raise ConfigError("devices=(draft, target) placement needs mode='concurrent' with a transformer pair")
     if concurrent:
-        run = DeviceRun(draft, target, prompt, config, trace_alive=False)
+        run = DeviceRun(draft, target, prompt, config, trace_alive=False, devices=devices)
         t0 = time.perf_counter()
         run.prefill()
         drv = _ConcurrentDriver(run)
-        torch.cuda.synchronize()
-        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        ev0.record()
-        drv.run_loop()
-        ev1.record()
+        for dev in {run.dev_d, run.dev_t}:
+            torch.cuda.synchronize(dev)
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev0.record(torch.cuda.current_stream(run.dev_t))
+        drv.run_loop()   # ends with both devices synchronised
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev1.record(torch.cuda.current_stream(run.dev_t))
         ev1.synchronize()
         run.timing["decode_ms"] = ev0.elapsed_time(ev1)
         run.timing["gpu_launches"] = drv.launches()
@@ -823,6 +860,7 @@ class VanillaRun:
         # a never-expanded cache: every query misses, so each step is a miss step
         self.cache = TreeCache(self.prompt[-1], CacheConfig(1, 1, 1), eos_token=target.eos_token, capacity=64)
         order = _order_of(target)
+        self.dev_d = self.dev_t = self.dev
         self.trt = _RowsAndTail(1, 1, order, self.dev)
         self.committed = torch.zeros(self.max_ctx + 8, dtype=torch.int32, device=self.dev)
         self.committed[:C0] = torch.tensor(self.prompt, dtype=torch.int32)

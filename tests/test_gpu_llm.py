@@ -190,3 +190,31 @@ def test_concurrent_mode_is_lossless(card, dtype):
     assert res.wall["target_steps"] < len(res.output)   # more than one token per verify on average
     events = {e.event for e in res.trace}
     assert {"verify", "correct"} <= events
+
+
+@pytest.mark.parametrize("devices", [(0, 0), (0, 1)])
+def test_concurrent_device_placement(card, devices):
+    """Draft||target placement of mode="concurrent": the tree and draft state
+    on the draft device, committed tokens and target state on the target
+    device, each side reading the other's small buffers directly (P2P over
+    NVLink on two GPUs; (0, 0) exercises the same code on one)."""
+    import torch
+
+    from paper_2508_04462_b200.llama import PRESETS, init_weights
+    from paper_2508_04462_b200.lm import LogitBias
+
+    if max(devices) >= torch.cuda.device_count():
+        pytest.skip("needs two GPUs")
+    bias = LogitBias(seed=11, order=2, sharpness=4000.0)
+    ct, cd = PRESETS["small-target"], PRESETS["small-draft"]
+    with torch.cuda.device(devices[1]):
+        t = card.LlamaModel(ct, dtype="bf16", weights=init_weights(ct, 2), spec=card.ModelSpec(8.0, 7.0), bias=bias)
+    with torch.cuda.device(devices[0]):
+        d = card.LlamaModel(cd, dtype="bf16", weights=init_weights(cd, 1), spec=card.ModelSpec(1.0, 1.0), bias=bias)
+    prompt = [int(x) for x in np.random.default_rng(8).integers(0, t.vocab.size, 40)]
+    cfg = card.EngineConfig(K=16, k=3, ratio=5, max_new_tokens=128, mode="concurrent")
+    with torch.cuda.device(devices[1]):
+        van = card.run_vanilla(t, prompt, cfg)
+    res = card.run_speculative(d, t, prompt, cfg, use_graphs=True, devices=devices)
+    assert res.output == van.output
+    assert res.wall["target_steps"] < len(res.output)
