@@ -202,8 +202,16 @@ def run_reference_arm(args):
 
 # ---------------------------------------------------------------- GPU arm
 def measure_roofline(target, rows_max, ctx_len, peak):
-    """Per-launch CUDA-event timing of every weight-streaming GEMM of one
-    target verify forward (M = rows_max rows), on the launching stream."""
+    """Roofline of the dominant kernel, tc_gemm_kernel, as it runs in a target
+    verify step (M = rows_max rows): the 4*L+1 weight-streaming GEMMs of one
+    verify forward, in forward order with their PDL chaining, captured as a
+    CUDA graph and replayed with CUDA events on the launching stream.
+    avg launch duration = replay time / launches; achieved = algorithmic
+    (weight) bytes per launch / avg launch duration.  The weights (15 GB)
+    exceed L2 (126 MB), so every replay streams them from HBM.  Also reports
+    the whole verify forward (attention and all) streamed at the same bytes
+    (forward_frac), and the isolated per-launch figure (isolated_frac: each
+    GEMM timed alone after an L2 flush, no overlap with its neighbours)."""
     import numpy as np
     import torch
 
@@ -217,32 +225,61 @@ def measure_roofline(target, rows_max, ctx_len, peak):
     if rt.fused:
         rt._bind_rows(plan, rows)   # RoPE / KV-slot / lm_head row pointers of the fused epilogues
     lins = [L[k] for L in plan["layers"] for k in ("qkv", "o", "gu", "d")] + [plan["lm_head"]]
+    nbytes = sum(lin.nbytes for lin in lins)
+
+    def run_gemms():
+        for lin in lins:
+            lin.run(rows.M if lin is not plan["lm_head"] else rows.n_out)
+
+    def graph_of(fn):
+        g = torch.cuda.CUDAGraph()
+        st = torch.cuda.Stream()
+        st.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(st), torch.cuda.graph(g, stream=st):
+            fn()
+        torch.cuda.current_stream().wait_stream(st)
+        return g
+
+    def replay_ms(g, reps=5):
+        stream = torch.cuda.current_stream()
+        g.replay()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(reps):
+            g.replay()
+        b.record(stream)
+        b.synchronize()
+        return a.elapsed_time(b) / reps
+
+    run_gemms()
+    rt.forward(rows, rows_max)
+    torch.cuda.synchronize()
+    t_gemm = replay_ms(graph_of(run_gemms))
+    t_fwd = replay_ms(graph_of(lambda: rt.forward(rows, rows_max)))
+    # isolated: each launch alone after an L2 flush (no PDL overlap)
     stream = torch.cuda.current_stream()
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
-    tot_b = tot_t = 0.0
-    for rep in range(3):
-        evs = []
-        flush.zero_()
-        for lin in lins:
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            lin.run(rows.M if lin is not plan["lm_head"] else rows.n_out)
-            b.record(stream)
-            evs.append((lin, a, b))
-        torch.cuda.synchronize()
-        if rep == 0:
-            continue   # warm
-        for lin, a, b in evs:
-            tot_b += lin.nbytes
-            tot_t += a.elapsed_time(b) * 1e-3
-    achieved = tot_b / tot_t / 1e9
-    per_launch = tot_b / (2 * len(lins))
+    iso_t = 0.0
+    flush.zero_()
+    evs = []
+    for lin in lins:
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        lin.run(rows.M if lin is not plan["lm_head"] else rows.n_out)
+        b.record(stream)
+        evs.append((a, b))
+    torch.cuda.synchronize()
+    iso_t = sum(a.elapsed_time(b) for a, b in evs)
     del flush
+    achieved = nbytes / (t_gemm * 1e-3) / 1e9
     return {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
             "frac": round(achieved / peak, 4), "traffic": None,
-            "kernel": "tc_gemm_kernel (tcgen05.mma + cp.async.bulk weight stream)",
-            "algorithmic_bytes_per_launch": round(per_launch), "launches_per_forward": len(lins),
-            "avg_launch_us": round(tot_t / (2 * len(lins)) * 1e6, 2)}
+            "kernel": "tc_gemm_kernel (tcgen05.mma + cp.async.bulk weight stream), target verify step",
+            "algorithmic_bytes_per_launch": round(nbytes / len(lins)), "launches_per_forward": len(lins),
+            "avg_launch_us": round(t_gemm * 1e3 / len(lins), 2),
+            "forward_ms": round(t_fwd, 3), "forward_frac": round(nbytes / (t_fwd * 1e-3) / 1e9 / peak, 4),
+            "isolated_frac": round(nbytes / (iso_t * 1e-3) / 1e9 / peak, 4)}
 
 
 def main():
@@ -324,6 +361,8 @@ def main():
         ar_ms += v.wall["decode_ms"]
         if i < len(outs) and args.temperature == 0.0:
             lossless &= (v.output == outs[i])
+    if args.temperature > 0.0:
+        lossless = None   # sampled tokens differ by design; losslessness is distributional (tests)
     ar_value = ar_tok / (ar_ms / 1000.0)
     roof = measure_roofline(target, args.ratio + 1, args.prompt_len + args.new_tokens // 2, peak)
     tr = traffic_from_profiles()

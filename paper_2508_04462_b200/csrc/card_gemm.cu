@@ -952,12 +952,18 @@ static cudaError_t launch_tc(const card_linear* h, const TcArgs& a, cudaStream_t
 // is resident at once (one wave) and the [128][Mpad+4] fp32 reduction
 // buffer fits in the freed pipeline stages.
 template <int EPI>
-static int choose_cluster(int n_tiles, int kb_total, int Mpad, int slots, int smem, int stage_smem) {
+static int choose_cluster(int n_tiles, int kb_total, int Mpad, int slots, int smem, int stage_smem, int ctas_per_sm) {
     if (getenv("CARD_NO_CLUSTER") || 2 * n_tiles > slots) return 1;
     int S = 8;
     while (S > 1 && (n_tiles * S > slots || S > kb_total || (size_t)kTileN * (Mpad + 4) * 4 > (size_t)stage_smem))
         S >>= 1;
     if (getenv("CARD_SPLITS")) S = atoi(getenv("CARD_SPLITS"));   // tuning knob (must divide 128)
+    if (getenv("CARD_CLUSTER_FORCE")) return S;   // tuning knob: skip the one-wave occupancy check
+    // cudaOccupancyMaxActiveClusters counts one CTA per SM for this kernel even
+    // when two fit (measured: 33 clusters of 4 at 105 KB and at 209 KB); with
+    // two CTAs per SM the slot count above is the better bound (the verify
+    // forward is 5% faster with S = 4 / 8 than with the API's S = 2 / 4)
+    if (ctas_per_sm >= 2) return S;
     while (S > 1) {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(n_tiles * S);
@@ -971,7 +977,11 @@ static int choose_cluster(int n_tiles, int kb_total, int Mpad, int slots, int sm
         cfg.attrs = &attr;
         cfg.numAttrs = 1;
         int nc = 0;
-        if (cudaOccupancyMaxActiveClusters(&nc, tc_gemm_kernel<EPI, true>, &cfg) == cudaSuccess && nc >= n_tiles) break;
+        const cudaError_t oe = cudaOccupancyMaxActiveClusters(&nc, tc_gemm_kernel<EPI, true>, &cfg);
+        if (getenv("CARD_CLUSTER_DEBUG"))
+            fprintf(stderr, "choose_cluster: tiles=%d kb=%d Mpad=%d S=%d smem=%d -> max active clusters %d (%s)\n", n_tiles,
+                    kb_total, Mpad, S, smem, nc, cudaGetErrorString(oe));
+        if (oe == cudaSuccess && nc >= n_tiles) break;
         cudaGetLastError();
         S >>= 1;
     }
@@ -1087,11 +1097,11 @@ int card_linear_create(const void* W, int N, int K, int wdtype, const void* X, i
     const int stage_smem = stages * stage_bytes;
     int S = 1;
     switch (epi) {
-        case EPI_STORE_F32: S = choose_cluster<EPI_STORE_F32>(a.n_tiles, a.kb_total, Mpad, slots, h->smem, stage_smem); break;
-        case EPI_RESID_F32: S = choose_cluster<EPI_RESID_F32>(a.n_tiles, a.kb_total, Mpad, slots, h->smem, stage_smem); break;
-        case EPI_STORE_BF16: S = choose_cluster<EPI_STORE_BF16>(a.n_tiles, a.kb_total, Mpad, slots, h->smem, stage_smem); break;
-        case EPI_SWIGLU_BF16: S = choose_cluster<EPI_SWIGLU_BF16>(a.n_tiles, a.kb_total, Mpad, slots, h->smem, stage_smem); break;
-        case EPI_QKV_ROPE: S = choose_cluster<EPI_QKV_ROPE>(a.n_tiles, a.kb_total, Mpad, slots, h->smem, stage_smem); break;
+        case EPI_STORE_F32: S = choose_cluster<EPI_STORE_F32>(a.n_tiles, a.kb_total, Mpad, slots, h->smem, stage_smem, ctas_per_sm); break;
+        case EPI_RESID_F32: S = choose_cluster<EPI_RESID_F32>(a.n_tiles, a.kb_total, Mpad, slots, h->smem, stage_smem, ctas_per_sm); break;
+        case EPI_STORE_BF16: S = choose_cluster<EPI_STORE_BF16>(a.n_tiles, a.kb_total, Mpad, slots, h->smem, stage_smem, ctas_per_sm); break;
+        case EPI_SWIGLU_BF16: S = choose_cluster<EPI_SWIGLU_BF16>(a.n_tiles, a.kb_total, Mpad, slots, h->smem, stage_smem, ctas_per_sm); break;
+        case EPI_QKV_ROPE: S = choose_cluster<EPI_QKV_ROPE>(a.n_tiles, a.kb_total, Mpad, slots, h->smem, stage_smem, ctas_per_sm); break;
     }
     if (S > 1 && (kTileN % S != 0 || (size_t)kTileN * (Mpad + 4) * 4 > (size_t)stage_smem)) {
         free(h);
