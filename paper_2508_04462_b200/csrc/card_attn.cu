@@ -418,9 +418,10 @@ int launch_attn_fused(const float* q, const int32_t* dM, int m_max, const int32_
     const int QT = (m_max * G >= 512) ? 128 : 64;
     const int n_qt = (m_max * G + QT - 1) / QT;
     // narrow forwards (verify / AR: one query tile per kv head) spread the
-    // context over 16 ranks (non-portable cluster; measured 2% faster verify
-    // forward than 8), wide ones over 8 or 4
-    int S = n_qt * nkv <= 18 ? 16 : n_qt * nkv <= 37 ? 8 : (QT == 128 ? 8 : 4);
+    // context over 16 ranks (non-portable cluster; 2% faster verify forward
+    // than 8); the wide draft tree forward is fastest with 4 (measured 4 <
+    // 8 < 2 < 16 on the 1B draft at 116 rows)
+    int S = QT == 128 ? 4 : n_qt * nkv <= 18 ? 16 : n_qt * nkv <= 37 ? 8 : 4;
     if (getenv("CARD_ATTN_S")) S = atoi(getenv("CARD_ATTN_S"));   // tuning knob (power of two <= 16)
     while (S > 1 && S > n_ch) S >>= 1;
     const int smem = attn_fused_smem(hd, S, QT);
