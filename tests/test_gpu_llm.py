@@ -218,3 +218,23 @@ def test_concurrent_device_placement(card, devices):
     res = card.run_speculative(d, t, prompt, cfg, use_graphs=True, devices=devices)
     assert res.output == van.output
     assert res.wall["target_steps"] < len(res.output)
+
+
+@pytest.mark.parametrize("mode", ["serial_sim", "concurrent"])
+def test_eos_on_transformer_pair(card, mode):
+    """An EOS-producing pair (lm.py:148-150 absorbing EOS, cache.py EOS parents
+    never extended, engine.py:247-262 clipping): CARD stops exactly where
+    greedy AR stops."""
+    from paper_2508_04462_b200.lm import LogitBias
+
+    bias = LogitBias(seed=11, order=2, sharpness=4000.0)
+    d, t, *_ = _tiny_pair(card, "bf16", "small-target", "small-draft", bias=bias)
+    prompt = [int(x) for x in np.random.default_rng(12).integers(0, t.vocab.size, 32)]
+    cfg = card.EngineConfig(K=16, k=3, ratio=4, max_new_tokens=200, mode=mode)
+    free = card.run_vanilla(t, prompt, cfg).output
+    eos = free[len(free) // 3]                   # a token greedy decoding emits early on
+    t.eos_token = d.eos_token = eos
+    van = card.run_vanilla(t, prompt, cfg)
+    res = card.run_speculative(d, t, prompt, cfg, use_graphs=True)
+    assert van.output[-1] == eos and len(van.output) <= len(free) // 3 + 1
+    assert res.output == van.output
