@@ -107,13 +107,23 @@ LAUNCHES = {
     "card_kgram_dist": 1, "card_rows_topk": 1, "card_log_cr": 1, "card_exp_cr": 1,
     "card_cache_reset": 2, "card_cache_expand": 2, "card_cache_expand_topk": 1, "card_cache_pool": 2,
     "card_cache_query": 1, "card_cache_correct": 1, "card_cache_advance_root": 1, "card_cache_count_alive": 1,
-    "card_cache_clear_status": 1, "card_embed": 1, "card_rmsnorm": 1, "card_rope_kv": 1, "card_attention": lambda a: 1 if (a[10] == 0 and a[17] == 0 and a[13] in (64, 128) and a[4]) else 3,
+    "card_cache_clear_status": 1, "card_embed": 1, "card_rmsnorm": 1, "card_rope_kv": 1, "card_attention": lambda a: 1 if (a[10] == 0 and a[17] == 0 and a[13] in (64, 128) and a[4] and _attn_fits(a)) else 3,
     "card_topk_logits": 2, "card_argmax_logits": 2, "card_softmax64": 1, "card_logit_bias": 1,
     "card_draft_rows": 1, "card_target_rows": 1, "card_eos_fix": 1, "card_record_width": 1,
     "card_verify_argmax": 1, "card_verify_probs": 1, "card_commit": 1, "card_draft_promote": 2,
     "card_kv_compact": 2, "card_cycle_end": 1, "card_engine_handoff": 1,
 }
 launch_count = [0]
+
+
+def _attn_fits(a) -> bool:
+    """Mirror of attn_fused_fits (card_attn.cu): the fused attention gathers at
+    most 1024 extra slots per tile of 64/128 query-heads."""
+    m_max, nh, nkv, extra_max = a[2], a[11], a[12], a[7]
+    G = nh // nkv
+    qt = 128 if m_max * G >= 512 else 64
+    rows = qt // G + 2
+    return rows <= 136 and rows * extra_max <= 1024
 
 
 class _Counted:

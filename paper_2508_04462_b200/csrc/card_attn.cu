@@ -36,7 +36,7 @@ namespace {
 
 constexpr int kCh = 64;      // keys per chunk
 constexpr int kMaxTileRows = 136;  // rows per tile of <= 128 query-heads (GQA group >= 1)
-constexpr int kMaxExtra = 1024;    // gathered extra slots per tile
+constexpr int kMaxExtra = 1024;    // gathered extra slots per tile (static smem: keep two CTAs per SM)
 
 __device__ __forceinline__ uint32_t s_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
 __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
@@ -407,6 +407,16 @@ static cudaError_t launch_qt(cudaLaunchConfig_t& cfg, const float* q, const int3
     }
     return cudaLaunchKernelEx(&cfg, attn_fused_kernel<HD, QT>, q, dM, plen, slot, n_extra, extra, extra_max,
                               (const __nv_bfloat16*)kc, (const __nv_bfloat16*)vc, nh, nkv, (__nv_bfloat16*)o);
+}
+
+// The fused kernel gathers every tile row's extra slots into one list of at
+// most kMaxExtra keys; callers fall back to the split-KV kernels when a tile
+// could need more (rows per tile x extra slots per row).
+bool attn_fused_fits(int m_max, int nh, int nkv, int extra_max) {
+    const int G = nh / nkv;
+    const int QT = (m_max * G >= 512) ? 128 : 64;
+    const int rows = QT / G + 2;
+    return rows <= kMaxTileRows && rows * extra_max <= kMaxExtra;
 }
 
 int launch_attn_fused(const float* q, const int32_t* dM, int m_max, const int32_t* plen, const int32_t* slot,

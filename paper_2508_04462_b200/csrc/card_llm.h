@@ -13,6 +13,7 @@ int launch_attn_fused(const float* q, const int32_t* dM, int m_max, const int32_
                       const int32_t* extra, int extra_max, const void* kc, const void* vc, int nh, int nkv, int hd,
                       int max_plen, void* o, cudaStream_t s);
 int attn_set_trace(unsigned long long* buf);
+bool attn_fused_fits(int m_max, int nh, int nkv, int extra_max);
 }  // namespace card
 
 // GEMM epilogues (card_gemm.cu)

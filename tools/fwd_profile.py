@@ -17,7 +17,7 @@ preset, m = {"d116": ("llama-3.2-1b", 116), "t8": ("llama-3.1-8b", 8), "t1": ("l
 cfg = PRESETS[preset]
 mdl = card.LlamaModel(cfg, seed=1, dtype="bf16")
 rt = mdl.runtime(1088, 0, sorted({m, 128}))
-rows = RowBlock(m, 32, rt.dev)
+rows = RowBlock(m, 16, rt.dev)
 rows.set_chain([int(x) for x in np.random.default_rng(0).integers(0, cfg.vocab_size, m)], 1000 - m,
                out_last_only=False)
 for _ in range(2):

@@ -35,7 +35,7 @@ def bench_model(name, preset, m_rows, ctx_len):
     cfg = PRESETS[preset]
     m = card.LlamaModel(cfg, seed=1, dtype="bf16")
     rt = m.runtime(ctx_len + 64, 0, sorted({m_rows, 128}))
-    rows = RowBlock(m_rows, 32, rt.dev)
+    rows = RowBlock(m_rows, 16, rt.dev)
     toks = list(np.random.default_rng(0).integers(0, cfg.vocab_size, m_rows))
     rows.set_chain(toks, ctx_len - m_rows, out_last_only=False)
     dM = rows.M

@@ -15,7 +15,7 @@ def build(preset, m, seed):
     cfg = PRESETS[preset]
     mdl = card.LlamaModel(cfg, seed=seed, dtype="bf16")
     rt = mdl.runtime(1088, 0, sorted({m, 128}))
-    rows = RowBlock(m, 32, rt.dev)
+    rows = RowBlock(m, 16, rt.dev)
     rows.set_chain([int(x) for x in np.random.default_rng(0).integers(0, cfg.vocab_size, m)], 1000 - m,
                    out_last_only=False)
     rt.forward(rows, m)

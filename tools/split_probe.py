@@ -11,7 +11,7 @@ cfg = PRESETS["llama-3.2-1b"]
 mdl = card.LlamaModel(cfg, seed=1, dtype="bf16")
 def mk(m):
     rt = DeviceLlama(cfg, mdl.packed, max_ctx=1088, tree_slots=0, row_budgets=sorted({m, 128}))
-    rows = RowBlock(m, 32, rt.dev)
+    rows = RowBlock(m, 16, rt.dev)
     rows.set_chain([int(x) for x in np.random.default_rng(m).integers(0, cfg.vocab_size, m)], 1000 - m, out_last_only=False)
     rt.forward(rows, m); torch.cuda.synchronize()
     g = torch.cuda.CUDAGraph(); st = torch.cuda.Stream(); st.wait_stream(torch.cuda.current_stream())
