@@ -138,22 +138,34 @@ def test_card_greedy_is_lossless_on_transformers(card, dtype):
     assert step.metrics.mean_acceptance_length > 1.0
 
 
-def test_fp32_card_matches_oracle_engine(card):
-    """Greedy fp32 run: the device engine and the oracle engine (the
-    reference schedule driving the CPU transformer) emit identical tokens."""
+@pytest.mark.parametrize("case", [
+    dict(seed=9, sharp=20.0, mix=0.05, cfg=dict(K=6, k=2, ratio=3, max_new_tokens=40)),
+    dict(seed=3, sharp=40.0, mix=0.0, cfg=dict(K=10, k=3, ratio=4, max_new_tokens=48)),
+    dict(seed=5, sharp=10.0, mix=0.2, cfg=dict(K=4, k=1, ratio=2, max_new_tokens=32)),
+    dict(seed=7, sharp=30.0, mix=0.05, cfg=dict(K=8, k=3, ratio=5, max_new_tokens=40, correction_enabled=False)),
+])
+def test_fp32_card_matches_oracle_engine(card, case):
+    """Greedy fp32 runs: the device engine and the oracle engine (the
+    reference schedule, engine.py:290-317, driving the CPU transformer) emit
+    identical tokens and an identical trace — hits, candidate lengths,
+    accepted-prefix lengths and committed counts per step, and the tree size
+    after every step (cache.py:174-184)."""
     from oracle import card_oracle as O
     from oracle.llama_ref import RefModel
     from paper_2508_04462_b200.lm import LogitBias
 
-    bias = LogitBias(seed=11, order=2, sharpness=20.0, mix_seed=131, mix_weight=0.05)
+    bias = LogitBias(seed=11, order=2, sharpness=case["sharp"], mix_seed=131, mix_weight=case["mix"])
     d, t, wd, wt, cd, ct = _tiny_pair(card, "fp32", bias=bias)
-    prompt = [int(x) for x in np.random.default_rng(9).integers(0, ct.vocab_size, 16)]
-    cfg = dict(K=6, k=2, ratio=3, max_new_tokens=40)
+    prompt = [int(x) for x in np.random.default_rng(case["seed"]).integers(0, ct.vocab_size, 16)]
+    cfg = case["cfg"]
     res = card.run_speculative(d, t, prompt, card.EngineConfig(**cfg), use_graphs=False)
     rd = RefModel(cd, wd, forward_latency=1.0, bias=bias)
     rt = RefModel(ct, wt, forward_latency=7.0, params_billions=8.0, bias=bias)
     out, trace = O.run_serial(rd, rt, prompt, **cfg)
     assert res.output == out
+    strip = lambda tr: [(e.event, e.hit, e.candidate_len, e.accepted_len, e.lnew, e.cache_alive_nodes)  # noqa: E731
+                        for e in tr]
+    assert strip(res.trace) == strip(trace)
 
 
 def test_card_greedy_lossless_high_acceptance_bf16(card):
