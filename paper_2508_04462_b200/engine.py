@@ -216,7 +216,13 @@ class _LlamaAdapter:
         budgets = {rows_max, PREFILL_CHUNK}
         dev = run.dev_d if role == "draft" else run.dev_t
         with torch.cuda.device(dev):
-            self.rt = model.runtime(run.max_ctx, tree_slots, budgets)
+            if getattr(run, "private_runtimes", False):   # batched requests: own KV cache and buffers, shared weights
+                from .llama import DeviceLlama
+
+                self.rt = DeviceLlama(model.cfg, model.packed, max_ctx=run.max_ctx, tree_slots=tree_slots,
+                                      row_budgets=sorted(budgets))
+            else:
+                self.rt = model.runtime(run.max_ctx, tree_slots, budgets)
         if self.rt.dev != dev:
             raise ConfigError(f"the {role} model lives on {self.rt.dev}, the run places it on {dev}")
         if self.rt.extra_max < run.cfg.max_depth + 1:
@@ -335,8 +341,9 @@ class DeviceRun:
     """State of one decode on the device (engine.py:149-272)."""
 
     def __init__(self, draft, target, prompt, config: EngineConfig, *, trace_alive: bool = True,
-                 devices: tuple[int, int] | None = None):
+                 devices: tuple[int, int] | None = None, private_runtimes: bool = False):
         _check_pair(draft, target)
+        self.private_runtimes = private_runtimes
         self.draft_model, self.target_model = draft, target
         self.cfg = config
         self.dev = require_cuda()
@@ -578,8 +585,12 @@ class DeviceRun:
         self.launches_per_graph = (c1 - c0, c2 - c1)
         self.replays = [0, 0]
 
-    def run_graphs(self, max_cycles: int | None = None):
-        """Throughput driver: one host<->device round trip per cycle."""
+    def graph_cycles(self, max_cycles: int | None = None):
+        """The graph driver as a generator (engine.py:290-317 schedule): each
+        step launches work on the current stream, records an event and yields
+        it; the caller resumes it once the event has completed.  One
+        host<->device round trip per cycle; run_graphs() drives one request,
+        the batch driver interleaves several on their own streams."""
         cfg = self.cfg
         d_lat = self.draft_model.spec.forward_latency
         t_lat = self.target_model.spec.forward_latency
@@ -589,7 +600,11 @@ class DeviceRun:
         for _ in range(cfg.query_depth):   # warm-up (engine.py:295-301)
             g_d.replay()
             self.replays[0] += 1
-        E = self.read_state()
+        self._host.copy_(self.E, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        yield ev
+        E = EngineState.from_buffer_copy(self._host.numpy().tobytes())
         for i in range(min(E.n_widths, 64)):
             w = E.widths[i]
             if w == 0:
@@ -605,10 +620,12 @@ class DeviceRun:
             n_exp = min(cfg.ratio, max(0, cfg.max_depth - depth))
             for _ in range(n_exp):
                 g_d.replay()
-            g_t.replay()
+            g_t.replay()   # ends with the record copy into self._host
             self.replays[0] += n_exp
             self.replays[1] += 1
-            torch.cuda.current_stream().synchronize()
+            ev = torch.cuda.Event()
+            ev.record()
+            yield ev
             E = EngineState.from_buffer_copy(self._host.numpy().tobytes())
             start, k = clock, 0
             for i in range(min(E.rec_n_widths, 64)):
@@ -628,7 +645,13 @@ class DeviceRun:
             cycles += 1
             if max_cycles is not None and cycles >= max_cycles:
                 break
-        return cycles
+        self.cycles = cycles
+
+    def run_graphs(self, max_cycles: int | None = None):
+        """Throughput driver: one host<->device round trip per cycle."""
+        for ev in self.graph_cycles(max_cycles):
+            ev.synchronize()
+        return self.cycles
 
 
 class _ConcurrentDriver:
@@ -840,6 +863,61 @@ def run_speculative(draft, target, prompt: Sequence[TokenId], config: EngineConf
     run.timing["wall_s"] = time.perf_counter() - t0
     return RunResult(output=run.output, metrics=finalize(run.trace, target.spec, draft.spec), trace=run.trace,
                      wall=run.timing)
+
+
+def run_speculative_batch(draft, target, prompts: Sequence[Sequence[TokenId]], config: EngineConfig,
+                          ) -> tuple[list[RunResult], dict]:
+    """Several requests decoded at once on one GPU (BASELINE configs[4]).
+
+    Every request gets its own candidate tree, engine state and model
+    runtimes (KV caches, activation buffers; the weights are shared) and its
+    own CUDA stream; the host interleaves the requests' serial_sim cycles
+    (DeviceRun.graph_cycles) so the GPU overlaps one request's
+    latency-bound draft kernels with another's.  Each request follows the
+    reference schedule exactly: its tokens and trace equal a single
+    run_speculative of the same prompt.  Returns (results, timing) with
+    timing["decode_ms"] the wall time of the interleaved decode (all
+    requests) and timing["tokens"] the tokens emitted by all of them."""
+    kinds = {getattr(draft, "engine_kind", "host"), getattr(target, "engine_kind", "host")}
+    if kinds != {"llama"}:
+        raise ConfigError("run_speculative_batch needs a transformer draft/target pair")
+    if not config.correction_enabled or config.mode != "serial_sim":
+        raise ConfigError("run_speculative_batch runs the serial_sim schedule with correction enabled")
+    _validate_run_config(draft, target, config)
+    runs, streams, gens = [], [], []
+    for p in prompts:
+        run = DeviceRun(draft, target, p, config, trace_alive=False, private_runtimes=True)
+        run.prefill()
+        run.capture()
+        runs.append(run)
+        streams.append(torch.cuda.Stream())
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    pending = []
+    for run, st in zip(runs, streams):
+        with torch.cuda.stream(st):
+            g = run.graph_cycles()
+            pending.append((g, next(g), st))
+    while pending:
+        nxt = []
+        for g, ev, st in pending:
+            if not ev.query():
+                nxt.append((g, ev, st))
+                continue
+            with torch.cuda.stream(st):
+                try:
+                    nxt.append((g, next(g), st))
+                except StopIteration:
+                    pass
+        pending = nxt
+    torch.cuda.synchronize()
+    wall_ms = (time.perf_counter() - t0) * 1e3
+    results = []
+    for run in runs:
+        run.timing.update(draft_steps=run.replays[0], target_steps=run.replays[1])
+        results.append(RunResult(output=run.output, metrics=finalize(run.trace, target.spec, draft.spec),
+                                 trace=run.trace, wall=run.timing))
+    return results, {"decode_ms": wall_ms, "tokens": sum(len(r.output) for r in results), "requests": len(runs)}
 
 
 # ====================================================================== vanilla AR

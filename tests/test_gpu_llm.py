@@ -250,3 +250,23 @@ def test_eos_on_transformer_pair(card, mode):
     res = card.run_speculative(d, t, prompt, cfg, use_graphs=True)
     assert van.output[-1] == eos and len(van.output) <= len(free) // 3 + 1
     assert res.output == van.output
+
+
+def test_batch_of_requests_equals_single_runs(card):
+    """run_speculative_batch (several requests interleaved on their own
+    streams, BASELINE configs[4]): every request's tokens and trace equal a
+    single run of the same prompt."""
+    from paper_2508_04462_b200.lm import LogitBias
+
+    bias = LogitBias(seed=11, order=2, sharpness=4000.0)
+    d, t, *_ = _tiny_pair(card, "bf16", "small-target", "small-draft", bias=bias)
+    rng = np.random.default_rng(21)
+    prompts = [[int(x) for x in rng.integers(0, t.vocab.size, n)] for n in (24, 40, 33)]
+    cfg = card.EngineConfig(K=16, k=3, ratio=5, max_new_tokens=96)
+    batch, timing = card.run_speculative_batch(d, t, prompts, cfg)
+    assert timing["requests"] == 3 and timing["tokens"] == sum(len(r.output) for r in batch)
+    strip = lambda tr: [(e.event, e.hit, e.candidate_len, e.accepted_len, e.lnew) for e in tr]  # noqa: E731
+    for p, got in zip(prompts, batch):
+        one = card.run_speculative(d, t, p, cfg)
+        assert got.output == one.output
+        assert strip(got.trace) == strip(one.trace)
