@@ -136,7 +136,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
         if (a.trace) a.trace[blockIdx.x * 16 + (k)] = gtimer(); \
     } while (0)
 
-__device__ __forceinline__ float silu(float x) { return x * __frcp_rn(1.0f + __expf(-x)); }
+__device__ __forceinline__ float silu(float x) { return __fdividef(x, 1.0f + __expf(-x)); }
 
 struct TcArgs;
 
