@@ -143,8 +143,18 @@ struct TcArgs;
 // ---------------------------------------------------------------- tcgen05 GEMM
 constexpr int kTileN = 128;   // weight rows per tile (MMA M)
 constexpr int kBK = 64;       // bf16 K per stage = one 128-byte swizzle atom
-constexpr int kEpiThreads = 128;
-constexpr int kTcThreads = 192;   // warps 0-3 epilogue, 4 TMA producer, 5 MMA issuer
+// NG epilogue groups of four warps (each group covers the 128 TMEM lanes =
+// tile rows; group g drains token chunks g, g+NG, ...), then the TMA
+// producer warp and the MMA issuer warp.  Wide tiles (Mpad > 16) use NG = 2:
+// their epilogues are bound by the math of 4 warps; narrow ones NG = 1 (two
+// CTAs per SM must fit the register file).
+constexpr int kGroupThreads = 128;
+template <int NG>
+struct Roles {
+    static constexpr int kEpiThreads = NG * kGroupThreads;
+    static constexpr int kProdWarp = NG * 4, kMmaWarp = NG * 4 + 1;
+    static constexpr int kThreads = NG * kGroupThreads + 64;
+};
 
 struct TcArgs {
     int N, K, kb_total, n_tiles, splits, items, Mpad, stages, tmem_cols, n_acc_buf;
@@ -194,7 +204,7 @@ __device__ __forceinline__ void sts_f32(uint32_t addr, float v) {
 template <int EPI>
 __device__ __forceinline__ void epi_chunk(const TcArgs& a, int tile, int n_glob, int n_local, int m0, int mc,
                                           float* v, uint32_t xch, const float* invs, const int* tpos,
-                                          const int* tslot, float* xch_ptr) {
+                                          const int* tslot, float* xch_ptr, int gbar) {
     const float b = a.bias ? a.bias[n_glob] : 0.f;
     if (a.ssq_in)
 #pragma unroll
@@ -203,7 +213,7 @@ __device__ __forceinline__ void epi_chunk(const TcArgs& a, int tile, int n_glob,
         // pair partner row n_local +- hd/2 of the same head, through xch [16][128]
 #pragma unroll
         for (int j = 0; j < 16; ++j) sts_f32(xch + (uint32_t)((j * 128 + n_local) * 4), v[j] + b);
-        named_bar(1, kEpiThreads);
+        named_bar(gbar, kGroupThreads);
         const int half = a.hd >> 1;
         const int head = n_glob / a.hd, i = n_glob - head * a.hd;
         if (i < half) {   // the first-half thread of each pair stores both
@@ -241,7 +251,7 @@ __device__ __forceinline__ void epi_chunk(const TcArgs& a, int tile, int n_glob,
                 }
             }
         }
-        named_bar(1, kEpiThreads);
+        named_bar(gbar, kGroupThreads);
         return;
     }
     if (EPI == EPI_SWIGLU_BF16) {
@@ -257,13 +267,13 @@ __device__ __forceinline__ void epi_chunk(const TcArgs& a, int tile, int n_glob,
 #pragma unroll
         for (int j = 0; j < 16; ++j)
             if ((j < 8) == up) sts_f32(xch + (uint32_t)((j * 128 + n_local) * 4), v[j] + b);
-        named_bar(1, kEpiThreads);
+        named_bar(gbar, kGroupThreads);
         const int jb = up ? 8 : 0;
         const uint32_t other = xch + (uint32_t)(((up ? f : 64 + f)) * 4);
         float o[8];
 #pragma unroll
         for (int jj = 0; jj < 8; ++jj) o[jj] = lds_f32(other + (uint32_t)((jb + jj) * 128 * 4));
-        named_bar(1, kEpiThreads);
+        named_bar(gbar, kGroupThreads);
         // stage bf16 outputs [16 tokens][64 features] in the (now free) front of xch
         __nv_bfloat16* stg = reinterpret_cast<__nv_bfloat16*>(xch_ptr);
 #pragma unroll
@@ -273,7 +283,7 @@ __device__ __forceinline__ void epi_chunk(const TcArgs& a, int tile, int n_glob,
             const float u = up ? v[j] + b : o[jj];
             stg[j * 64 + f] = __float2bfloat16(silu(g) * u);
         }
-        named_bar(1, kEpiThreads);
+        named_bar(gbar, kGroupThreads);
         {
             const int row = n_local >> 3, piece = n_local & 7;   // 16 rows x 8 pieces of 16 B
             if (row < mc) {
@@ -281,7 +291,7 @@ __device__ __forceinline__ void epi_chunk(const TcArgs& a, int tile, int n_glob,
                 *reinterpret_cast<uint4*>(a.out_bf16 + (int64_t)(m0 + row) * a.ldo + tile * 64 + piece * 8) = val;
             }
         }
-        named_bar(1, kEpiThreads);
+        named_bar(gbar, kGroupThreads);
         return;
     }
     if (EPI == EPI_RESID_F32) {
@@ -313,9 +323,10 @@ __device__ __forceinline__ void epi_chunk(const TcArgs& a, int tile, int n_glob,
 // CL: split-K cluster variant (one item per CTA, DSMEM reduction); else the
 // persistent direct-epilogue variant.  Separate instantiations keep each
 // kernel's code small (instruction-cache misses were a measurable cost).
-template <int EPI, bool CL>
-__global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_constant__ CUtensorMap tmW,
+template <int EPI, bool CL, int NG>
+__global__ void __launch_bounds__(Roles<NG>::kThreads, 1) tc_gemm_kernel(const __grid_constant__ CUtensorMap tmW,
                                                                const __grid_constant__ CUtensorMap tmX, TcArgs a) {
+    using R_ = Roles<NG>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1024-byte alignment for SWIZZLE_128B atoms
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -329,21 +340,21 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
     uint64_t* tfull = empty + S;    // [2]
     uint64_t* tempty = tfull + 2;   // [2]
     uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
-    float* xch = (float*)(tmem_slot + 4);   // [16][128]
-    float* invs = xch + 16 * 128;            // [256] per-token rsqrt(mean x^2 + eps)
+    float* xch = (float*)(tmem_slot + 4);   // [groups][16][128] (group 1's only when Mpad > 16)
+    float* invs = xch + (a.Mpad > 16 ? 2 : 1) * 16 * 128;   // [256] per-token rsqrt(mean x^2 + eps)
     int* tpos = (int*)(invs + 256);          // [256] QKV: RoPE position of each token row
     int* tslot = tpos + 256;                 // [256] QKV: KV-cache slot of each token row
 
     const int warp = warp_id(), lane = lane_id();
     if (threadIdx.x == 0) TC_STAMP(0);
-    if (warp == 4 && lane == 0) {
+    if (warp == R_::kProdWarp && lane == 0) {
         for (int i = 0; i < S; ++i) {
             mbar_init(&full[i], 1);
             mbar_init(&empty[i], 1);
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&tfull[i], 1);
-            mbar_init(&tempty[i], 4);
+            mbar_init(&tempty[i], R_::kEpiThreads / 32);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         tma_prefetch_desc(&tmW);
@@ -353,7 +364,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
     // first pipeline stages of weights before the TMEM allocation (which may
     // wait for a co-resident CTA of the previous GEMM) and the grid dependency.
     int pre = 0;
-    if (warp == 4 && lane == 0 && a.w_tiled) {
+    if (warp == R_::kProdWarp && lane == 0 && a.w_tiled) {
         const int item = blockIdx.x;
         if (item < a.items) {
             const int tile = item / a.splits, split = item % a.splits;
@@ -387,12 +398,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
 
     if (M <= 0) {
         // zero-row replay: drain the prefetched stages, then leave
-        if (warp == 4 && lane == 0)
+        if (warp == R_::kProdWarp && lane == 0)
             for (int i = 0; i < pre; ++i) {
                 tma_load_2d(sB + (size_t)i * bytesB, &tmX, &full[i], 0, xoff);
                 mbar_wait(&full[i], 0);
             }
-    } else if (warp == 4) {
+    } else if (warp == R_::kProdWarp) {
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
@@ -427,7 +438,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
                 first = false;
             }
         }
-    } else if (warp == 5) {
+    } else if (warp == R_::kMmaWarp) {
         if (lane == 0) {
             const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n_mma >> 3) << 17) |
                                    ((uint32_t)(kTileN >> 4) << 24);
@@ -471,14 +482,16 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
             }
         }
     } else {
-        // ---------------- epilogue warps 0..3: TMEM lane = tile row n_local
-        const int n_local = warp * 32 + lane;
+        // ---------------- epilogue warps 0..7: TMEM lane = tile row n_local
+        const int grp = warp >> 2, wq = warp & 3;
+        const int n_local = wq * 32 + lane;
+        const int et = threadIdx.x;   // 0..255 over both groups
         if (EPI == EPI_QKV_ROPE) {
-            for (int m = n_local; m < M; m += kEpiThreads) {
+            for (int m = et; m < M; m += R_::kEpiThreads) {
                 tpos[m] = a.pos[m];
                 tslot[m] = a.slot[m];
             }
-            if (!a.ssq_in) named_bar(1, kEpiThreads);
+            if (!a.ssq_in) named_bar(1, R_::kEpiThreads);
         }
         if (a.ssq_in) {
             // RMSNorm scale of each token row (overlaps the main loop).  T = 8
@@ -487,11 +500,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
             // the same token would get a different scale in an M=1 AR step
             // than in an M=8 verify step (greedy CARD must equal greedy AR).
             constexpr int T = 8;
-            const int t = n_local & (T - 1);
+            const int t = et & (T - 1);
             const int per = (a.ssq_parts + T - 1) / T;
             const int p0 = t * per, p1 = min(a.ssq_parts, p0 + per);
-            for (int mb = 0; mb * (kEpiThreads / T) < M; ++mb) {   // uniform trip count (shuffles)
-                const int m = mb * (kEpiThreads / T) + n_local / T;
+            for (int mb = 0; mb * (R_::kEpiThreads / T) < M; ++mb) {   // uniform trip count (shuffles)
+                const int m = mb * (R_::kEpiThreads / T) + et / T;
                 float acc = 0.f;
                 if (m < M) {
                     const float* src = a.ssq_in + xoff + m;
@@ -506,7 +519,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
                 for (int o = T >> 1; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
                 if (m < M && t == 0) invs[m] = rsqrtf(acc * a.inv_h + a.norm_eps);
             }
-            named_bar(1, kEpiThreads);
+            named_bar(1, R_::kEpiThreads);
         }
         int acc = 0;
         uint32_t acc_phase = 0;
@@ -531,14 +544,15 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
                 __nanosleep(128);
             }
             tc_fence_after();
-            const uint32_t trow = tmem_base + ((uint32_t)(warp * 32) << 16) + (uint32_t)(acc * a.Mpad);
+            const uint32_t trow = tmem_base + ((uint32_t)(wq * 32) << 16) + (uint32_t)(acc * a.Mpad);
             // cluster mode (splits > 1): the accumulator stays in TMEM until
             // every rank of the cluster has finished its main loop (below)
-            for (int m0 = 0; m0 < M && !CL; m0 += 16) {
+            float* gx = xch + grp * 16 * 128;
+            for (int m0 = grp * 16; m0 < M && !CL; m0 += NG * 16) {
                 float v[16];
                 tmem_ld16(trow + (uint32_t)m0, v);
                 const int mc = (M - m0) < 16 ? (M - m0) : 16;
-                epi_chunk<EPI>(a, tile, n_glob, n_local, m0, mc, v, smem_u32(xch), invs, tpos, tslot, xch);
+                epi_chunk<EPI>(a, tile, n_glob, n_local, m0, mc, v, smem_u32(gx), invs, tpos, tslot, gx, 2 + grp);
             }
             tc_fence_before();
             __syncwarp();
@@ -569,15 +583,16 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
         float* buf = reinterpret_cast<float*>(smem);   // [S][R][ld] over the stage buffers
         cluster_sync_all();
         if (threadIdx.x == 0) TC_STAMP(5);
-        if (warp < 4 && M > 0) {
+        if (warp < R_::kEpiThreads / 32 && M > 0) {
             const int me = (int)cluster_rank();
-            const int n_local = warp * 32 + lane;
+            const int grp = warp >> 2;
+            const int n_local = (warp & 3) * 32 + lane;
             const int i = n_local % P, qd = n_local / P;
             const int owner = i / Pp;
             const int lr = qd * Pp + (i - owner * Pp);
             const uint32_t dst = dsmem_addr(smem_u32(buf), (uint32_t)owner) + (uint32_t)(((me * R + lr) * ld) * 4);
-            const uint32_t trow = tmem_base + ((uint32_t)(warp * 32) << 16);
-            for (int m0 = 0; m0 < M; m0 += 16) {
+            const uint32_t trow = tmem_base + ((uint32_t)((warp & 3) * 32) << 16);
+            for (int m0 = grp * 16; m0 < M; m0 += NG * 16) {
                 float v[16];
                 tmem_ld16(trow + (uint32_t)m0, v);
 #pragma unroll
@@ -590,7 +605,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
         if (threadIdx.x == 0) TC_STAMP(6);
         cluster_sync_all();   // all pushes landed; no remote access after this point
         if (threadIdx.x == 0) TC_STAMP(7);
-        if (warp < 4 && M > 0) {
+        if (warp < R_::kEpiThreads / 32 && M > 0) {
             // owner reduction: thread -> (output j, token stripe); RJ outputs per
             // token (R rows, or R/2 pairs), TP token lanes; B tokens per pass
             // with every load issued first.
@@ -599,7 +614,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
             const uint32_t sbuf = smem_u32(buf);
             const bool paired = (EPI == EPI_SWIGLU_BF16 || EPI == EPI_QKV_ROPE);
             const int RJ = paired ? R / 2 : R;
-            const int TP = kEpiThreads / RJ;
+            const int TP = R_::kEpiThreads / RJ;
             const int j = threadIdx.x % RJ, m_first = threadIdx.x / RJ;
             // local rows and tile rows of output j (pair: lr0/n0 and lr0 + Pp / n0 + P)
             int lr0, n0;
@@ -698,9 +713,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
             }
             if (EPI == EPI_RESID_F32 && a.ssq_out) {
                 // per-16-column sums of squares, fixed order, from slice 0
-                named_bar(1, kEpiThreads);
+                named_bar(1, R_::kEpiThreads);
                 const int G16 = R / 16;
-                for (int e = threadIdx.x; e < G16 * M; e += kEpiThreads) {
+                for (int e = threadIdx.x; e < G16 * M; e += R_::kEpiThreads) {
                     const int gi = e / M, m = e - gi * M;
                     float t = 0.f;
 #pragma unroll
@@ -913,19 +928,26 @@ namespace card {
 
 // The attribute is per kernel, not per plan: always allow the full 227 KB so
 // plans of different Mpad (hence smem) can share one template instance.
+template <int EPI, int NG>
+static void set_tc_attr_ng() {
+    cudaFuncSetAttribute(tc_gemm_kernel<EPI, true, NG>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(tc_gemm_kernel<EPI, true, NG>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(tc_gemm_kernel<EPI, false, NG>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+}
 template <int EPI>
 static cudaError_t set_tc_attr(int smem) {
     (void)smem;
-    cudaFuncSetAttribute(tc_gemm_kernel<EPI, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    cudaFuncSetAttribute(tc_gemm_kernel<EPI, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    return cudaFuncSetAttribute(tc_gemm_kernel<EPI, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    set_tc_attr_ng<EPI, 1>();
+    set_tc_attr_ng<EPI, 2>();
+    return cudaGetLastError();
 }
 
 template <int EPI>
 static cudaError_t launch_tc(const card_linear* h, const TcArgs& a, cudaStream_t s) {
     cudaLaunchConfig_t cfg = {};
+    const int ng = a.Mpad > 16 ? 2 : 1;
     cfg.gridDim = dim3(h->grid);
-    cfg.blockDim = dim3(kTcThreads);
+    cfg.blockDim = dim3(ng == 2 ? Roles<2>::kThreads : Roles<1>::kThreads);
     cfg.dynamicSmemBytes = h->smem;
     cfg.stream = s;
     cudaLaunchAttribute attr[2];
@@ -941,8 +963,12 @@ static cudaError_t launch_tc(const card_linear* h, const TcArgs& a, cudaStream_t
     }
     cfg.attrs = attr;
     cfg.numAttrs = n;
-    if (a.cluster > 1) return cudaLaunchKernelEx(&cfg, tc_gemm_kernel<EPI, true>, h->tmW, h->tmX, a);
-    return cudaLaunchKernelEx(&cfg, tc_gemm_kernel<EPI, false>, h->tmW, h->tmX, a);
+    if (ng == 2) {
+        if (a.cluster > 1) return cudaLaunchKernelEx(&cfg, tc_gemm_kernel<EPI, true, 2>, h->tmW, h->tmX, a);
+        return cudaLaunchKernelEx(&cfg, tc_gemm_kernel<EPI, false, 2>, h->tmW, h->tmX, a);
+    }
+    if (a.cluster > 1) return cudaLaunchKernelEx(&cfg, tc_gemm_kernel<EPI, true, 1>, h->tmW, h->tmX, a);
+    return cudaLaunchKernelEx(&cfg, tc_gemm_kernel<EPI, false, 1>, h->tmW, h->tmX, a);
 }
 
 // Cluster split-K choice.  Wide N (>= half the resident CTA slots in
@@ -967,7 +993,7 @@ static int choose_cluster(int n_tiles, int kb_total, int Mpad, int slots, int sm
     while (S > 1) {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(n_tiles * S);
-        cfg.blockDim = dim3(kTcThreads);
+        cfg.blockDim = dim3(Mpad > 16 ? Roles<2>::kThreads : Roles<1>::kThreads);
         cfg.dynamicSmemBytes = smem;
         cudaLaunchAttribute attr;
         attr.id = cudaLaunchAttributeClusterDimension;
@@ -977,7 +1003,8 @@ static int choose_cluster(int n_tiles, int kb_total, int Mpad, int slots, int sm
         cfg.attrs = &attr;
         cfg.numAttrs = 1;
         int nc = 0;
-        const cudaError_t oe = cudaOccupancyMaxActiveClusters(&nc, tc_gemm_kernel<EPI, true>, &cfg);
+        const cudaError_t oe = Mpad > 16 ? cudaOccupancyMaxActiveClusters(&nc, tc_gemm_kernel<EPI, true, 2>, &cfg)
+                                         : cudaOccupancyMaxActiveClusters(&nc, tc_gemm_kernel<EPI, true, 1>, &cfg);
         if (getenv("CARD_CLUSTER_DEBUG"))
             fprintf(stderr, "choose_cluster: tiles=%d kb=%d Mpad=%d S=%d smem=%d -> max active clusters %d (%s)\n", n_tiles,
                     kb_total, Mpad, S, smem, nc, cudaGetErrorString(oe));
@@ -1073,7 +1100,7 @@ int card_linear_create(const void* W, int N, int K, int wdtype, const void* X, i
     const int stage_bytes = kTileN * kBK * 2 + Mpad * kBK * 2;
     int budget = (ctas_per_sm == 2 ? 110 : 220) * 1024;
     if (getenv("CARD_GEMM_SMEM_KB")) budget = atoi(getenv("CARD_GEMM_SMEM_KB")) * 1024;   // tuning knob
-    const int extra = 1024 + 64 * 8 + 16 * 128 * 4 + 3 * 256 * 4 + 64;
+    const int extra = 1024 + 64 * 8 + (Mpad > 16 ? 2 : 1) * 16 * 128 * 4 + 3 * 256 * 4 + 64;
     int stages = (budget - extra) / stage_bytes;
     if (stages > 8) stages = 8;
     if (stages < 2) stages = 2;
