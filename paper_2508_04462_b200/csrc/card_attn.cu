@@ -150,9 +150,13 @@ __global__ void __launch_bounds__(QT * 2) attn_fused_kernel(const float* __restr
     // one thread per tile row loads (plen, n_extra); warp 0 scans the extra
     // counts (a serial single-thread loop of dependent loads cost ~10 us)
     if (threadIdx.x == 0) s_kmax = 0;
-    for (int i = threadIdx.x; i < nrows; i += kThr) xne[i] = max(0, min(n_extra[r0 + i], extra_max));
     __syncthreads();
-    for (int i = threadIdx.x; i < nrows; i += kThr) atomicMax(&s_kmax, plen[r0 + i]);
+    for (int i = threadIdx.x; i < nrows; i += kThr) {   // both loads in flight together
+        const int ne = n_extra[r0 + i], pl = plen[r0 + i];
+        xne[i] = max(0, min(ne, extra_max));
+        atomicMax(&s_kmax, pl);
+    }
+    __syncthreads();
     if (warp_id() == 0) {
         int carry = 0;
         for (int b0 = 0; b0 < nrows; b0 += 32) {
@@ -173,8 +177,12 @@ __global__ void __launch_bounds__(QT * 2) attn_fused_kernel(const float* __restr
         if (lane_id() == 0) s_nx = min(carry, kMaxExtra);
     }
     __syncthreads();
-    for (int i = 0; i <= r1 - r0; ++i)
-        for (int j = threadIdx.x; j < xne[i]; j += kThr) xs[xoff[i] + j] = extra[(int64_t)(r0 + i) * extra_max + j];
+    // gather over the flat (row, j) space: a few independent loads per thread
+    // instead of one dependent load-store pair per tile row
+    for (int e = threadIdx.x; e < nrows * extra_max; e += kThr) {
+        const int i = e / extra_max, j = e - i * extra_max;
+        if (j < xne[i]) xs[xoff[i] + j] = extra[(int64_t)r0 * extra_max + e];
+    }
     const int n_ch = (s_kmax + kCh - 1) / kCh;
     const int n_xch = (s_nx + kCh - 1) / kCh;
     const int n_all = n_ch + n_xch;
@@ -367,24 +375,35 @@ __global__ void __launch_bounds__(QT * 2) attn_fused_kernel(const float* __restr
         float Mx = -INFINITY;
         for (int s = 0; s < S; ++s) Mx = fmaxf(Mx, recv[(s * QO + ql) * PW]);
         const float Ms = Mx == -INFINITY ? 0.f : Mx;
-        float w[16], L = 0.f;
+        float L = 0.f;
         for (int s = 0; s < S; ++s) {
             const float* rec = recv + (s * QO + ql) * PW;
-            w[s] = rec[0] == -INFINITY ? 0.f : __expf(rec[0] - Ms);
-            L += w[s] * rec[1];
+            const float w = rec[0] == -INFINITY ? 0.f : __expf(rec[0] - Ms);
+            s_w[ql][s] = w;
+            L += w * rec[1];
         }
         const float invL = L > 0.f ? 1.0f / L : 0.f;
-        for (int s = 0; s < S; ++s) s_w[ql][s] = w[s] * invL;
+        for (int s = 0; s < S; ++s) s_w[ql][s] *= invL;
     }
     __syncthreads();
-    for (int e = threadIdx.x; e < QO * HD; e += kThr) {
-        const int ql = e / HD, d = e - ql * HD;
+    // two adjacent dims per thread (8-byte smem loads, bf16x2 stores); the
+    // rank loop is unrolled to the cluster-size bound so its loads overlap
+    for (int e = threadIdx.x; e < QO * HD / 2; e += kThr) {
+        const int ql = e / (HD / 2), d = 2 * (e - ql * (HD / 2));
         const int qi = q0 + rank * QO + ql;
         if (qi >= nq) break;
-        float acc = 0.f;
-        for (int s = 0; s < S; ++s) acc += s_w[ql][s] * recv[(s * QO + ql) * PW + 2 + d];
-        const int r = qi / G, h = g * G + qi % G;
-        o_out[((int64_t)r * nh + h) * HD + d] = __float2bfloat16(acc);
+        float ax = 0.f, ay = 0.f;
+#pragma unroll
+        for (int s = 0; s < 16; ++s) {
+            if (s < S) {
+                const float w = s_w[ql][s];
+                const float2 v = *reinterpret_cast<const float2*>(recv + (s * QO + ql) * PW + 2 + d);
+                ax += w * v.x;
+                ay += w * v.y;
+            }
+        }
+        const int r = qi / G, h = g * G + (qi - r * G);
+        *reinterpret_cast<__nv_bfloat162*>(o_out + ((int64_t)r * nh + h) * HD + d) = __floats2bfloat162_rn(ax, ay);
     }
     at_stamp(7);
 }
