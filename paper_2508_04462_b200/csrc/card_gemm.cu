@@ -98,6 +98,15 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
 #pragma unroll
     for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
+// issue-only TMEM load (no wait): several chunks go in flight before one tmem_wait_ld()
+__device__ __forceinline__ void tmem_ld16_issue(uint32_t taddr, uint32_t* r) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
 __device__ __forceinline__ void cluster_sync_all() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
@@ -339,7 +348,8 @@ __global__ void __launch_bounds__(Roles<NG>::kThreads, 1) tc_gemm_kernel(const _
     uint64_t* empty = full + S;
     uint64_t* tfull = empty + S;    // [2]
     uint64_t* tempty = tfull + 2;   // [2]
-    uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+    uint64_t* rbar = tempty + 2;    // split-K: every rank's slice of my rows landed (bulk DSMEM copies)
+    uint32_t* tmem_slot = (uint32_t*)(rbar + 2);
     float* xch = (float*)(tmem_slot + 4);   // [groups][16][128] (group 1's only when Mpad > 16)
     float* invs = xch + (a.Mpad > 16 ? 2 : 1) * 16 * 128;   // [256] per-token rsqrt(mean x^2 + eps)
     int* tpos = (int*)(invs + 256);          // [256] QKV: RoPE position of each token row
@@ -356,6 +366,7 @@ __global__ void __launch_bounds__(Roles<NG>::kThreads, 1) tc_gemm_kernel(const _
             mbar_init(&tfull[i], 1);
             mbar_init(&tempty[i], R_::kEpiThreads / 32);
         }
+        mbar_init(rbar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         tma_prefetch_desc(&tmW);
         tma_prefetch_desc(&tmX);
@@ -567,44 +578,104 @@ __global__ void __launch_bounds__(Roles<NG>::kThreads, 1) tc_gemm_kernel(const _
     }
     if (CL) {
         // split-K over the cluster (S = a.cluster ranks = the K-slices of one
-        // tile).  Push-based DSMEM reduction.  Tile rows are grouped in pair
-        // blocks of P rows (P = 128 plain, 64 SwiGLU gate/up, hd/2 RoPE): rank
-        // r owns Pp = P/S rows of every P-block, so each pair (n, n + P) stays
-        // on one owner.  After barrier 1 every rank's pipeline smem is free;
-        // each epilogue thread (one tile row) stores its partial sums into the
-        // owner's smem with 16-byte st.shared::cluster (fire-and-forget).
-        // After barrier 2 each owner sums its S slices in rank order
-        // (deterministic) from local smem and applies the epilogue.
+        // tile).  Tile rows are grouped in pair blocks of P rows (P = 128
+        // plain, 64 SwiGLU gate/up, hd/2 RoPE): rank r owns Pp = P/S rows of
+        // every P-block, so each pair (n, n + P) stays on one owner.  The
+        // pipeline smem is free once the accumulator is ready; it holds
+        //   recv [S][R][ld]  slice s = rank s's partial of my rows, and
+        //   send [S][R][ld]  block o = my partial of owner o's rows (NG = 1).
+        // Narrow tiles (NG = 1): each epilogue thread (one tile row) drains
+        // TMEM into its send block with local 16-byte stores; after cluster
+        // barrier 1 (every rank's recv region is free) S lanes move the
+        // blocks with bulk DSMEM copies that complete_tx on the owner's rbar,
+        // and the owner waits on rbar alone.  Either way the owner sums its S
+        // slices in rank order (deterministic).
         const int S = a.cluster;
         const int R = kTileN / S;
         const int P = (EPI == EPI_SWIGLU_BF16) ? 64 : (EPI == EPI_QKV_ROPE) ? (a.hd >> 1) : kTileN;
         const int Pp = P / S;
         const int ld = a.Mpad + 4;   // padded slice row (floats): spreads banks
-        float* buf = reinterpret_cast<float*>(smem);   // [S][R][ld] over the stage buffers
-        cluster_sync_all();
-        if (threadIdx.x == 0) TC_STAMP(5);
-        if (warp < R_::kEpiThreads / 32 && M > 0) {
-            const int me = (int)cluster_rank();
-            const int grp = warp >> 2;
-            const int n_local = (warp & 3) * 32 + lane;
-            const int i = n_local % P, qd = n_local / P;
-            const int owner = i / Pp;
-            const int lr = qd * Pp + (i - owner * Pp);
-            const uint32_t dst = dsmem_addr(smem_u32(buf), (uint32_t)owner) + (uint32_t)(((me * R + lr) * ld) * 4);
-            const uint32_t trow = tmem_base + ((uint32_t)((warp & 3) * 32) << 16);
-            for (int m0 = grp * 16; m0 < M; m0 += NG * 16) {
-                float v[16];
-                tmem_ld16(trow + (uint32_t)m0, v);
+        float* buf = reinterpret_cast<float*>(smem);   // recv [S][R][ld] over the stage buffers
+        float* snd = buf + kTileN * ld;                // send [S][R][ld]
+        if (NG == 2) {
+            // wide tiles: each epilogue thread pushes its row's partial sums
+            // straight into the owner's recv slice with 16-byte
+            // st.shared::cluster (overlaps the TMEM drain; a staged bulk copy
+            // measured slower here, DSMEM bandwidth bounds both), then a
+            // second cluster barrier publishes them
+            cluster_sync_all();   // every rank's main loop done: recv regions free
+            if (threadIdx.x == 0) TC_STAMP(5);
+            if (warp < R_::kEpiThreads / 32 && M > 0) {
+                const int me = (int)cluster_rank();
+                const int grp = warp >> 2;
+                const int n_local = (warp & 3) * 32 + lane;
+                const int i = n_local % P, qd = n_local / P;
+                const int owner = i / Pp;
+                const int lr = qd * Pp + (i - owner * Pp);
+                const uint32_t dst = dsmem_addr(smem_u32(buf), (uint32_t)owner) + (uint32_t)(((me * R + lr) * ld) * 4);
+                const uint32_t trow = tmem_base + ((uint32_t)((warp & 3) * 32) << 16);
+                for (int m0 = grp * 16; m0 < M; m0 += NG * 16) {
+                    float v[16];
+                    tmem_ld16(trow + (uint32_t)m0, v);
 #pragma unroll
-                for (int q = 0; q < 4; ++q)
-                    asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(dst + (uint32_t)((m0 + 4 * q) * 4)),
-                                 "f"(v[4 * q]), "f"(v[4 * q + 1]), "f"(v[4 * q + 2]), "f"(v[4 * q + 3])
-                                 : "memory");
+                    for (int q = 0; q < 4; ++q)
+                        asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(
+                                         dst + (uint32_t)((m0 + 4 * q) * 4)),
+                                     "f"(v[4 * q]), "f"(v[4 * q + 1]), "f"(v[4 * q + 2]), "f"(v[4 * q + 3])
+                                     : "memory");
+                }
             }
+            if (threadIdx.x == 0) TC_STAMP(6);
+            cluster_sync_all();   // all pushes landed; no remote access after this point
+            if (threadIdx.x == 0) TC_STAMP(7);
+        } else {
+            const uint32_t blk_bytes = (uint32_t)(R * ld * 4);
+            const int me = (int)cluster_rank();
+            if (warp < R_::kEpiThreads / 32 && M > 0) {
+                if (threadIdx.x == 0) mbar_expect_tx(rbar, (uint32_t)S * blk_bytes);
+                const int grp = warp >> 2;
+                const int n_local = (warp & 3) * 32 + lane;
+                const int i = n_local % P, qd = n_local / P;
+                const int owner = i / Pp;
+                const int lr = qd * Pp + (i - owner * Pp);
+                const uint32_t dst = smem_u32(snd) + (uint32_t)(((owner * R + lr) * ld) * 4);
+                const uint32_t trow = tmem_base + ((uint32_t)((warp & 3) * 32) << 16);
+                // up to four 16-column chunks in flight per TMEM wait
+                constexpr int kStep = NG * 16;
+                for (int m0 = grp * 16; m0 < M; m0 += 4 * kStep) {
+                    uint32_t r[4][16];
+    #pragma unroll
+                    for (int c = 0; c < 4; ++c)
+                        if (m0 + c * kStep < M) tmem_ld16_issue(trow + (uint32_t)(m0 + c * kStep), r[c]);
+                    tmem_wait_ld();
+    #pragma unroll
+                    for (int c = 0; c < 4; ++c)
+                        if (m0 + c * kStep < M)
+    #pragma unroll
+                            for (int q = 0; q < 4; ++q)
+                                asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(
+                                                 dst + (uint32_t)((m0 + c * kStep + 4 * q) * 4)),
+                                             "r"(r[c][4 * q]), "r"(r[c][4 * q + 1]), "r"(r[c][4 * q + 2]), "r"(r[c][4 * q + 3])
+                                             : "memory");
+                }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // staged rows -> bulk-copy reads
+            }
+            cluster_sync_all();   // send blocks staged; every rank's recv region free
+            if (threadIdx.x == 0) TC_STAMP(5);
+            if (warp == 0 && lane < S && M > 0) {
+                const uint32_t src = smem_u32(snd) + (uint32_t)lane * blk_bytes;
+                const uint32_t dst = dsmem_addr(smem_u32(buf), (uint32_t)lane) + (uint32_t)me * blk_bytes;
+                const uint32_t bar = dsmem_addr(smem_u32(rbar), (uint32_t)lane);
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n\t"
+                    "cp.async.bulk.commit_group;" ::"r"(dst),
+                    "r"(src), "r"(blk_bytes), "r"(bar)
+                    : "memory");
+            }
+            if (threadIdx.x == 0) TC_STAMP(6);
+            if (warp < R_::kEpiThreads / 32 && M > 0) mbar_wait(rbar, 0);   // all S slices of my rows landed
+            if (threadIdx.x == 0) TC_STAMP(7);
         }
-        if (threadIdx.x == 0) TC_STAMP(6);
-        cluster_sync_all();   // all pushes landed; no remote access after this point
-        if (threadIdx.x == 0) TC_STAMP(7);
         if (warp < R_::kEpiThreads / 32 && M > 0) {
             // owner reduction: thread -> (output j, token stripe); RJ outputs per
             // token (R rows, or R/2 pairs), TP token lanes; B tokens per pass
@@ -726,6 +797,8 @@ __global__ void __launch_bounds__(Roles<NG>::kThreads, 1) tc_gemm_kernel(const _
         }
     }
     if (threadIdx.x == 0) TC_STAMP(8);
+    // the send blocks must stay intact until the bulk copies have read them
+    if (CL && NG == 1 && warp == 0 && lane < a.cluster && M > 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
     tc_fence_before();
     __syncthreads();
     if (warp == 0) {
@@ -981,7 +1054,8 @@ template <int EPI>
 static int choose_cluster(int n_tiles, int kb_total, int Mpad, int slots, int smem, int stage_smem, int ctas_per_sm) {
     if (getenv("CARD_NO_CLUSTER") || 2 * n_tiles > slots) return 1;
     int S = 8;
-    while (S > 1 && (n_tiles * S > slots || S > kb_total || (size_t)kTileN * (Mpad + 4) * 4 > (size_t)stage_smem))
+    const size_t red_bytes = (Mpad > 16 ? 1 : 2) * (size_t)kTileN * (Mpad + 4) * 4;   // recv (+ send) regions
+    while (S > 1 && (n_tiles * S > slots || S > kb_total || red_bytes > (size_t)stage_smem))
         S >>= 1;
     if (getenv("CARD_SPLITS")) S = atoi(getenv("CARD_SPLITS"));   // tuning knob (must divide 128)
     if (getenv("CARD_CLUSTER_FORCE")) return S;   // tuning knob: skip the one-wave occupancy check
@@ -1130,7 +1204,7 @@ int card_linear_create(const void* W, int N, int K, int wdtype, const void* X, i
         case EPI_SWIGLU_BF16: S = choose_cluster<EPI_SWIGLU_BF16>(a.n_tiles, a.kb_total, Mpad, slots, h->smem, stage_smem, ctas_per_sm); break;
         case EPI_QKV_ROPE: S = choose_cluster<EPI_QKV_ROPE>(a.n_tiles, a.kb_total, Mpad, slots, h->smem, stage_smem, ctas_per_sm); break;
     }
-    if (S > 1 && (kTileN % S != 0 || (size_t)kTileN * (Mpad + 4) * 4 > (size_t)stage_smem)) {
+    if (S > 1 && (kTileN % S != 0 || (Mpad > 16 ? 1 : 2) * (size_t)kTileN * (Mpad + 4) * 4 > (size_t)stage_smem)) {
         free(h);
         return CARD_E_CONFIG;
     }
