@@ -264,43 +264,25 @@ __device__ __forceinline__ void epi_chunk(const TcArgs& a, int tile, int n_glob,
         return;
     }
     if (EPI == EPI_SWIGLU_BF16) {
-        // rows [0,64) of a tile are gates, [64,128) the matching ups.  Gate
-        // thread f and up thread 64+f swap halves of the chunk through xch
-        // ([16][128] fp32) so all 128 threads share the SwiGLU: the gate thread
-        // finishes tokens 0..7, the up thread tokens 8..15 of feature f.  The
-        // bf16 results are staged as a [16][64] tile and written as 16-byte
-        // vectors (one 128-byte row per token): scattered 2-byte stores made
-        // this epilogue 4x slower.
-        const int f = n_local & 63;
-        const bool up = n_local >= 64;
-#pragma unroll
-        for (int j = 0; j < 16; ++j)
-            if ((j < 8) == up) sts_f32(xch + (uint32_t)((j * 128 + n_local) * 4), v[j] + b);
-        named_bar(gbar, kGroupThreads);
+        // rows 32q..32q+15 of a tile are the gates of features 16q..16q+15,
+        // rows 32q+16..32q+31 the matching ups (interleave_gate_up), so warp q
+        // holds both halves of its 16 features: lanes l and l^16 swap halves
+        // of the chunk with one shuffle per token pair.  The gate lane
+        // finishes tokens 0..7, the up lane tokens 8..15 of feature
+        // 16q + (l & 15); each store instruction writes two 32-byte rows.
+        const int lane = n_local & 31;
+        const bool up = lane >= 16;
+        const int f = tile * 64 + (n_local >> 5) * 16 + (lane & 15);
         const int jb = up ? 8 : 0;
-        const uint32_t other = xch + (uint32_t)(((up ? f : 64 + f)) * 4);
-        float o[8];
-#pragma unroll
-        for (int jj = 0; jj < 8; ++jj) o[jj] = lds_f32(other + (uint32_t)((jb + jj) * 128 * 4));
-        named_bar(gbar, kGroupThreads);
-        // stage bf16 outputs [16 tokens][64 features] in the (now free) front of xch
-        __nv_bfloat16* stg = reinterpret_cast<__nv_bfloat16*>(xch_ptr);
 #pragma unroll
         for (int jj = 0; jj < 8; ++jj) {
-            const int j = jb + jj;
-            const float g = up ? o[jj] : v[j] + b;
-            const float u = up ? v[j] + b : o[jj];
-            stg[j * 64 + f] = __float2bfloat16(silu(g) * u);
+            const float lo = v[jj] + b, hi = v[8 + jj] + b;   // static indices: v stays in registers
+            const float mine = up ? hi : lo;
+            const float other = __shfl_xor_sync(0xffffffffu, up ? lo : hi, 16);
+            const float g = up ? other : mine;
+            const float u = up ? mine : other;
+            if (jb + jj < mc) a.out_bf16[(int64_t)(m0 + jb + jj) * a.ldo + f] = __float2bfloat16(silu(g) * u);
         }
-        named_bar(gbar, kGroupThreads);
-        {
-            const int row = n_local >> 3, piece = n_local & 7;   // 16 rows x 8 pieces of 16 B
-            if (row < mc) {
-                const uint4 val = *reinterpret_cast<const uint4*>(stg + row * 64 + piece * 8);
-                *reinterpret_cast<uint4*>(a.out_bf16 + (int64_t)(m0 + row) * a.ldo + tile * 64 + piece * 8) = val;
-            }
-        }
-        named_bar(gbar, kGroupThreads);
         return;
     }
     if (EPI == EPI_RESID_F32) {
@@ -579,7 +561,7 @@ __global__ void __launch_bounds__(Roles<NG>::kThreads, 1) tc_gemm_kernel(const _
     if (CL) {
         // split-K over the cluster (S = a.cluster ranks = the K-slices of one
         // tile).  Tile rows are grouped in pair blocks of P rows (P = 128
-        // plain, 64 SwiGLU gate/up, hd/2 RoPE): rank r owns Pp = P/S rows of
+        // plain, 16 SwiGLU gate/up, hd/2 RoPE): rank r owns Pp = P/S rows of
         // every P-block, so each pair (n, n + P) stays on one owner.  The
         // pipeline smem is free once the accumulator is ready; it holds
         //   recv [S][R][ld]  slice s = rank s's partial of my rows, and
@@ -592,7 +574,7 @@ __global__ void __launch_bounds__(Roles<NG>::kThreads, 1) tc_gemm_kernel(const _
         // slices in rank order (deterministic).
         const int S = a.cluster;
         const int R = kTileN / S;
-        const int P = (EPI == EPI_SWIGLU_BF16) ? 64 : (EPI == EPI_QKV_ROPE) ? (a.hd >> 1) : kTileN;
+        const int P = (EPI == EPI_SWIGLU_BF16) ? 16 : (EPI == EPI_QKV_ROPE) ? (a.hd >> 1) : kTileN;
         const int Pp = P / S;
         const int ld = a.Mpad + 4;   // padded slice row (floats): spreads banks
         float* buf = reinterpret_cast<float*>(smem);   // recv [S][R][ld] over the stage buffers
@@ -750,7 +732,8 @@ __global__ void __launch_bounds__(Roles<NG>::kThreads, 1) tc_gemm_kernel(const _
                     const float sc = a.ssq_in ? invs[m] : 1.f;
                     const float x = v0[q] * sc + bias0;
                     if (EPI == EPI_SWIGLU_BF16) {
-                        a.out_bf16[(int64_t)m * a.ldo + tile * 64 + n0] = __float2bfloat16(silu(x) * (v1[q] * sc + bias1));
+                        a.out_bf16[(int64_t)m * a.ldo + tile * 64 + (n0 >> 5) * 16 + (n0 & 15)] =
+                            __float2bfloat16(silu(x) * (v1[q] * sc + bias1));
                     } else if (EPI == EPI_QKV_ROPE) {
                         const float x2 = v1[q] * sc + bias1;
                         if (qhead < a.nh + a.nkv) {
@@ -875,7 +858,7 @@ __global__ void __launch_bounds__(256) gemv_bf16_kernel(const __nv_bfloat16* __r
                 const int n = row0 + r;
                 if (n >= N) continue;
                 if (EPI == EPI_SWIGLU_BF16) {
-                    // interleaved tiles: partner row of gate n is n + 64 (same tile)
+                    // interleaved rows: partner of gate row n is n + 16 (same 32-row block)
                     continue;
                 }
                 epi_store<EPI>(a, n, 0, 0, acc[r], nullptr);
@@ -894,9 +877,9 @@ __global__ void swiglu_from_rows_kernel(const float* __restrict__ rows, const in
     const int F = N / 2;
     for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < M * F; idx += gridDim.x * blockDim.x) {
         const int m = idx / F, f = idx % F;
-        const int tile = f / 64, j = f % 64;
-        const float g = rows[(int64_t)m * N + tile * 128 + j];
-        const float u = rows[(int64_t)m * N + tile * 128 + 64 + j];
+        const int blk = f / 16, j = f % 16;   // 16 gate rows, then the 16 matching up rows
+        const float g = rows[(int64_t)m * N + blk * 32 + j];
+        const float u = rows[(int64_t)m * N + blk * 32 + 16 + j];
         out[(int64_t)m * ldo + f] = __float2bfloat16(silu(g) * u);
     }
 }
@@ -935,9 +918,9 @@ __global__ void swiglu_f32_kernel(const float* __restrict__ rows, const int32_t*
     const int F = N / 2;
     for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < M * F; idx += gridDim.x * blockDim.x) {
         const int m = idx / F, f = idx % F;
-        const int tile = f / 64, j = f % 64;
-        const float g = rows[(int64_t)m * N + tile * 128 + j];
-        const float u = rows[(int64_t)m * N + tile * 128 + 64 + j];
+        const int blk = f / 16, j = f % 16;   // 16 gate rows, then the 16 matching up rows
+        const float g = rows[(int64_t)m * N + blk * 32 + j];
+        const float u = rows[(int64_t)m * N + blk * 32 + 16 + j];
         out[(int64_t)m * ldo + f] = (g / (1.0f + expf(-g))) * u;
     }
 }

@@ -11,8 +11,8 @@ libcard_b200.so; the weights stream through the tcgen05/TMA GEMM.
 
 Weight layout in HBM (bf16 production / fp32 parity):
   embed [V,H]; per layer wqkv [(nh+2nkv)*hd, H] (+ fp32 bias for Qwen2),
-  wo [H, nh*hd], wgu [2F, H] interleaved per 128-row tile (64 gate rows then
-  the 64 matching up rows), wd [H, F], fp32 norms; lm_head [V,H] (tied for
+  wo [H, nh*hd], wgu [2F, H] interleaved per 32-row block (16 gate rows then
+  the 16 matching up rows), wd [H, F], fp32 norms; lm_head [V,H] (tied for
   Llama-3.2-1B / Qwen2.5-0.5B).  KV cache per layer: K,V [slots, nkv, hd]
   with slots = prefix positions (rounded to 64) + draft tree slots.
 """
@@ -172,9 +172,10 @@ def tile_sw128(w: torch.Tensor) -> torch.Tensor:
 
 
 def interleave_gate_up(wg: torch.Tensor, wu: torch.Tensor) -> torch.Tensor:
-    """[2F, H]: per 128-row tile, 64 gate rows then the 64 matching up rows."""
+    """[2F, H]: per 32-row block, 16 gate rows then the 16 matching up rows, so
+    one epilogue warp (32 TMEM lanes) holds both halves of its 16 features."""
     F, H = wg.shape
-    t = torch.stack([wg.view(F // 64, 64, H), wu.view(F // 64, 64, H)], dim=1)
+    t = torch.stack([wg.view(F // 16, 16, H), wu.view(F // 16, 16, H)], dim=1)
     return t.reshape(2 * F, H).contiguous()
 
 
