@@ -428,12 +428,17 @@ static cudaError_t launch_qt(cudaLaunchConfig_t& cfg, const float* q, const int3
                               (const __nv_bfloat16*)kc, (const __nv_bfloat16*)vc, nh, nkv, (__nv_bfloat16*)o);
 }
 
+static int attn_qt(int m_max, int G) {
+    if (getenv("CARD_ATTN_QT")) return atoi(getenv("CARD_ATTN_QT")) == 128 ? 128 : 64;   // tuning knob
+    return (m_max * G >= 512) ? 128 : 64;
+}
+
 // The fused kernel gathers every tile row's extra slots into one list of at
 // most kMaxExtra keys; callers fall back to the split-KV kernels when a tile
 // could need more (rows per tile x extra slots per row).
 bool attn_fused_fits(int m_max, int nh, int nkv, int extra_max) {
     const int G = nh / nkv;
-    const int QT = (m_max * G >= 512) ? 128 : 64;
+    const int QT = attn_qt(m_max, G);
     const int rows = QT / G + 2;
     return rows <= kMaxTileRows && rows * extra_max <= kMaxExtra;
 }
@@ -444,7 +449,7 @@ int launch_attn_fused(const float* q, const int32_t* dM, int m_max, const int32_
     const int G = nh / nkv;
     const int n_ch = (max_plen + kCh - 1) / kCh;
     // wide (draft tree) forwards: 128 query-heads per CTA; narrow: 64
-    const int QT = (m_max * G >= 512) ? 128 : 64;
+    const int QT = attn_qt(m_max, G);
     const int n_qt = (m_max * G + QT - 1) / QT;
     // narrow forwards (verify / AR: one query tile per kv head) spread the
     // context over 16 ranks (non-portable cluster; 2% faster verify forward
