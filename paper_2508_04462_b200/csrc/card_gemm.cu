@@ -69,6 +69,12 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
         "l"(src), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
 }
+// one stage's weight block as `pieces` bulk copies on the same barrier
+__device__ __forceinline__ void bulk_load_split(uint8_t* dst, const uint8_t* src, uint32_t bytes, uint64_t* bar,
+                                                int pieces) {
+    const uint32_t part = bytes / (uint32_t)pieces;
+    for (int p = 0; p < pieces; ++p) bulk_load(dst + p * part, src + p * part, part, bar);
+}
 __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* map) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
 }
@@ -170,6 +176,7 @@ struct TcArgs {
     const int32_t* dM;
     const uint8_t* w_tiled;   // non-null: [n_tiles][kb_total][128 x 128 B] pre-swizzled blocks
     int epi;
+    int bulk_pieces;   // bulk copies per 16 KB weight stage (tuning)
     int cluster;      // == splits: split-K over a thread-block cluster, DSMEM reduction
     float* out_f32;
     __nv_bfloat16* out_bf16;
@@ -367,8 +374,8 @@ __global__ void __launch_bounds__(Roles<NG>::kThreads, 1) tc_gemm_kernel(const _
 #pragma unroll 1
             for (int i = 0; i < pre; ++i) {
                 mbar_expect_tx(&full[i], bytesA + bytesB);
-                bulk_load(sA + (size_t)i * bytesA, a.w_tiled + ((size_t)tile * a.kb_total + kb0 + i) * (size_t)bytesA,
-                          bytesA, &full[i]);
+                bulk_load_split(sA + (size_t)i * bytesA, a.w_tiled + ((size_t)tile * a.kb_total + kb0 + i) * (size_t)bytesA,
+                                bytesA, &full[i], a.bulk_pieces);
             }
         }
     }
@@ -418,8 +425,9 @@ __global__ void __launch_bounds__(Roles<NG>::kThreads, 1) tc_gemm_kernel(const _
                     mbar_wait(&empty[stage], phase ^ 1);
                     mbar_expect_tx(&full[stage], bytesA + bytesB);
                     if (a.w_tiled)
-                        bulk_load(sA + (size_t)stage * bytesA,
-                                  a.w_tiled + ((size_t)tile * a.kb_total + kb) * (size_t)bytesA, bytesA, &full[stage]);
+                        bulk_load_split(sA + (size_t)stage * bytesA,
+                                        a.w_tiled + ((size_t)tile * a.kb_total + kb) * (size_t)bytesA, bytesA, &full[stage],
+                                        a.bulk_pieces);
                     else
                         tma_load_2d(sA + (size_t)stage * bytesA, &tmW, &full[stage], kb * kBK, tile * kTileN);
                     tma_load_2d(sB + (size_t)stage * bytesB, &tmX, &full[stage], kb * kBK, xoff);
@@ -1162,6 +1170,9 @@ int card_linear_create(const void* W, int N, int K, int wdtype, const void* X, i
     if (stages > 8) stages = 8;
     if (stages < 2) stages = 2;
     a.stages = stages;
+    a.bulk_pieces = 1;
+    if (getenv("CARD_BULK_PIECES")) a.bulk_pieces = atoi(getenv("CARD_BULK_PIECES"));   // tuning knob (1, 2, 4, 8)
+    if (a.bulk_pieces != 2 && a.bulk_pieces != 4 && a.bulk_pieces != 8) a.bulk_pieces = 1;
     h->smem = stages * stage_bytes + extra;
     const int slots = num_sms() * ctas_per_sm;
     cudaError_t e;
