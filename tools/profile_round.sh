@@ -3,7 +3,7 @@
 set -x
 mkdir -p gpurun_out/prof
 # 1. launch list of a short CARD + AR decode on the BASELINE config
-NEW=32 SHARP=${SHARP:-0} timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+NEW=32 SHARP=${SHARP:-1e6} timeout 900 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv \
   --log-file gpurun_out/prof/launches_card.csv python tools/profile_steps.py > gpurun_out/prof/launches_card.log 2>&1
 # 2. per-launch DRAM traffic of every tc_gemm launch of one target verify forward (M = r+1 = 8)
 timeout 600 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none \
