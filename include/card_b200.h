@@ -94,6 +94,12 @@ int card_cache_create(int root_token, int K, int k, int max_depth, int eos_token
                       int capacity, card_cache** out);
 int card_cache_destroy(card_cache* h);
 
+/* Return the handle to the state card_cache_create(root_token, ...) leaves
+ * it in (arena, hash, frontier, epoch and counters), asynchronously on
+ * `stream`.  No reference counterpart: it lets a serving session reuse one
+ * arena (and the CUDA graphs that point into it) across requests. */
+int card_cache_clear(card_cache* h, int root_token, void* stream);
+
 /* reset(root_token) (cache.py:439-444).  If d_root_token != NULL the token
  * is read on the device (engine path), else root_token is used. */
 int card_cache_reset(card_cache* h, const int32_t* d_root_token, int root_token, void* stream);

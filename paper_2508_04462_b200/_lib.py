@@ -39,6 +39,7 @@ SIGNATURES = {
     "card_cache_create": (c_int, [c_int, c_int, c_int, c_int, c_int, c_int, POINTER(c_void_p)]),
     "card_cache_destroy": (c_int, [_P]),
     "card_cache_reset": (c_int, [_P, _P, c_int, _P]),
+    "card_cache_clear": (c_int, [_P, c_int, _P]),
     "card_cache_expand": (c_int, [_P, _P, c_int, c_int, _P]),
     "card_cache_expand_topk": (c_int, [_P, _P, _P, _P, c_int, c_int, _P, _P]),
     "card_cache_pool": (c_int, [_P, _P, c_int, c_int, _P, _P, _P, _P, _P]),
@@ -105,7 +106,7 @@ class EngineState(ctypes.Structure):
 # kernels launched per C-ABI call (for the bench's gpu_launches count)
 LAUNCHES = {
     "card_kgram_dist": 1, "card_rows_topk": 1, "card_log_cr": 1, "card_exp_cr": 1,
-    "card_cache_reset": 2, "card_cache_expand": 2, "card_cache_expand_topk": 1, "card_cache_pool": 2,
+    "card_cache_reset": 2, "card_cache_clear": 3, "card_cache_expand": 2, "card_cache_expand_topk": 1, "card_cache_pool": 2,
     "card_cache_query": 1, "card_cache_correct": 1, "card_cache_advance_root": 1, "card_cache_count_alive": 1,
     "card_cache_clear_status": 1, "card_embed": 1, "card_rmsnorm": 1, "card_rope_kv": 1, "card_attention": lambda a: 1 if (a[10] == 0 and a[17] == 0 and a[13] in (64, 128) and a[4] and _attn_fits(a)) else 3,
     "card_topk_logits": 2, "card_argmax_logits": 2, "card_softmax64": 1, "card_logit_bias": 1,

@@ -284,6 +284,10 @@ class TreeCache:
         raise_for_status(st.status, "advance_root")
         return bool(st.moved)
 
+    def clear(self, root_token: TokenId) -> None:
+        """Back to the freshly created state (new request on a reused arena)."""
+        raise_for_status(lib().card_cache_clear(self._h, int(root_token), stream_ptr()), "clear")
+
     def reset(self, root_token: TokenId) -> None:
         """cache.py:439-444 on the device."""
         if not isinstance(root_token, (int, np.integer)) or root_token < 0:

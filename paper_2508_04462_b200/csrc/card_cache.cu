@@ -59,6 +59,7 @@ struct Bufs {
 struct card_cache {
     card::Bufs b;
     void* block;
+    size_t bytes;
     int K, k, max_depth, eos, capacity, hcap;
 };
 
@@ -750,6 +751,7 @@ int card_cache_create(int root_token, int K, int k, int max_depth, int eos_token
     char* base = (char*)block;
     card_cache* h = (card_cache*)calloc(1, sizeof(card_cache));
     h->block = block;
+    h->bytes = off;
     h->K = K;
     h->k = k;
     h->max_depth = max_depth;
@@ -812,6 +814,30 @@ int card_cache_destroy(card_cache* h) {
     if (!h) return CARD_OK;
     cudaFree(h->block);
     free(h);
+    return CARD_OK;
+}
+
+namespace card {
+__global__ void state_init_kernel(card_cache_state* st, int K, int k, int max_depth, int eos, int capacity,
+                                  int hash_mask) {
+    st->K = K;
+    st->k = k;
+    st->max_depth = max_depth;
+    st->eos = eos;
+    st->capacity = capacity;
+    st->hash_mask = hash_mask;
+}
+}  // namespace card
+
+int card_cache_clear(card_cache* h, int root_token, void* stream) {
+    if (!h) return CARD_E_INPUT;
+    if (root_token < 0) return CARD_E_INPUT;
+    cudaStream_t s = (cudaStream_t)stream;
+    CARD_CUDA_TRY(cudaMemsetAsync(h->block, 0, h->bytes, s));
+    state_init_kernel<<<1, 1, 0, s>>>(h->b.st, h->K, h->k, h->max_depth, h->eos, h->capacity, h->hcap - 1);
+    clear_hash_kernel<<<64, 256, 0, s>>>(h->b, h->hcap);
+    init_root_kernel<<<1, 1, 0, s>>>(h->b, nullptr, root_token, 0);
+    CARD_LAUNCH_CHECK();
     return CARD_OK;
 }
 

@@ -156,6 +156,10 @@ class _RowsAndTail:
         self.order = max(1, order)
         self.tail = torch.full((rows_max, self.order), -1, dtype=torch.int32, device=dev)
 
+    def reset(self):
+        self.rows.block.zero_()
+        self.tail.fill_(-1)
+
 
 class _KGramAdapter:
     """Device k-gram toy (lm.py:199-256 via card_kgram_dist)."""
@@ -172,6 +176,10 @@ class _KGramAdapter:
         self.tok = torch.zeros((rows_max, k), dtype=torch.int32, device=dev)
         self.val = torch.zeros((rows_max, k), dtype=torch.float64, device=dev)
         self.cnt = torch.zeros(rows_max, dtype=torch.int32, device=dev)
+
+    def reset(self):
+        for t in (self.probs, self.tok, self.val, self.cnt):
+            t.zero_()
 
     def _dists(self, rt: _RowsAndTail, t_score: float):
         m = self.m
@@ -244,6 +252,13 @@ class _LlamaAdapter:
             self.scratch_v = torch.zeros_like(self.scratch_k)
             self.scratch_ptrs = torch.tensor([self.scratch_k.data_ptr(), self.scratch_v.data_ptr()],
                                              dtype=torch.int64, device=dev)
+
+    def reset(self):
+        """Per-request buffers back to their initial contents (session reuse)."""
+        for t in (self.tok, self.logp, self.cnt, self.amax, self.lm_work, self.probs,
+                  getattr(self, "scratch_k", None), getattr(self, "scratch_v", None)):
+            if t is not None:
+                t.zero_()
 
     def _bias_args(self, rt_tail: _RowsAndTail) -> tuple:
         """(ctx_tail, order, stride, seed, seed2, mix, sharpness) of the k-gram
@@ -392,6 +407,7 @@ class DeviceRun:
         st.anchor_origin = int(not cfg.correction_enabled)
         st.n_uni = n_uni
         self.E = torch.frombuffer(bytearray(bytes(st)), dtype=torch.int32).to(self.dev_t)
+        self._E0 = self.E.clone()   # initial state, for rebind()
         self.E_ptr = ptr(self.E)
         # draft-side state: the same buffer in the lockstep drivers; a separate
         # copy in mode="concurrent" (the draft stream never reads the target's
@@ -411,6 +427,33 @@ class DeviceRun:
         self.trace: list[StepTrace] = []
         self.graphs = None
         self.timing = {}
+
+    def rebind(self, prompt) -> None:
+        """Start a new request on this run's device buffers, keeping its
+        captured graphs (which point into them).  The prompt length and the
+        config must be the ones the run was built for; every buffer the first
+        step could read is restored to its constructor contents."""
+        prompt = _check_prompt(prompt, self.target_model.vocab.size)
+        if len(prompt) != len(self.prompt):
+            raise ConfigError("rebind needs a prompt of the run's length")
+        self.prompt = prompt
+        C0 = len(prompt)
+        with torch.cuda.device(self.dev_d):
+            self.cache.clear(prompt[-1])
+        self.committed.zero_()
+        self.committed[:C0] = torch.tensor(prompt, dtype=torch.int32)
+        self.E.copy_(self._E0)
+        if self.Ed is not self.E:
+            self.Ed.copy_(self._E0)
+        self.drt.reset()
+        self.trt.reset()
+        self.da.reset()
+        self.ta.reset()
+        self.output = []
+        self.trace = []
+        self.timing = {}
+        if self.graphs is not None:
+            self.replays = [0, 0]
 
     # ---------------------------------------------------------------- state io
     def _fptr(self, name: str, draft: bool = False) -> ctypes.c_void_p:
@@ -803,6 +846,36 @@ def enable_peer_access(a: int, b: int):
     raise_for_status(lib().card_enable_peer_access(a, b), "card_enable_peer_access")
 
 
+_SESSIONS_PER_TARGET = 2
+
+
+def _model_sig(model) -> tuple:
+    """What a captured run depends on besides the weights: identity, EOS and
+    the agreement-bias / k-gram parameters (all baked into the graphs)."""
+    fields = ("eos_token", "bias", "seed", "mix_seed", "mix_weight", "sharpness", "order")
+    return (id(model),) + tuple(repr(getattr(model, f, None)) for f in fields)
+
+
+def _session_run(draft, target, prompt, config: EngineConfig, trace_alive: bool) -> DeviceRun:
+    """A serving session per (draft, target, config, prompt length): the run's
+    device buffers and its two captured graphs are built by the first request
+    and reused by the next ones (rebind), as a server captures its graphs
+    once per shape at start-up.  Kept on the target model, at most
+    _SESSIONS_PER_TARGET of them, least recently used dropped first."""
+    key = (_model_sig(draft), _model_sig(target), len(prompt), tuple(sorted(config.to_dict().items())),
+           bool(trace_alive))
+    store = target.__dict__.setdefault("_card_sessions", {})
+    run = store.pop(key, None)
+    if run is not None and run.draft_model is draft:
+        run.rebind(prompt)
+    else:
+        run = DeviceRun(draft, target, prompt, config, trace_alive=trace_alive)
+    store[key] = run
+    while len(store) > _SESSIONS_PER_TARGET:
+        store.pop(next(iter(store)))
+    return run
+
+
 def run_speculative(draft, target, prompt: Sequence[TokenId], config: EngineConfig, *,
                     use_graphs: bool | None = None, trace_alive: bool | None = None,
                     devices: tuple[int, int] | None = None) -> RunResult:
@@ -843,11 +916,15 @@ def run_speculative(draft, target, prompt: Sequence[TokenId], config: EngineConf
         run.timing["wall_s"] = time.perf_counter() - t0
         return RunResult(output=run.output, metrics=finalize(run.trace, target.spec, draft.spec), trace=run.trace,
                          wall=run.timing)
-    run = DeviceRun(draft, target, prompt, config, trace_alive=trace_alive)
+    if use_graphs:
+        run = _session_run(draft, target, prompt, config, trace_alive)
+    else:
+        run = DeviceRun(draft, target, prompt, config, trace_alive=trace_alive)
     t0 = time.perf_counter()
     if use_graphs:
         run.prefill()
-        run.capture()
+        if run.graphs is None:
+            run.capture()
         torch.cuda.synchronize()
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ev0.record()

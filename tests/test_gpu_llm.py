@@ -270,3 +270,33 @@ def test_batch_of_requests_equals_single_runs(card):
         one = card.run_speculative(d, t, p, cfg)
         assert got.output == one.output
         assert strip(got.trace) == strip(one.trace)
+
+
+@pytest.mark.parametrize("temperature", [0.0, 1.0])
+def test_session_reuse_equals_fresh_runs(card, temperature):
+    """run_speculative keeps a serving session (device buffers and the two
+    captured graphs) per (pair, config, prompt length).  A request on a reused
+    session emits exactly the tokens, trace and metrics of a fresh run."""
+    from paper_2508_04462_b200.lm import LogitBias
+
+    bias = LogitBias(seed=11, order=2, sharpness=4000.0)
+    d, t, *_ = _tiny_pair(card, "bf16", "small-target", "small-draft", bias=bias)
+    cfg = card.EngineConfig(K=16, k=3, ratio=4, max_new_tokens=96, temperature=temperature, seed=3)
+    prompts = [[int(x) for x in np.random.default_rng(40 + i).integers(0, t.vocab.size, 32)] for i in range(3)]
+    fresh = []
+    for p in prompts:
+        t.__dict__.pop("_card_sessions", None)
+        fresh.append(card.run_speculative(d, t, p, cfg, use_graphs=True))
+    t.__dict__.pop("_card_sessions", None)
+    for i in [0, 1, 2, 0, 2]:
+        res = card.run_speculative(d, t, prompts[i], cfg, use_graphs=True)
+        assert res.output == fresh[i].output
+        assert [e.to_dict() for e in res.trace] == [e.to_dict() for e in fresh[i].trace]
+        assert res.metrics == fresh[i].metrics
+    assert len(t._card_sessions) == 1
+    if temperature > 0.0:
+        return
+    # a changed EOS is part of the session key: the next run builds a new session
+    t.eos_token = d.eos_token = fresh[0].output[5]
+    res = card.run_speculative(d, t, prompts[0], cfg, use_graphs=True)
+    assert len(t._card_sessions) == 2 and res.output[-1] == t.eos_token
