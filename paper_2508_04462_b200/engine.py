@@ -856,20 +856,21 @@ def _model_sig(model) -> tuple:
     return (id(model),) + tuple(repr(getattr(model, f, None)) for f in fields)
 
 
-def _session_run(draft, target, prompt, config: EngineConfig, trace_alive: bool) -> DeviceRun:
+def _session_run(draft, target, prompt, config: EngineConfig, trace_alive: bool,
+                 devices: tuple[int, int] | None = None) -> DeviceRun:
     """A serving session per (draft, target, config, prompt length): the run's
     device buffers and its two captured graphs are built by the first request
     and reused by the next ones (rebind), as a server captures its graphs
     once per shape at start-up.  Kept on the target model, at most
     _SESSIONS_PER_TARGET of them, least recently used dropped first."""
     key = (_model_sig(draft), _model_sig(target), len(prompt), tuple(sorted(config.to_dict().items())),
-           bool(trace_alive))
+           bool(trace_alive), devices)
     store = target.__dict__.setdefault("_card_sessions", {})
     run = store.pop(key, None)
     if run is not None and run.draft_model is draft:
         run.rebind(prompt)
     else:
-        run = DeviceRun(draft, target, prompt, config, trace_alive=trace_alive)
+        run = DeviceRun(draft, target, prompt, config, trace_alive=trace_alive, devices=devices)
     store[key] = run
     while len(store) > _SESSIONS_PER_TARGET:
         store.pop(next(iter(store)))
@@ -898,10 +899,13 @@ def run_speculative(draft, target, prompt: Sequence[TokenId], config: EngineConf
     if devices is not None and not concurrent:
         raise ConfigError("devices=(draft, target) placement needs mode='concurrent' with a transformer pair")
     if concurrent:
-        run = DeviceRun(draft, target, prompt, config, trace_alive=False, devices=devices)
+        run = _session_run(draft, target, prompt, config, False, devices=devices)
         t0 = time.perf_counter()
         run.prefill()
-        drv = _ConcurrentDriver(run)
+        drv = getattr(run, "_cdriver", None)
+        if drv is None:   # the four graphs are captured once per session
+            drv = run._cdriver = _ConcurrentDriver(run)
+        drv.replays = [0, 0, 0, 0]
         for dev in {run.dev_d, run.dev_t}:
             torch.cuda.synchronize(dev)
         ev0 = torch.cuda.Event(enable_timing=True)
