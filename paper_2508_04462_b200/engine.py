@@ -43,7 +43,7 @@ from .metrics import RunMetrics, finalize
 
 TokenId = int
 MODES = ("serial_sim", "concurrent")
-PREFILL_CHUNK = 128
+PREFILL_CHUNK = 256
 
 
 def communication_ratio(target_latency: float, draft_latency: float) -> int:
