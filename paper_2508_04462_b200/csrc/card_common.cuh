@@ -51,6 +51,10 @@ __host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
 __device__ __forceinline__ double to_unit(uint64_t v) {
     return (double)(v >> 11) * (1.0 / 9007199254740992.0);
 }
+// (float)to_unit(v) without the fp64 pipe: v >> 11 < 2^53 is exact in double,
+// the scale is a power of two and the result is a normal float, so rounding
+// the integer to float first and scaling after gives the same bits.
+__device__ __forceinline__ float to_unit_f(uint64_t v) { return __ull2float_rn(v >> 11) * 0x1p-53f; }
 
 // ---------------------------------------------------------------- double-double
 struct dd {

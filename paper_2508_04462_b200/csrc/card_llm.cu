@@ -511,11 +511,14 @@ __device__ __forceinline__ void kg_row_state(const KgBias& b, int r, uint64_t& s
         s2 = mix64(s2 ^ mix64((uint64_t)t + 1));
     }
 }
-__device__ __forceinline__ float kg_apply(const KgBias& b, float logit, int i, uint64_t s1, uint64_t s2) {
-    const uint64_t step = (uint64_t)(i + 1) * kGamma;
-    float u = (float)to_unit(mix64(s1 + step));
-    if (b.mixw != 0.f) u += b.mixw * (float)to_unit(mix64(s2 + step));
+// bias of token i given its splitmix64 stream offset step = (i + 1) * kGamma
+__device__ __forceinline__ float kg_apply_step(const KgBias& b, float logit, uint64_t step, uint64_t s1, uint64_t s2) {
+    float u = to_unit_f(mix64(s1 + step));
+    if (b.mixw != 0.f) u += b.mixw * to_unit_f(mix64(s2 + step));
     return logit + b.sharp * u;
+}
+__device__ __forceinline__ float kg_apply(const KgBias& b, float logit, int i, uint64_t s1, uint64_t s2) {
+    return kg_apply_step(b, logit, (uint64_t)(i + 1) * kGamma, s1, s2);
 }
 
 // ---------------------------------------------------------------- lm_head epilogues (split over the vocab)
@@ -582,10 +585,18 @@ __global__ void __launch_bounds__(256) topk_partial_kernel(const float* __restri
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 const int i = lo + 4 * (vi + u * blockDim.x);
-                consume(lg(q[u].x, i) * inv_temp, i);
-                consume(lg(q[u].y, i + 1) * inv_temp, i + 1);
-                consume(lg(q[u].z, i + 2) * inv_temp, i + 2);
-                consume(lg(q[u].w, i + 3) * inv_temp, i + 3);
+                if (biased) {   // consecutive tokens: the stream offset steps by kGamma
+                    const uint64_t st = (uint64_t)(i + 1) * kGamma;
+                    consume(kg_apply_step(kb, q[u].x, st, ks1, ks2) * inv_temp, i);
+                    consume(kg_apply_step(kb, q[u].y, st + kGamma, ks1, ks2) * inv_temp, i + 1);
+                    consume(kg_apply_step(kb, q[u].z, st + 2 * kGamma, ks1, ks2) * inv_temp, i + 2);
+                    consume(kg_apply_step(kb, q[u].w, st + 3 * kGamma, ks1, ks2) * inv_temp, i + 3);
+                } else {
+                    consume(q[u].x * inv_temp, i);
+                    consume(q[u].y * inv_temp, i + 1);
+                    consume(q[u].z * inv_temp, i + 2);
+                    consume(q[u].w * inv_temp, i + 3);
+                }
             }
         }
         for (; vi < nv; vi += blockDim.x) {
@@ -884,8 +895,8 @@ __global__ void logit_bias_kernel(float* __restrict__ logits, const int32_t* dM,
     float* lr = logits + (int64_t)r * V;
     for (int i = threadIdx.x; i < V; i += blockDim.x) {
         const uint64_t step = (uint64_t)(i + 1) * kGamma;
-        float u = (float)to_unit(mix64(st[0] + step));
-        if (mixw != 0.f) u += mixw * (float)to_unit(mix64(st[1] + step));
+        float u = to_unit_f(mix64(st[0] + step));
+        if (mixw != 0.f) u += mixw * to_unit_f(mix64(st[1] + step));
         lr[i] += sharp * u;
     }
 }
