@@ -194,6 +194,13 @@ int card_linear_fuse_norm(card_linear* h, const float* ssq, int parts, int ld, f
 int card_linear_fuse_resid(card_linear* h, float* ssq_out, int ld, void* xb_out);
 int card_linear_fuse_rope(card_linear* h, const int32_t* pos, const int32_t* slot, const float* cos_t,
                           const float* sin_t, int nh, int nkv, int hd, float* q_out, void* k_cache, void* v_cache);
+/* fuse_kgram: an EPI_STORE_F32 lm_head adds the k-gram logit bias of
+ * card_logit_bias (_kernels.pyx:44-93 uniforms, output row m's context tail
+ * ctx_tail[m*stride ..]) to every logit it stores, so the top-k / argmax
+ * readers run without it.  Same fp32 arithmetic as the readers' on-the-fly
+ * bias (bit-identical logits).  ctx_tail == NULL turns it off. */
+int card_linear_fuse_kgram(card_linear* h, const int32_t* ctx_tail, int order, int stride, uint64_t seed,
+                           uint64_t seed2, float mix_weight, float sharpness);
 /* tuning: per-CTA %globaltimer stamps [grid][16] (NULL disables) */
 int card_linear_trace(card_linear* h, unsigned long long* trace);
 int card_linear_destroy(card_linear* h);

@@ -60,6 +60,8 @@ SIGNATURES = {
     "card_linear_fuse_norm": (c_int, [_P, _P, c_int, c_int, ctypes.c_float, c_int, _P]),
     "card_linear_fuse_resid": (c_int, [_P, _P, c_int, _P]),
     "card_linear_fuse_rope": (c_int, [_P, _P, _P, _P, _P, c_int, c_int, c_int, _P, _P, _P]),
+    "card_linear_fuse_kgram": (c_int, [_P, _P, c_int, c_int, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_float,
+                                       ctypes.c_float]),
     "card_linear_destroy": (c_int, [_P]),
     "card_embed": (c_int, [_P, _P, c_int, _P, c_int, c_int, _P, _P, _P, c_int, _P]),
     "card_rmsnorm": (c_int, [_P, _P, c_int, ctypes.c_float, _P, c_int, _P, _P, c_int, _P]),

@@ -56,6 +56,37 @@ __device__ __forceinline__ double to_unit(uint64_t v) {
 // the integer to float first and scaling after gives the same bits.
 __device__ __forceinline__ float to_unit_f(uint64_t v) { return __ull2float_rn(v >> 11) * 0x1p-53f; }
 
+// k-gram logit bias (agreement knob): logits[r][i] + sharp * (u1_i + mixw *
+// u2_i), the splitmix64 k-gram stream of (seed, context tail of row r),
+// _kernels.pyx:26-41.  Same fp32 arithmetic wherever it is applied (top-k /
+// argmax readers, logit_bias_kernel, the fused lm_head epilogue).
+struct KgBias {
+    const int32_t* tail;
+    int order, stride;
+    uint64_t seed, seed2;
+    float mixw, sharp;
+};
+__device__ __forceinline__ void kg_row_state(const KgBias& b, int r, uint64_t& s1, uint64_t& s2) {
+    s1 = mix64(b.seed + kSeedSalt);
+    s2 = mix64(b.seed2 + kSeedSalt);
+    for (int j = 0; j < b.order; ++j) {
+        const int t = b.tail[(int64_t)r * b.stride + j];
+        if (t < 0) continue;
+        s1 = mix64(s1 ^ mix64((uint64_t)t + 1));
+        s2 = mix64(s2 ^ mix64((uint64_t)t + 1));
+    }
+}
+// bias of token i given its splitmix64 stream offset step = (i + 1) * kGamma
+__device__ __forceinline__ float kg_apply_step(const KgBias& b, float logit, uint64_t step, uint64_t s1, uint64_t s2) {
+    float u = to_unit_f(mix64(s1 + step));
+    if (b.mixw != 0.f) u += b.mixw * to_unit_f(mix64(s2 + step));
+    return logit + b.sharp * u;
+}
+__device__ __forceinline__ float kg_apply(const KgBias& b, float logit, int i, uint64_t s1, uint64_t s2) {
+    return kg_apply_step(b, logit, (uint64_t)(i + 1) * kGamma, s1, s2);
+}
+
+
 // ---------------------------------------------------------------- double-double
 struct dd {
     double hi, lo;

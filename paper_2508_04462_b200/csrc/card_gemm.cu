@@ -202,6 +202,9 @@ struct TcArgs {
     __nv_bfloat16* v_cache;
     int nh, nkv, hd;
     float qscale;
+    // lm_head (EPI_STORE_F32): k-gram logit bias of output row m, vocab id n
+    // (card_linear_fuse_kgram); off when kg.sharp == 0
+    KgBias kg;
 };
 
 // sum over the 16 lanes of a half-warp (all 32 lanes must call)
@@ -220,7 +223,7 @@ __device__ __forceinline__ void sts_f32(uint32_t addr, float v) {
 template <int EPI>
 __device__ __forceinline__ void epi_chunk(const TcArgs& a, int tile, int n_glob, int n_local, int m0, int mc,
                                           float* v, uint32_t xch, const float* invs, const int* tpos,
-                                          const int* tslot, float* xch_ptr, int gbar) {
+                                          const int* tslot, float* xch_ptr, int gbar, const uint64_t* kgs) {
     const float b = a.bias ? a.bias[n_glob] : 0.f;
     if (a.ssq_in)
 #pragma unroll
@@ -310,6 +313,17 @@ __device__ __forceinline__ void epi_chunk(const TcArgs& a, int tile, int n_glob,
         }
         return;
     }
+    if (EPI == EPI_STORE_F32 && a.kg.sharp != 0.f) {
+        // fused k-gram bias: the top-k / argmax readers then skip the hash
+        const uint64_t step = (uint64_t)(n_glob + 1) * kGamma;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            if (j >= mc) break;
+            a.out_f32[(int64_t)(m0 + j) * a.ldo + n_glob] =
+                kg_apply_step(a.kg, v[j] + b, step, kgs[2 * (m0 + j)], kgs[2 * (m0 + j) + 1]);
+        }
+        return;
+    }
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
         if (j >= mc) break;
@@ -343,6 +357,7 @@ __global__ void __launch_bounds__(Roles<NG>::kThreads, 1) tc_gemm_kernel(const _
     float* invs = xch + (a.Mpad > 16 ? 2 : 1) * 16 * 128;   // [256] per-token rsqrt(mean x^2 + eps)
     int* tpos = (int*)(invs + 256);          // [256] QKV: RoPE position of each token row
     int* tslot = tpos + 256;                 // [256] QKV: KV-cache slot of each token row
+    uint64_t* kgs = (uint64_t*)(tslot + 256);   // [256][2] lm_head: k-gram stream state of each output row
 
     const int warp = warp_id(), lane = lane_id();
     if (threadIdx.x == 0) TC_STAMP(0);
@@ -494,6 +509,10 @@ __global__ void __launch_bounds__(Roles<NG>::kThreads, 1) tc_gemm_kernel(const _
             }
             if (!a.ssq_in) named_bar(1, R_::kEpiThreads);
         }
+        if (EPI == EPI_STORE_F32 && a.kg.sharp != 0.f) {
+            for (int m = et; m < M; m += R_::kEpiThreads) kg_row_state(a.kg, m, kgs[2 * m], kgs[2 * m + 1]);
+            if (!a.ssq_in) named_bar(1, R_::kEpiThreads);
+        }
         if (a.ssq_in) {
             // RMSNorm scale of each token row (overlaps the main loop).  T = 8
             // lanes per token each sum a fixed slice of the partials, then a
@@ -553,7 +572,7 @@ __global__ void __launch_bounds__(Roles<NG>::kThreads, 1) tc_gemm_kernel(const _
                 float v[16];
                 tmem_ld16(trow + (uint32_t)m0, v);
                 const int mc = (M - m0) < 16 ? (M - m0) : 16;
-                epi_chunk<EPI>(a, tile, n_glob, n_local, m0, mc, v, smem_u32(gx), invs, tpos, tslot, gx, 2 + grp);
+                epi_chunk<EPI>(a, tile, n_glob, n_local, m0, mc, v, smem_u32(gx), invs, tpos, tslot, gx, 2 + grp, kgs);
             }
             tc_fence_before();
             __syncwarp();
@@ -761,7 +780,9 @@ __global__ void __launch_bounds__(Roles<NG>::kThreads, 1) tc_gemm_kernel(const _
                             vr[qi + half] = __float2bfloat16(x2);
                         }
                     } else if (EPI == EPI_STORE_F32) {
-                        a.out_f32[(int64_t)m * a.ldo + ng0] = x;
+                        a.out_f32[(int64_t)m * a.ldo + ng0] =
+                            a.kg.sharp != 0.f ? kg_apply_step(a.kg, x, (uint64_t)(ng0 + 1) * kGamma, kgs[2 * m], kgs[2 * m + 1])
+                                              : x;
                     } else if (EPI == EPI_RESID_F32) {
                         const float xn = old[q] + x;
                         a.out_f32[(int64_t)m * a.ldo + ng0] = xn;
@@ -1165,7 +1186,7 @@ int card_linear_create(const void* W, int N, int K, int wdtype, const void* X, i
     const int stage_bytes = kTileN * kBK * 2 + Mpad * kBK * 2;
     int budget = (ctas_per_sm == 2 ? 110 : 220) * 1024;
     if (getenv("CARD_GEMM_SMEM_KB")) budget = atoi(getenv("CARD_GEMM_SMEM_KB")) * 1024;   // tuning knob
-    const int extra = 1024 + 64 * 8 + (Mpad > 16 ? 2 : 1) * 16 * 128 * 4 + 3 * 256 * 4 + 64;
+    const int extra = 1024 + 64 * 8 + (Mpad > 16 ? 2 : 1) * 16 * 128 * 4 + 3 * 256 * 4 + 2 * 256 * 8 + 64;
     int stages = (budget - extra) / stage_bytes;
     if (stages > 8) stages = 8;
     if (stages < 2) stages = 2;
@@ -1304,6 +1325,15 @@ int card_linear_fuse_rope(card_linear* h, const int32_t* pos, const int32_t* slo
     a.q_out = q_out;
     a.k_cache = (__nv_bfloat16*)k_cache;
     a.v_cache = (__nv_bfloat16*)v_cache;
+    return CARD_OK;
+}
+
+int card_linear_fuse_kgram(card_linear* h, const int32_t* ctx_tail, int order, int stride, uint64_t seed,
+                           uint64_t seed2, float mix_weight, float sharpness) {
+    if (!h || h->kind != 0 || h->epi != EPI_STORE_F32) return CARD_E_INPUT;
+    if (ctx_tail && (order < 0 || stride < order)) return CARD_E_INPUT;
+    if (h->Mpad > 256) return CARD_E_CONFIG;
+    h->args.kg = KgBias{ctx_tail, order, stride, seed, seed2, mix_weight, ctx_tail ? sharpness : 0.f};
     return CARD_OK;
 }
 

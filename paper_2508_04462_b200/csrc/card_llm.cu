@@ -495,31 +495,8 @@ __global__ void attn_combine_kernel(const int32_t* dM, const int32_t* __restrict
 // (seed, context tail of row r), _kernels.pyx:26-41.  Applied on the fly by
 // the top-k / argmax readers (one read of the logits instead of a separate
 // read-modify-write pass); same fp32 arithmetic as logit_bias_kernel.
-struct KgBias {
-    const int32_t* tail;
-    int order, stride;
-    uint64_t seed, seed2;
-    float mixw, sharp;
-};
-__device__ __forceinline__ void kg_row_state(const KgBias& b, int r, uint64_t& s1, uint64_t& s2) {
-    s1 = mix64(b.seed + kSeedSalt);
-    s2 = mix64(b.seed2 + kSeedSalt);
-    for (int j = 0; j < b.order; ++j) {
-        const int t = b.tail[(int64_t)r * b.stride + j];
-        if (t < 0) continue;
-        s1 = mix64(s1 ^ mix64((uint64_t)t + 1));
-        s2 = mix64(s2 ^ mix64((uint64_t)t + 1));
-    }
-}
-// bias of token i given its splitmix64 stream offset step = (i + 1) * kGamma
-__device__ __forceinline__ float kg_apply_step(const KgBias& b, float logit, uint64_t step, uint64_t s1, uint64_t s2) {
-    float u = to_unit_f(mix64(s1 + step));
-    if (b.mixw != 0.f) u += b.mixw * to_unit_f(mix64(s2 + step));
-    return logit + b.sharp * u;
-}
-__device__ __forceinline__ float kg_apply(const KgBias& b, float logit, int i, uint64_t s1, uint64_t s2) {
-    return kg_apply_step(b, logit, (uint64_t)(i + 1) * kGamma, s1, s2);
-}
+// KgBias, kg_row_state and kg_apply live in card_common.cuh (shared with the
+// lm_head GEMM epilogue, card_linear_fuse_kgram).
 
 // ---------------------------------------------------------------- lm_head epilogues (split over the vocab)
 // Stage 1: CTA (row, split) scans a vocab slice: online max / sum-exp and a

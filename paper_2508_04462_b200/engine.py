@@ -28,6 +28,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 import time
 from dataclasses import asdict, dataclass, field
 from typing import Sequence
@@ -293,12 +294,31 @@ class _LlamaAdapter:
             self.prefill_rows.set_chain(chunk, s)
             self.rt.forward(self.prefill_rows, PREFILL_CHUNK)
 
+    def _fused_lm_head(self):
+        """The bf16 tcgen05 lm_head of the draft plan (None on the fp32 path)."""
+        if os.environ.get("CARD_NO_FUSED_KGRAM"):   # A/B knob: bias in the top-k reader instead
+            return None
+        lm = self.rt.plans[self.rows_max].get("lm_head") if self.rt.fused else None
+        return lm if lm is not None and lm.info["kind"] == 0 else None
+
     def draft(self, run):
         rows = run.drt.rows
-        self.rt.forward(rows, self.rows_max)
+        bias = self._bias_args(run.drt)
+        lm = self._fused_lm_head() if bias[6] != 0.0 else None
+        if lm is not None:
+            # the k-gram bias rides in the lm_head epilogue (set for this launch
+            # only: the plan is shared by every run of this model)
+            raise_for_status(lib().card_linear_fuse_kgram(lm.h, *bias), "fuse_kgram")
+        try:
+            self.rt.forward(rows, self.rows_max)
+        finally:
+            if lm is not None:
+                raise_for_status(lib().card_linear_fuse_kgram(lm.h, None, 0, 0, 0, 0, 0.0, 0.0), "fuse_kgram")
+        if lm is not None:
+            bias = (None, 0, 0, 0, 0, 0.0, 0.0)
         raise_for_status(lib().card_topk_logits(ptr(self.rt.logits), ptr(rows.n_out), self.rows_max, self.V, self.k,
                                                 1.0 / run.t_score, ptr(self.tok), ptr(self.logp), ptr(self.cnt),
-                                                ptr(self.lm_work), *self._bias_args(run.drt), stream_ptr()),
+                                                ptr(self.lm_work), *bias, stream_ptr()),
                          "topk_logits")
         return self.tok, self.logp, self.cnt, 0
 

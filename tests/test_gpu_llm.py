@@ -302,3 +302,37 @@ def test_session_reuse_equals_fresh_runs(card, mode, temperature):
     t.eos_token = d.eos_token = fresh[0].output[5]
     res = card.run_speculative(d, t, prompts[0], cfg, use_graphs=True)
     assert len(t._card_sessions) == 2 and res.output[-1] == t.eos_token
+
+
+def test_lm_head_fused_kgram_bias_is_bit_identical(card):
+    """card_linear_fuse_kgram: the lm_head epilogue adds the k-gram logit bias
+    with the same fp32 arithmetic as card_logit_bias applied afterwards."""
+    from paper_2508_04462_b200._device import ptr, stream_ptr
+    from paper_2508_04462_b200._lib import lib
+    from paper_2508_04462_b200.llama import RowBlock
+    from paper_2508_04462_b200.lm import LogitBias
+
+    bias = LogitBias(seed=11, order=2, sharpness=4000.0)
+    d, t, *_ = _tiny_pair(card, "bf16", "small-target", "small-draft", bias=bias)
+    m = 24
+    rt = d.runtime(256, 64, {m})
+    assert rt.fused
+    V = d.cfg.vocab_size
+    rows = RowBlock(m, 16, rt.dev)
+    rows.set_chain([int(x) for x in np.random.default_rng(3).integers(0, V, m)], 100, out_last_only=False)
+    tail = torch.randint(0, V, (m, 2), dtype=torch.int32, device="cuda", generator=torch.Generator("cuda").manual_seed(5))
+    tail[3, 0] = -1   # a short context
+    rt.forward(rows, m)
+    want = rt.logits[:m].clone()
+    raise_for_status = card.errors.raise_for_status
+    raise_for_status(lib().card_logit_bias(ptr(want), ptr(rows.n_out), m, V, ptr(tail), 2, 2, 11, 131, 0.0, 4000.0,
+                                           stream_ptr()), "logit_bias")
+    lm = rt.plans[m]["lm_head"]
+    raise_for_status(lib().card_linear_fuse_kgram(lm.h, ptr(tail), 2, 2, 11, 131, 0.0, 4000.0), "fuse")
+    rt.forward(rows, m)
+    raise_for_status(lib().card_linear_fuse_kgram(lm.h, None, 0, 0, 0, 0, 0.0, 0.0), "fuse off")
+    torch.cuda.synchronize()
+    assert torch.equal(rt.logits[:m], want)
+    rt.forward(rows, m)   # and off again
+    torch.cuda.synchronize()
+    assert not torch.equal(rt.logits[:m], want)

@@ -78,11 +78,15 @@ def bench_model(name, preset, m_rows, ctx_len):
     wk = torch.zeros(L.card_lmhead_work_floats(m_rows, 3), dtype=torch.float32, device="cuda")
     t_topk = timeit(lambda: L.card_topk_logits(ptr(rt.logits), ptr(dM), m_rows, c.vocab_size, 3, 1.0, ptr(tok),
                                                 ptr(lp), ptr(cnt), ptr(wk), None, 0, 0, 0, 0, 0.0, 0.0, stream_ptr()))
+    tail = torch.randint(0, c.vocab_size, (m_rows, 2), dtype=torch.int32, device="cuda")
+    t_topk_b = timeit(lambda: L.card_topk_logits(ptr(rt.logits), ptr(dM), m_rows, c.vocab_size, 3, 1.0, ptr(tok),
+                                                  ptr(lp), ptr(cnt), ptr(wk), ptr(tail), 2, 2, 11, 131, 0.0, 1e6,
+                                                  stream_ptr()))
     am = torch.zeros(m_rows, dtype=torch.int32, device="cuda")
     t_am = timeit(lambda: L.card_argmax_logits(ptr(rt.logits), ptr(dM), m_rows, c.vocab_size, ptr(am), ptr(wk),
                                                 None, 0, 0, 0, 0, 0.0, 0.0, stream_ptr()))
     print(f"  attention {t_att*1e3:.1f} us  rmsnorm {t_norm*1e3:.1f} us  rope {t_rope*1e3:.1f} us  "
-          f"topk {t_topk*1e3:.1f} us  argmax {t_am*1e3:.1f} us")
+          f"topk {t_topk*1e3:.1f} us (k-gram biased {t_topk_b*1e3:.1f} us)  argmax {t_am*1e3:.1f} us")
     t_fwd = timeit(lambda: rt.forward(rows, m_rows), reps=5)
     g = torch.cuda.CUDAGraph()
     st = torch.cuda.Stream()
