@@ -201,6 +201,18 @@ int card_linear_fuse_rope(card_linear* h, const int32_t* pos, const int32_t* slo
  * bias (bit-identical logits).  ctx_tail == NULL turns it off. */
 int card_linear_fuse_kgram(card_linear* h, const int32_t* ctx_tail, int order, int stride, uint64_t seed,
                            uint64_t seed2, float mix_weight, float sharpness);
+/* fuse_topk: an EPI_TOPK (5) lm_head (pre-tiled bf16 weights) stores no
+ * logits.  For every output row m and 128-token vocab tile t it writes the
+ * record out[(m * (N/128) + t) * 10] = [max, sum exp(x - max), (x, token) x 4]
+ * over x = logit * inv_temp (k-gram bias first, if fused; tokens >= V are
+ * padding and skipped).  card_lmhead_topk_merge combines the records into the
+ * rows_topk result (fused lm_head + softmax + top-k). */
+int card_linear_fuse_topk(card_linear* h, int V, float inv_temp);
+/* Merge the EPI_TOPK records of rows [0, *dM): fp64 log-sum-exp over the
+ * n_tiles tiles and the top-k (k <= 4) by (value desc, token asc); out_logp =
+ * value - lse (same output contract as card_topk_logits). */
+int card_lmhead_topk_merge(const float* work, const int32_t* dM, int m_max, int n_tiles, int k, int V,
+                           int32_t* out_tok, double* out_logp, int32_t* out_cnt, void* stream);
 /* tuning: per-CTA %globaltimer stamps [grid][16] (NULL disables) */
 int card_linear_trace(card_linear* h, unsigned long long* trace);
 int card_linear_destroy(card_linear* h);

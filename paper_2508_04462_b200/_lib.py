@@ -62,6 +62,8 @@ SIGNATURES = {
     "card_linear_fuse_rope": (c_int, [_P, _P, _P, _P, _P, c_int, c_int, c_int, _P, _P, _P]),
     "card_linear_fuse_kgram": (c_int, [_P, _P, c_int, c_int, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_float,
                                        ctypes.c_float]),
+    "card_linear_fuse_topk": (c_int, [_P, c_int, ctypes.c_float]),
+    "card_lmhead_topk_merge": (c_int, [_P, _P, c_int, c_int, c_int, c_int, _P, _P, _P, _P]),
     "card_linear_destroy": (c_int, [_P]),
     "card_embed": (c_int, [_P, _P, c_int, _P, c_int, c_int, _P, _P, _P, c_int, _P]),
     "card_rmsnorm": (c_int, [_P, _P, c_int, ctypes.c_float, _P, c_int, _P, _P, c_int, _P]),
@@ -111,7 +113,7 @@ LAUNCHES = {
     "card_cache_reset": 2, "card_cache_clear": 3, "card_cache_expand": 2, "card_cache_expand_topk": 1, "card_cache_pool": 2,
     "card_cache_query": 1, "card_cache_correct": 1, "card_cache_advance_root": 1, "card_cache_count_alive": 1,
     "card_cache_clear_status": 1, "card_embed": 1, "card_rmsnorm": 1, "card_rope_kv": 1, "card_attention": lambda a: 1 if (a[10] == 0 and a[17] == 0 and a[13] in (64, 128) and a[4] and _attn_fits(a)) else 3,
-    "card_topk_logits": 2, "card_argmax_logits": 2, "card_softmax64": 1, "card_logit_bias": 1,
+    "card_topk_logits": 2, "card_lmhead_topk_merge": 1, "card_argmax_logits": 2, "card_softmax64": 1, "card_logit_bias": 1,
     "card_draft_rows": 1, "card_target_rows": 1, "card_eos_fix": 1, "card_record_width": 1,
     "card_verify_argmax": 1, "card_verify_probs": 1, "card_commit": 1, "card_draft_promote": 2,
     "card_kv_compact": 2, "card_cycle_end": 1, "card_engine_handoff": 1,

@@ -202,9 +202,12 @@ struct TcArgs {
     __nv_bfloat16* v_cache;
     int nh, nkv, hd;
     float qscale;
-    // lm_head (EPI_STORE_F32): k-gram logit bias of output row m, vocab id n
-    // (card_linear_fuse_kgram); off when kg.sharp == 0
+    // lm_head (EPI_STORE_F32 / EPI_TOPK): k-gram logit bias of output row m,
+    // vocab id n (card_linear_fuse_kgram); off when kg.sharp == 0
     KgBias kg;
+    // EPI_TOPK: vocab size (rows >= V are padding) and 1 / temperature
+    int topk_V;
+    float inv_temp;
 };
 
 // sum over the 16 lanes of a half-warp (all 32 lanes must call)
@@ -293,6 +296,85 @@ __device__ __forceinline__ void epi_chunk(const TcArgs& a, int tile, int n_glob,
             const float u = up ? mine : other;
             if (jb + jj < mc) a.out_bf16[(int64_t)(m0 + jb + jj) * a.ldo + f] = __float2bfloat16(silu(g) * u);
         }
+        return;
+    }
+    if (EPI == EPI_TOPK) {
+        // the group's 16-token x 128-vocab chunk, transposed through xch
+        // ([16][128] fp32): 8 threads per token each scan 16 vocab rows
+        // (online max / sum-exp and a sorted top-4 by (value desc, token asc)),
+        // then merge over the 8 lanes; lane 0 writes the (row, tile) record
+        // that card_lmhead_topk_merge combines over the tiles.
+        const bool live = n_glob < a.topk_V;
+        const uint64_t step = (uint64_t)(n_glob + 1) * kGamma;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            float x = v[j] + b;
+            if (a.kg.sharp != 0.f && j < mc) x = kg_apply_step(a.kg, x, step, kgs[2 * (m0 + j)], kgs[2 * (m0 + j) + 1]);
+            sts_f32(xch + (uint32_t)((j * 128 + n_local) * 4), (live && j < mc) ? x * a.inv_temp : -INFINITY);
+        }
+        named_bar(gbar, kGroupThreads);
+        const int jt = n_local >> 3, sub = n_local & 7, rot = (n_local >> 3) & 3;
+        float mx = -INFINITY, sum = 0.f;
+        float tv[kTopkKT];
+        int tt[kTopkKT];
+#pragma unroll
+        for (int q = 0; q < kTopkKT; ++q) {
+            tv[q] = -INFINITY;
+            tt[q] = 0x7fffffff;
+        }
+        auto insert = [&](float cv, int ci) {
+#pragma unroll
+            for (int q = 0; q < kTopkKT; ++q) {
+                const bool bt = cv > tv[q] || (cv == tv[q] && ci < tt[q]);
+                const float ov = tv[q];
+                const int oi = tt[q];
+                tv[q] = bt ? cv : ov;
+                tt[q] = bt ? ci : oi;
+                cv = bt ? ov : cv;
+                ci = bt ? oi : ci;
+            }
+        };
+#pragma unroll 4
+        for (int q = 0; q < 16; ++q) {
+            const int r = sub + 8 * ((q + rot) & 15);   // rotated: the 32 lanes hit 32 banks
+            const float x = lds_f32(xch + (uint32_t)((jt * 128 + r) * 4));
+            if (x == -INFINITY) continue;
+            if (x > mx) {
+                sum = sum * __expf(mx - x) + 1.f;
+                mx = x;
+            } else {
+                sum += __expf(x - mx);
+            }
+            insert(x, tile * kTileN + r);
+        }
+#pragma unroll
+        for (int o = 1; o < 8; o <<= 1) {
+            const float omx = __shfl_xor_sync(0xffffffffu, mx, o);
+            const float osum = __shfl_xor_sync(0xffffffffu, sum, o);
+            const float nm = fmaxf(mx, omx);
+            sum = (mx == -INFINITY ? 0.f : sum * __expf(mx - nm)) + (omx == -INFINITY ? 0.f : osum * __expf(omx - nm));
+            mx = nm;
+            float ov[kTopkKT];
+            int ot[kTopkKT];
+#pragma unroll
+            for (int q = 0; q < kTopkKT; ++q) {
+                ov[q] = __shfl_xor_sync(0xffffffffu, tv[q], o);
+                ot[q] = __shfl_xor_sync(0xffffffffu, tt[q], o);
+            }
+#pragma unroll
+            for (int q = 0; q < kTopkKT; ++q) insert(ov[q], ot[q]);
+        }
+        if (sub == 0 && jt < mc) {
+            float* rec = a.out_f32 + ((int64_t)(m0 + jt) * a.n_tiles + tile) * kTopkRec;
+            rec[0] = mx;
+            rec[1] = sum;
+#pragma unroll
+            for (int q = 0; q < kTopkKT; ++q) {
+                rec[2 + 2 * q] = tv[q];
+                rec[3 + 2 * q] = __int_as_float(tt[q]);
+            }
+        }
+        named_bar(gbar, kGroupThreads);
         return;
     }
     if (EPI == EPI_RESID_F32) {
@@ -509,7 +591,7 @@ __global__ void __launch_bounds__(Roles<NG>::kThreads, 1) tc_gemm_kernel(const _
             }
             if (!a.ssq_in) named_bar(1, R_::kEpiThreads);
         }
-        if (EPI == EPI_STORE_F32 && a.kg.sharp != 0.f) {
+        if ((EPI == EPI_STORE_F32 || EPI == EPI_TOPK) && a.kg.sharp != 0.f) {
             for (int m = et; m < M; m += R_::kEpiThreads) kg_row_state(a.kg, m, kgs[2 * m], kgs[2 * m + 1]);
             if (!a.ssq_in) named_bar(1, R_::kEpiThreads);
         }
@@ -585,7 +667,7 @@ __global__ void __launch_bounds__(Roles<NG>::kThreads, 1) tc_gemm_kernel(const _
             }
         }
     }
-    if (CL) {
+    if (CL && EPI != EPI_TOPK) {   // (the top-k lm_head is never split: card_linear_create)
         // split-K over the cluster (S = a.cluster ranks = the K-slices of one
         // tile).  Tile rows are grouped in pair blocks of P rows (P = 128
         // plain, 16 SwiGLU gate/up, hd/2 RoPE): rank r owns Pp = P/S rows of
@@ -1127,6 +1209,12 @@ int card_linear_create(const void* W, int N, int K, int wdtype, const void* X, i
     else a.out_f32 = (float*)out;
     const bool tiled = (wdtype == 2);
     if (tiled) a.w_tiled = (const uint8_t*)W;
+    a.topk_V = N;
+    a.inv_temp = 1.f;
+    if (epi == EPI_TOPK && !tiled) {   // tcgen05 path only (pre-tiled bf16 weights)
+        free(h);
+        return CARD_E_CONFIG;
+    }
     if (wdtype == 1) {   // fp32 parity path
         h->kind = 2;
         a.out_f32 = (float*)out;
@@ -1203,6 +1291,7 @@ int card_linear_create(const void* W, int N, int K, int wdtype, const void* X, i
         case EPI_STORE_BF16: e = set_tc_attr<EPI_STORE_BF16>(h->smem); break;
         case EPI_SWIGLU_BF16: e = set_tc_attr<EPI_SWIGLU_BF16>(h->smem); break;
         case EPI_QKV_ROPE: e = set_tc_attr<EPI_QKV_ROPE>(h->smem); break;
+        case EPI_TOPK: e = set_tc_attr<EPI_TOPK>(h->smem); break;
         default: free(h); return CARD_E_CONFIG;
     }
     if (e != cudaSuccess) {
@@ -1218,6 +1307,7 @@ int card_linear_create(const void* W, int N, int K, int wdtype, const void* X, i
         case EPI_STORE_BF16: S = choose_cluster<EPI_STORE_BF16>(a.n_tiles, a.kb_total, Mpad, slots, h->smem, stage_smem, ctas_per_sm); break;
         case EPI_SWIGLU_BF16: S = choose_cluster<EPI_SWIGLU_BF16>(a.n_tiles, a.kb_total, Mpad, slots, h->smem, stage_smem, ctas_per_sm); break;
         case EPI_QKV_ROPE: S = choose_cluster<EPI_QKV_ROPE>(a.n_tiles, a.kb_total, Mpad, slots, h->smem, stage_smem, ctas_per_sm); break;
+        case EPI_TOPK: S = 1; break;
     }
     if (S > 1 && (kTileN % S != 0 || (Mpad > 16 ? 1 : 2) * (size_t)kTileN * (Mpad + 4) * 4 > (size_t)stage_smem)) {
         free(h);
@@ -1250,6 +1340,7 @@ int card_linear_run(card_linear* h, const int32_t* dM, void* stream) {
             case EPI_STORE_BF16: e = launch_tc<EPI_STORE_BF16>(h, a, s); break;
             case EPI_SWIGLU_BF16: e = launch_tc<EPI_SWIGLU_BF16>(h, a, s); break;
             case EPI_QKV_ROPE: e = launch_tc<EPI_QKV_ROPE>(h, a, s); break;
+            case EPI_TOPK: e = launch_tc<EPI_TOPK>(h, a, s); break;
         }
         if (e != cudaSuccess) {
             set_cuda_error(e);
@@ -1330,10 +1421,17 @@ int card_linear_fuse_rope(card_linear* h, const int32_t* pos, const int32_t* slo
 
 int card_linear_fuse_kgram(card_linear* h, const int32_t* ctx_tail, int order, int stride, uint64_t seed,
                            uint64_t seed2, float mix_weight, float sharpness) {
-    if (!h || h->kind != 0 || h->epi != EPI_STORE_F32) return CARD_E_INPUT;
+    if (!h || h->kind != 0 || (h->epi != EPI_STORE_F32 && h->epi != EPI_TOPK)) return CARD_E_INPUT;
     if (ctx_tail && (order < 0 || stride < order)) return CARD_E_INPUT;
     if (h->Mpad > 256) return CARD_E_CONFIG;
     h->args.kg = KgBias{ctx_tail, order, stride, seed, seed2, mix_weight, ctx_tail ? sharpness : 0.f};
+    return CARD_OK;
+}
+
+int card_linear_fuse_topk(card_linear* h, int V, float inv_temp) {
+    if (!h || h->kind != 0 || h->epi != EPI_TOPK || V <= 0 || V > h->N) return CARD_E_INPUT;
+    h->args.topk_V = V;
+    h->args.inv_temp = inv_temp;
     return CARD_OK;
 }
 

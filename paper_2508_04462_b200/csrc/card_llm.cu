@@ -1020,6 +1020,15 @@ int card_topk_logits(const float* logits, const int32_t* dM, int m_max, int V, i
     return CARD_OK;
 }
 
+int card_lmhead_topk_merge(const float* work, const int32_t* dM, int m_max, int n_tiles, int k, int V,
+                           int32_t* out_tok, double* out_logp, int32_t* out_cnt, void* stream) {
+    if (k < 1 || k > kTopkKT || n_tiles < 1) return CARD_E_CONFIG;
+    CARD_PDL((topk_merge_kernel<kTopkKT>), dim3((m_max + 7) / 8), dim3(256), 0, (cudaStream_t)stream, dM, n_tiles, k, V,
+             work, out_tok, out_logp, out_cnt);
+    CARD_LAUNCH_CHECK();
+    return CARD_OK;
+}
+
 int card_argmax_logits(const float* logits, const int32_t* dM, int m_max, int V, int32_t* out, float* work,
                        const int32_t* ctx_tail, int order, int stride, uint64_t seed, uint64_t seed2, float mix_weight,
                        float sharpness, void* stream) {

@@ -23,7 +23,10 @@ enum {
     EPI_STORE_BF16 = 2,
     EPI_SWIGLU_BF16 = 3,
     EPI_QKV_ROPE = 4,   // RoPE + q scale + KV-cache write (card_linear_fuse_rope)
+    EPI_TOPK = 5,       // lm_head: per (row, 128-token vocab tile) top-4 + max / sum-exp records
 };
+constexpr int kTopkKT = 4;                  // candidates per (row, vocab tile) record
+constexpr int kTopkRec = 2 + 2 * kTopkKT;   // [max, sum, (value, token) x KT] floats
 
 // Per-forward row descriptors written by the row builders (card_engine.cu)
 // and consumed by the model kernels (card_llm.cu).  Device memory.

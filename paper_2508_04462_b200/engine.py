@@ -301,9 +301,27 @@ class _LlamaAdapter:
         lm = self.rt.plans[self.rows_max].get("lm_head") if self.rt.fused else None
         return lm if lm is not None and lm.info["kind"] == 0 else None
 
+    def _topk_head(self):
+        """The fused lm_head + softmax + top-k linear (bf16 path, k <= 4)."""
+        if os.environ.get("CARD_NO_FUSED_TOPK") or self.k > 4:   # A/B knob: logits + top-k reader
+            return None
+        return self.rt.lm_topk_head(self.rows_max)
+
     def draft(self, run):
         rows = run.drt.rows
         bias = self._bias_args(run.drt)
+        head = self._topk_head()
+        if head is not None:
+            # SURVEY a13: the lm_head epilogue reduces every 128-token vocab
+            # tile to a top-4 + (max, sum-exp) record; no logits are stored
+            L_ = lib()
+            raise_for_status(L_.card_linear_fuse_kgram(head.h, *bias), "fuse_kgram")
+            raise_for_status(L_.card_linear_fuse_topk(head.h, self.V, 1.0 / run.t_score), "fuse_topk")
+            self.rt.forward(rows, self.rows_max, topk=True)
+            raise_for_status(L_.card_lmhead_topk_merge(ptr(head.work), ptr(rows.n_out), self.rows_max, head.n_tiles,
+                                                       self.k, self.V, ptr(self.tok), ptr(self.logp), ptr(self.cnt),
+                                                       stream_ptr()), "lmhead_topk_merge")
+            return self.tok, self.logp, self.cnt, 0
         lm = self._fused_lm_head() if bias[6] != 0.0 else None
         if lm is not None:
             # the k-gram bias rides in the lm_head epilogue (set for this launch

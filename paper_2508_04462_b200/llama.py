@@ -30,7 +30,8 @@ from ._device import ptr, require_cuda, stream_ptr
 from ._lib import lib
 from .errors import ConfigError, raise_for_status
 
-EPI_STORE_F32, EPI_RESID_F32, EPI_STORE_BF16, EPI_SWIGLU_BF16, EPI_QKV_ROPE = 0, 1, 2, 3, 4
+EPI_STORE_F32, EPI_RESID_F32, EPI_STORE_BF16, EPI_SWIGLU_BF16, EPI_QKV_ROPE, EPI_TOPK = 0, 1, 2, 3, 4, 5
+TOPK_REC = 10   # floats per (row, vocab tile) record of an EPI_TOPK lm_head (csrc/card_llm.h kTopkRec)
 
 
 @dataclass
@@ -374,6 +375,8 @@ class DeviceLlama:
             P_["qkv"].fuse_rope(rows, self.cos, self.sin, c.n_heads, c.n_kv_heads, c.head_dim, self.q,
                                 self.k_cache[li], self.v_cache[li])
         plan["lm_head"].fuse_norm(self.ssq, c.hidden // 16, self.mpad, c.rms_eps, c.hidden, rows.out_rows)
+        if "lm_head_topk" in plan:
+            plan["lm_head_topk"].fuse_norm(self.ssq, c.hidden // 16, self.mpad, c.rms_eps, c.hidden, rows.out_rows)
         plan["bound_rows"] = key
 
     def kv_row_elems(self) -> int:
@@ -383,15 +386,18 @@ class DeviceLlama:
         return 2 if self.dtype == "bf16" else 4
 
     # ------------------------------------------------------------ forward
-    def forward(self, rows: "RowBlock", m_max: int):
+    def forward(self, rows: "RowBlock", m_max: int, topk: bool = False):
         """Run the forward over the device rows; logits for the output rows
-        land in self.logits[:n_out].  Asynchronous, graph-capturable."""
+        land in self.logits[:n_out] (topk=True: the lm_head_topk records
+        instead, see lm_topk_head).  Asynchronous, graph-capturable."""
         c = self.cfg
         L_ = lib()
         s = stream_ptr()
         plan = self.plans[m_max]
         if self.fused:
-            return self._forward_fused(rows, plan)
+            return self._forward_fused(rows, plan, topk)
+        if topk:
+            raise ConfigError("the fused top-k lm_head needs the bf16 path")
         dM, dOut = rows.M, rows.n_out
         hd = c.head_dim
         mm = plan["m_max"]   # grids sized for this plan's rows (rows >= M exit at once)
@@ -418,7 +424,24 @@ class DeviceLlama:
                             ptr(self.hf), self.code, s), "final norm")
         plan["lm_head"].run(dOut)
 
-    def _forward_fused(self, rows: "RowBlock", plan: dict):
+    def lm_topk_head(self, m_max: int):
+        """The fused lm_head + softmax + top-k linear of plan m_max (bf16 path;
+        None on the fp32 path): EPI_TOPK records instead of logits, merged by
+        card_lmhead_topk_merge.  Built on first use."""
+        if not self.fused:
+            return None
+        plan = self.plans[m_max]
+        lin = plan.get("lm_head_topk")
+        if lin is None:
+            n_tiles = self.lm_head.shape[0] if self.lm_head.dim() == 4 else self.lm_head.shape[0] // 128
+            work = torch.zeros(m_max * n_tiles * TOPK_REC, dtype=torch.float32, device=self.dev)
+            lin = _Linear(self.lm_head, self.xb, m_max, EPI_TOPK, work, 0)
+            lin.work, lin.n_tiles = work, n_tiles
+            plan["lm_head_topk"] = lin
+            plan["bound_rows"] = None   # rebind the row offset of the new head
+        return lin
+
+    def _forward_fused(self, rows: "RowBlock", plan: dict, topk: bool = False):
         c = self.cfg
         L_ = lib()
         s = stream_ptr()
@@ -437,7 +460,7 @@ class DeviceLlama:
             P["o"].run(dM)
             P["gu"].run(dM)
             P["d"].run(dM)
-        plan["lm_head"].run(rows.n_out)
+        plan["lm_head_topk" if topk else "lm_head"].run(rows.n_out)
 
     def launches_per_forward(self) -> int:
         gu_extra = 0

@@ -336,3 +336,42 @@ def test_lm_head_fused_kgram_bias_is_bit_identical(card):
     rt.forward(rows, m)   # and off again
     torch.cuda.synchronize()
     assert not torch.equal(rt.logits[:m], want)
+
+
+@pytest.mark.parametrize("m", [1, 24, 116])
+@pytest.mark.parametrize("sharp,temp", [(0.0, 1.0), (4000.0, 1.0), (4000.0, 0.8)])
+def test_fused_lm_head_topk_matches_logits_path(card, m, sharp, temp):
+    """the EPI_TOPK lm_head (per vocab-tile top-4 + sum-exp records,
+    card_lmhead_topk_merge) returns the tokens of the logits + top-k reader
+    path, and the same log-probs up to the fp32 partial-sum order."""
+    from paper_2508_04462_b200._device import ptr, stream_ptr
+    from paper_2508_04462_b200._lib import lib
+    from paper_2508_04462_b200.llama import RowBlock
+    from paper_2508_04462_b200.lm import LogitBias
+
+    d, t, *_ = _tiny_pair(card, "bf16", "small-target", "small-draft", bias=LogitBias(seed=11, order=2, sharpness=sharp))
+    rt = d.runtime(256, 64, {m})
+    V, k = d.cfg.vocab_size, 3
+    rows = RowBlock(m, 16, rt.dev)
+    rows.set_chain([int(x) for x in np.random.default_rng(m).integers(0, V, m)], 100, out_last_only=False)
+    g = torch.Generator("cuda").manual_seed(m + 1)
+    tail = torch.randint(0, V, (m, 2), dtype=torch.int32, device="cuda", generator=g)
+    bias = (ptr(tail), 2, 2, 11, 131, 0.0, sharp) if sharp else (None, 0, 0, 0, 0, 0.0, 0.0)
+    chk = card.errors.raise_for_status
+    L = lib()
+    out = [(torch.zeros((m, k), dtype=torch.int32, device="cuda"), torch.zeros((m, k), dtype=torch.float64, device="cuda"),
+            torch.zeros(m, dtype=torch.int32, device="cuda")) for _ in range(2)]
+    rt.forward(rows, m)
+    wk = torch.zeros(L.card_lmhead_work_floats(m, k), dtype=torch.float32, device="cuda")
+    chk(L.card_topk_logits(ptr(rt.logits), ptr(rows.n_out), m, V, k, 1.0 / temp, ptr(out[0][0]), ptr(out[0][1]),
+                           ptr(out[0][2]), ptr(wk), *bias, stream_ptr()), "topk_logits")
+    head = rt.lm_topk_head(m)
+    chk(L.card_linear_fuse_kgram(head.h, *bias), "fuse_kgram")
+    chk(L.card_linear_fuse_topk(head.h, V, 1.0 / temp), "fuse_topk")
+    rt.forward(rows, m, topk=True)
+    chk(L.card_lmhead_topk_merge(ptr(head.work), ptr(rows.n_out), m, head.n_tiles, k, V, ptr(out[1][0]),
+                                 ptr(out[1][1]), ptr(out[1][2]), stream_ptr()), "merge")
+    torch.cuda.synchronize()
+    assert torch.equal(out[1][0], out[0][0])
+    assert torch.equal(out[1][2], out[0][2])
+    assert (out[1][1] - out[0][1]).abs().max().item() < 2e-5
