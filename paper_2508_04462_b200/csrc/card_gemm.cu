@@ -322,7 +322,7 @@ __device__ __forceinline__ void epi_chunk(const TcArgs& a, int tile, int n_glob,
             tv[q] = -INFINITY;
             tt[q] = 0x7fffffff;
         }
-        auto insert = [&](float cv, int ci) {
+        auto insert = [&](float cv, int ci) {   // branch-free sorted insertion
 #pragma unroll
             for (int q = 0; q < kTopkKT; ++q) {
                 const bool bt = cv > tv[q] || (cv == tv[q] && ci < tt[q]);
@@ -334,19 +334,19 @@ __device__ __forceinline__ void epi_chunk(const TcArgs& a, int tile, int n_glob,
                 ci = bt ? oi : ci;
             }
         };
-#pragma unroll 4
-        for (int q = 0; q < 16; ++q) {
-            const int r = sub + 8 * ((q + rot) & 15);   // rotated: the 32 lanes hit 32 banks
-            const float x = lds_f32(xch + (uint32_t)((jt * 128 + r) * 4));
-            if (x == -INFINITY) continue;
-            if (x > mx) {
-                sum = sum * __expf(mx - x) + 1.f;
-                mx = x;
-            } else {
-                sum += __expf(x - mx);
-            }
-            insert(x, tile * kTileN + r);
-        }
+        // branch-free scan (divergent per-element branches dominated the
+        // stalls): all 16 loads, the local max, the sum-exp, then insertion
+        float xs[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q)   // rotated rows: the 32 lanes hit 32 banks
+            xs[q] = lds_f32(xch + (uint32_t)((jt * 128 + sub + 8 * ((q + rot) & 15)) * 4));
+#pragma unroll
+        for (int q = 0; q < 16; ++q) mx = fmaxf(mx, xs[q]);
+#pragma unroll
+        for (int q = 0; q < 16; ++q) sum += xs[q] == -INFINITY ? 0.f : __expf(xs[q] - mx);
+#pragma unroll
+        for (int q = 0; q < 16; ++q)
+            insert(xs[q], xs[q] == -INFINITY ? 0x7fffffff : tile * kTileN + sub + 8 * ((q + rot) & 15));
 #pragma unroll
         for (int o = 1; o < 8; o <<= 1) {
             const float omx = __shfl_xor_sync(0xffffffffu, mx, o);

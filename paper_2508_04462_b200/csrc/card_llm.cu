@@ -988,6 +988,117 @@ static int vocab_splits(int m_max) {
     return s < 1 ? 1 : (s > 64 ? 64 : s);
 }
 
+}  // extern "C"
+
+namespace card {
+// Merge of the EPI_TOPK lm_head records of one row (one CTA per row; the
+// ~1000 records of a row are spread over the threads so every load is
+// independent): fp64 log-sum-exp, then k rounds of block arg-best over the
+// per-thread sorted top-4 lists.
+__global__ void __launch_bounds__(256) tiles_merge_kernel(const int32_t* dM, int S, int k, int V,
+                                                          const float* __restrict__ work, int32_t* __restrict__ out_tok,
+                                                          double* __restrict__ out_logp, int32_t* __restrict__ out_cnt) {
+    pdl_wait();
+    pdl_trigger();
+    const int r = blockIdx.x;
+    if (r >= *dM) return;
+    const float* base = work + (int64_t)r * S * kTopkRec;
+    __shared__ double sh_d[8];
+    __shared__ float sh_v[8];
+    __shared__ int sh_t[8], sh_w[8];
+    float tv[kTopkKT];
+    int tt[kTopkKT];
+#pragma unroll
+    for (int q = 0; q < kTopkKT; ++q) {
+        tv[q] = -INFINITY;
+        tt[q] = 0x7fffffff;
+    }
+    float lm = -INFINITY;
+    for (int s = threadIdx.x; s < S; s += blockDim.x) {
+        const float* p = base + (int64_t)s * kTopkRec;
+        lm = fmaxf(lm, p[0]);
+#pragma unroll
+        for (int c = 0; c < kTopkKT; ++c) {
+            float cv = p[2 + 2 * c];
+            int ci = __float_as_int(p[3 + 2 * c]);
+#pragma unroll
+            for (int q = 0; q < kTopkKT; ++q) {
+                const bool bt = lbefore(cv, ci, tv[q], tt[q]);
+                const float ov = tv[q];
+                const int oi = tt[q];
+                tv[q] = bt ? cv : ov;
+                tt[q] = bt ? ci : oi;
+                cv = bt ? ov : cv;
+                ci = bt ? oi : ci;
+            }
+        }
+    }
+    // block max of the record maxima
+    for (int o = 16; o > 0; o >>= 1) lm = fmaxf(lm, __shfl_xor_sync(0xffffffffu, lm, o));
+    if (lane_id() == 0) sh_v[warp_id()] = lm;
+    __syncthreads();
+    float gmf = sh_v[0];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) gmf = fmaxf(gmf, sh_v[w]);
+    const double gm = (double)gmf;
+    double tot = 0.0;
+    for (int s = threadIdx.x; s < S; s += blockDim.x) {
+        const float* p = base + (int64_t)s * kTopkRec;
+        if (p[1] > 0.f) tot += (double)p[1] * exp((double)p[0] - gm);
+    }
+    for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+    if (lane_id() == 0) sh_d[warp_id()] = tot;
+    __syncthreads();
+    double T = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) T += sh_d[w];
+    const double lse = gm + log(T);
+    int head = 0;
+    for (int round = 0; round < k; ++round) {
+        float v = -INFINITY;
+        int t = 0x7fffffff;
+#pragma unroll
+        for (int q = 0; q < kTopkKT; ++q)
+            if (q == head) {
+                v = tv[q];
+                t = tt[q];
+            }
+        int who = threadIdx.x;
+        for (int o = 16; o > 0; o >>= 1) {
+            const float ov = __shfl_xor_sync(0xffffffffu, v, o);
+            const int ot = __shfl_xor_sync(0xffffffffu, t, o);
+            const int ow = __shfl_xor_sync(0xffffffffu, who, o);
+            if (lbefore(ov, ot, v, t)) {
+                v = ov;
+                t = ot;
+                who = ow;
+            }
+        }
+        __syncthreads();
+        if (lane_id() == 0) {
+            sh_v[warp_id()] = v;
+            sh_t[warp_id()] = t;
+            sh_w[warp_id()] = who;
+        }
+        __syncthreads();
+        float bv = sh_v[0];
+        int bt = sh_t[0], bw = sh_w[0];
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
+            if (lbefore(sh_v[w], sh_t[w], bv, bt)) {
+                bv = sh_v[w];
+                bt = sh_t[w];
+                bw = sh_w[w];
+            }
+        if (threadIdx.x == bw) ++head;
+        if (threadIdx.x == 0) {
+            out_tok[(int64_t)r * k + round] = bt;
+            out_logp[(int64_t)r * k + round] = (double)bv - lse;
+        }
+    }
+    if (threadIdx.x == 0) out_cnt[r] = k < V ? k : V;
+}
+}  // namespace card
+
+extern "C" {
+
 int card_lmhead_work_floats(int m_max, int k) { return m_max * vocab_splits(m_max) * (2 + 2 * 8); }
 
 int card_topk_logits(const float* logits, const int32_t* dM, int m_max, int V, int k, double inv_temp,
@@ -1023,8 +1134,8 @@ int card_topk_logits(const float* logits, const int32_t* dM, int m_max, int V, i
 int card_lmhead_topk_merge(const float* work, const int32_t* dM, int m_max, int n_tiles, int k, int V,
                            int32_t* out_tok, double* out_logp, int32_t* out_cnt, void* stream) {
     if (k < 1 || k > kTopkKT || n_tiles < 1) return CARD_E_CONFIG;
-    CARD_PDL((topk_merge_kernel<kTopkKT>), dim3((m_max + 7) / 8), dim3(256), 0, (cudaStream_t)stream, dM, n_tiles, k, V,
-             work, out_tok, out_logp, out_cnt);
+    CARD_PDL((tiles_merge_kernel), dim3(m_max), dim3(256), 0, (cudaStream_t)stream, dM, n_tiles, k, V, work, out_tok,
+             out_logp, out_cnt);
     CARD_LAUNCH_CHECK();
     return CARD_OK;
 }

@@ -302,8 +302,12 @@ class _LlamaAdapter:
         return lm if lm is not None and lm.info["kind"] == 0 else None
 
     def _topk_head(self):
-        """The fused lm_head + softmax + top-k linear (bf16 path, k <= 4)."""
-        if os.environ.get("CARD_NO_FUSED_TOPK") or self.k > 4:   # A/B knob: logits + top-k reader
+        """The fused lm_head + softmax + top-k linear (bf16 path, k <= 4), opt-in
+        with CARD_FUSED_TOPK=1.  Measured slower than logits + top-k reader at
+        M = 116 (217 + 14 us vs 115 + 52 us, tools/topk_probe.py): its
+        per-element insertion chains run at two warps per scheduler and do
+        not hide under the weight stream."""
+        if not os.environ.get("CARD_FUSED_TOPK") or self.k > 4:
             return None
         return self.rt.lm_topk_head(self.rows_max)
 
