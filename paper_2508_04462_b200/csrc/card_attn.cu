@@ -366,24 +366,23 @@ __global__ void __launch_bounds__(QT * 2) attn_fused_kernel(const float* __restr
     at_stamp(5);
     cl_sync();   // every partial has landed in its owner's smem
     at_stamp(6);
-    // owner merge: query-heads [rank*QO, rank*QO + QO), S partials in rank
-    // order.  Per query-head weights w_s / L first (one thread each), then
-    // every output element is S independent loads.
+    // owner merge: query-heads [rank*QO, rank*QO + QO), S partials.  The
+    // weights w_s / L take one thread per (query-head, partial): QO * S = QT
+    // threads, the S lanes of a query-head reduce by shuffles (S divides 32;
+    // a fixed tree, the same for every M).  Then every output element is S
+    // independent loads.
     __shared__ float s_w[QT][16];
-    if (threadIdx.x < QO) {
-        const int ql = threadIdx.x;
-        float Mx = -INFINITY;
-        for (int s = 0; s < S; ++s) Mx = fmaxf(Mx, recv[(s * QO + ql) * PW]);
+    if (threadIdx.x < QT) {
+        const int ql = threadIdx.x / S, s = threadIdx.x - ql * S;
+        const float* rec = recv + (s * QO + ql) * PW;
+        const float m_s = rec[0], l_s = rec[1];
+        float Mx = m_s;
+        for (int o = 1; o < S; o <<= 1) Mx = fmaxf(Mx, __shfl_xor_sync(0xffffffffu, Mx, o));
         const float Ms = Mx == -INFINITY ? 0.f : Mx;
-        float L = 0.f;
-        for (int s = 0; s < S; ++s) {
-            const float* rec = recv + (s * QO + ql) * PW;
-            const float w = rec[0] == -INFINITY ? 0.f : __expf(rec[0] - Ms);
-            s_w[ql][s] = w;
-            L += w * rec[1];
-        }
-        const float invL = L > 0.f ? 1.0f / L : 0.f;
-        for (int s = 0; s < S; ++s) s_w[ql][s] *= invL;
+        const float w = m_s == -INFINITY ? 0.f : __expf(m_s - Ms);
+        float L = w * l_s;
+        for (int o = 1; o < S; o <<= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
+        s_w[ql][s] = L > 0.f ? w * (1.0f / L) : 0.f;
     }
     __syncthreads();
     // two adjacent dims per thread (8-byte smem loads, bf16x2 stores); the
