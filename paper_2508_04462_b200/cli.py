@@ -1,6 +1,5 @@
-"""Front end (the `run` and `ablate` commands of the reference CLI,
-/root/reference/pkg/src/specache/cli.py:174-203, 259-294), over the device
-engine.  Inputs and outputs keep the reference formats:
+"""Front end (the `run`, `sweep` and `ablate` commands of the reference CLI,
+/root/reference/pkg/src/specache/cli.py:174-294), over the device engine.  Inputs and outputs keep the reference formats:
 
 * models JSON (lm.py:438-464, plus ``"type": "llama"`` entries);
 * engine config JSON (EngineConfig fields; ``"ratio": "auto"`` resolves from
@@ -27,6 +26,7 @@ from .errors import ConfigError, CorpusFormatError, SpecacheError
 from .lm import load_models_file
 from .metrics import aggregate
 
+SWEEP_PARAMS = {"K": int, "ratio": int, "k": int, "query_depth": int, "temperature": float}   # cli.py:21
 COLUMNS = (("tokens", "tokens_emitted", "{:d}"), ("time", "sim_time", "{:.2f}"),
            ("fwd_t", "target_forwards", "{:d}"), ("fwd_d", "draft_forwards", "{:d}"),
            ("hit%", "cache_hit_rate", "{:.3f}"), ("lnew", "mean_acceptance_length", "{:.3f}"),
@@ -139,6 +139,48 @@ def cmd_run(args) -> int:
     return 0
 
 
+def parse_sweep(spec: str) -> tuple[str, list]:
+    """``param=v1,v2,...`` (cli.py:235-256)."""
+    if "=" not in spec:
+        raise ConfigError(f"--sweep must look like param=v1,v2,... got {spec!r}")
+    name, _, tail = spec.partition("=")
+    name = name.strip()
+    if name not in SWEEP_PARAMS:
+        raise ConfigError(f"cannot sweep {name!r}; choose one of {sorted(SWEEP_PARAMS)}")
+    values = []
+    for part in (p.strip() for p in tail.split(",")):
+        if not part:
+            continue
+        try:
+            values.append(SWEEP_PARAMS[name](part))
+        except ValueError as e:
+            raise ConfigError(f"bad sweep value {part!r} for {name}: {e}") from e
+    if not values:
+        raise ConfigError(f"--sweep {name} needs at least one value")
+    return name, values
+
+
+def cmd_sweep(args) -> int:
+    """The corpus once per value of one engine parameter (cli.py:206-232)."""
+    draft, target, raw, overrides, corpus = _setup(args)
+    name, values = parse_sweep(args.sweep)
+    records, rows = [], []
+    for value in values:
+        cfg = engine_config(raw, draft, target, {**overrides, name: value})
+        per = []
+        for rid, prompt in corpus:
+            res = run_speculative(draft, target, prompt, cfg)
+            per.append(res.metrics)
+            records.append({"id": rid, name: value, "config": cfg.to_dict(), "metrics": res.metrics.to_dict()})
+        total = aggregate(per)
+        records.append({"id": "__aggregate__", name: value, "metrics": total.to_dict()})
+        rows.append([f"{name}={value}"] + _cells(total))
+    if args.out:
+        _dump(args.out, records)
+    print(_table(f"sweep {name}  prompts={len(corpus)}", rows, name))
+    return 0
+
+
 def cmd_ablate(args) -> int:
     """Vanilla AR vs the cache without correction vs the full protocol
     (Table 3; cli.py:259-294)."""
@@ -165,6 +207,7 @@ def build_parser() -> argparse.ArgumentParser:
                                  description="CARD query-and-correct decoding on B200 (drop-in for specache).")
     sub = ap.add_subparsers(dest="command", required=True)
     for name, fn, hlp in (("run", cmd_run, "decode every prompt once"),
+                          ("sweep", cmd_sweep, "rerun the corpus across parameter values"),
                           ("ablate", cmd_ablate, "vanilla vs cache-only vs cache-plus-correction")):
         p = sub.add_parser(name, help=hlp)
         p.add_argument("--models", required=True, help="models JSON file")
@@ -175,6 +218,9 @@ def build_parser() -> argparse.ArgumentParser:
         p.add_argument("--seed", type=int, help="override the run seed")
         if name == "run":
             p.add_argument("--trace", help="write per-step trace records to this JSONL file")
+        if name == "sweep":
+            p.add_argument("--sweep", required=True, metavar="param=v1,v2,...",
+                           help=f"one of {sorted(SWEEP_PARAMS)} and its values")
         p.set_defaults(func=fn)
     return ap
 

@@ -84,3 +84,32 @@ def test_cli_run_and_ablate_on_device(tmp_path, capsys):
     ab = {r["variant"]: r["metrics"] for r in map(json.loads, open(out))}
     assert ab["vanilla"]["mean_acceptance_length"] == 1.0
     assert ab["cache_plus_correct"]["mean_acceptance_length"] >= ab["cache_only"]["mean_acceptance_length"] > 1.0
+
+
+def test_sweep_spec_parsing():
+    """--sweep param=v1,v2 (cli.py:235-256 of the reference)."""
+    from paper_2508_04462_b200.cli import parse_sweep
+    from paper_2508_04462_b200.errors import ConfigError
+
+    assert parse_sweep("K=8, 16,") == ("K", [8, 16])
+    assert parse_sweep("temperature=0,1.5") == ("temperature", [0.0, 1.5])
+    for bad in ("K", "seed=1,2", "K=a", "ratio="):
+        with pytest.raises(ConfigError):
+            parse_sweep(bad)
+
+
+@pytest.mark.gpu
+def test_cli_sweep_on_device(tmp_path):
+    """sweep: one record per (prompt, value) plus an aggregate per value; each
+    record equals a direct run at that value."""
+    import paper_2508_04462_b200 as card
+    from paper_2508_04462_b200.cli import main
+
+    m, c, cfg = _files(tmp_path, ['{"id": "p0", "tokens": [1, 2, 3]}'], {"K": 16, "k": 3, "ratio": 5, "max_new_tokens": 30})
+    out = str(tmp_path / "sweep.jsonl")
+    assert main(["sweep", "--models", m, "--corpus", c, "--config", cfg, "--out", out, "--sweep", "K=4,16"]) == 0
+    recs = [json.loads(x) for x in open(out)]
+    assert [(r["id"], r["K"]) for r in recs] == [("p0", 4), ("__aggregate__", 4), ("p0", 16), ("__aggregate__", 16)]
+    draft, target = card.load_models_file(m)
+    want = card.run_speculative(draft, target, [1, 2, 3], card.EngineConfig(K=4, k=3, ratio=5, max_new_tokens=30))
+    assert recs[0]["metrics"] == want.metrics.to_dict()
