@@ -568,11 +568,49 @@ __global__ void __launch_bounds__(256) topk_partial_kernel(const float* __restri
                     consume(kg_apply_step(kb, q[u].y, st + kGamma, ks1, ks2) * inv_temp, i + 1);
                     consume(kg_apply_step(kb, q[u].z, st + 2 * kGamma, ks1, ks2) * inv_temp, i + 2);
                     consume(kg_apply_step(kb, q[u].w, st + 3 * kGamma, ks1, ks2) * inv_temp, i + 3);
-                } else {
-                    consume(q[u].x * inv_temp, i);
-                    consume(q[u].y * inv_temp, i + 1);
-                    consume(q[u].z * inv_temp, i + 2);
-                    consume(q[u].w * inv_temp, i + 3);
+                }
+            }
+            if (!biased) {
+                // batch of 16: one max-rescale per batch, independent exps,
+                // insertion only for values that beat the current k-th best
+                float xs[16];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    xs[4 * u] = q[u].x * inv_temp;
+                    xs[4 * u + 1] = q[u].y * inv_temp;
+                    xs[4 * u + 2] = q[u].z * inv_temp;
+                    xs[4 * u + 3] = q[u].w * inv_temp;
+                }
+                float bm = xs[0];
+#pragma unroll
+                for (int e = 1; e < 16; ++e) bm = fmaxf(bm, xs[e]);
+                if (bm > mx) {
+                    sum = mx == -INFINITY ? 0.f : sum * __expf(mx - bm);
+                    mx = bm;
+                }
+                float part = 0.f;
+#pragma unroll
+                for (int e = 0; e < 16; ++e) part += xs[e] == -INFINITY ? 0.f : __expf(xs[e] - mx);
+                sum += part;
+                if (bm >= tv[KT - 1]) {
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) {
+                        const int i = lo + 4 * (vi + (e >> 2) * blockDim.x) + (e & 3);
+                        if (lbefore(xs[e], i, tv[KT - 1], tt[KT - 1])) {
+                            float cv = xs[e];
+                            int ci = i;
+#pragma unroll
+                            for (int j = 0; j < KT; ++j) {
+                                const bool b = lbefore(cv, ci, tv[j], tt[j]);
+                                const float ov = tv[j];
+                                const int oi = tt[j];
+                                tv[j] = b ? cv : ov;
+                                tt[j] = b ? ci : oi;
+                                cv = b ? ov : cv;
+                                ci = b ? oi : ci;
+                            }
+                        }
+                    }
                 }
             }
         }
