@@ -282,6 +282,44 @@ def measure_roofline(target, rows_max, ctx_len, peak):
             "isolated_frac": round(nbytes / (iso_t * 1e-3) / 1e9 / peak, 4)}
 
 
+def measure_draft(draft, rows_max, ctx_len, peak):
+    """The draft forward of a full-width tree step (rows_max = K + max_depth + 2
+    rows), graph-replayed: the step the speedup is bound by.
+    Reported beside the roofline, at the draft's own weight bytes."""
+    import numpy as np
+    import torch
+
+    from paper_2508_04462_b200.llama import RowBlock
+
+    rt = draft._runtime
+    if rows_max not in rt.plans:
+        return {}
+    rows = RowBlock(rows_max, 16, rt.dev)
+    toks = [int(x) for x in np.random.default_rng(6).integers(0, draft.cfg.vocab_size, rows_max)]
+    rows.set_chain(toks, ctx_len - rows_max, out_last_only=False)
+    plan = rt.plans[rows_max]
+    nbytes = sum(L[k].nbytes for L in plan["layers"] for k in ("qkv", "o", "gu", "d")) + plan["lm_head"].nbytes
+    rt.forward(rows, rows_max)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    st = torch.cuda.Stream()
+    st.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(st), torch.cuda.graph(g, stream=st):
+        rt.forward(rows, rows_max)
+    torch.cuda.current_stream().wait_stream(st)
+    g.replay()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(5):
+        g.replay()
+    b.record()
+    b.synchronize()
+    t = a.elapsed_time(b) / 5
+    return {"draft_forward_ms": round(t, 3), "draft_rows": rows_max,
+            "draft_forward_frac": round(nbytes / (t * 1e-3) / 1e9 / peak, 4)}
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -365,6 +403,7 @@ def main():
         lossless = None   # sampled tokens differ by design; losslessness is distributional (tests)
     ar_value = ar_tok / (ar_ms / 1000.0)
     roof = measure_roofline(target, args.ratio + 1, args.prompt_len + args.new_tokens // 2, peak)
+    roof.update(measure_draft(draft, args.K + 2 * args.ratio + 2, args.prompt_len + args.new_tokens // 2, peak))
     tr = traffic_from_profiles()
     if tr:
         roof["traffic"] = tr.get("bytes_per_launch")
