@@ -334,26 +334,44 @@ __device__ __forceinline__ void epi_chunk(const TcArgs& a, int tile, int n_glob,
                 ci = bt ? oi : ci;
             }
         };
-        // branch-free scan (divergent per-element branches dominated the
-        // stalls): all 16 loads, the local max, the sum-exp, then insertion
+        // The tile's top-4 are all >= T, the 4th largest of the 8 lanes'
+        // maxima (those are 4 distinct elements), so each lane inserts only
+        // its elements >= T (a handful per tile).  The sum-exp is taken
+        // against the tile max directly (no rescaling chain).
         float xs[16];
 #pragma unroll
         for (int q = 0; q < 16; ++q)   // rotated rows: the 32 lanes hit 32 banks
             xs[q] = lds_f32(xch + (uint32_t)((jt * 128 + sub + 8 * ((q + rot) & 15)) * 4));
+        float lm = xs[0];
 #pragma unroll
-        for (int q = 0; q < 16; ++q) mx = fmaxf(mx, xs[q]);
+        for (int q = 1; q < 16; ++q) lm = fmaxf(lm, xs[q]);
+        float tmx = lm;
 #pragma unroll
-        for (int q = 0; q < 16; ++q) sum += xs[q] == -INFINITY ? 0.f : __expf(xs[q] - mx);
+        for (int o = 1; o < 8; o <<= 1) tmx = fmaxf(tmx, __shfl_xor_sync(0xffffffffu, tmx, o));
+        float s = 0.f;
+#pragma unroll
+        for (int q = 0; q < 16; ++q) s += xs[q] == -INFINITY ? 0.f : __expf(xs[q] - tmx);
+#pragma unroll
+        for (int o = 1; o < 8; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        mx = tmx;
+        sum = s;
+        // rank of this lane's max among the 8 (ties: lower lane first)
+        int rnk = 0;
+#pragma unroll
+        for (int o = 1; o < 8; ++o) {
+            const float om = __shfl_xor_sync(0xffffffffu, lm, o);
+            rnk += (om > lm || (om == lm && (sub ^ o) < sub)) ? 1 : 0;
+        }
+        const unsigned hit = __ballot_sync(0xffffffffu, rnk == kTopkKT - 1);
+        const int lane_id_ = n_local & 31;
+        const unsigned grpmask = 0xffu << (lane_id_ & 24);
+        const int src = __ffs(hit & grpmask) - 1;
+        const float T = __shfl_sync(0xffffffffu, lm, src);
 #pragma unroll
         for (int q = 0; q < 16; ++q)
-            insert(xs[q], xs[q] == -INFINITY ? 0x7fffffff : tile * kTileN + sub + 8 * ((q + rot) & 15));
+            if (xs[q] >= T && xs[q] != -INFINITY) insert(xs[q], tile * kTileN + sub + 8 * ((q + rot) & 15));
 #pragma unroll
         for (int o = 1; o < 8; o <<= 1) {
-            const float omx = __shfl_xor_sync(0xffffffffu, mx, o);
-            const float osum = __shfl_xor_sync(0xffffffffu, sum, o);
-            const float nm = fmaxf(mx, omx);
-            sum = (mx == -INFINITY ? 0.f : sum * __expf(mx - nm)) + (omx == -INFINITY ? 0.f : osum * __expf(omx - nm));
-            mx = nm;
             float ov[kTopkKT];
             int ot[kTopkKT];
 #pragma unroll
