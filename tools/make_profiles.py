@@ -48,7 +48,7 @@ def summary(recs, metric="gpu__time_duration.sum"):
 p = os.path.join(SRC, "launches_card.csv")
 if os.path.exists(p):
     recs = launch_rows(p, "gpu__time_duration.sum")
-    txt = ("# ncu launch list: tools/profile_steps.py (CARD K=100 k=3 r=7, agreement knob s=1e6, 32 new tokens incl. prefill + graph capture, then run_vanilla AR; model init and a warm-up request excluded via --profile-from-start off)\n"
+    txt = ("# ncu launch list: tools/profile_steps.py (CARD K=100 k=3 r=7, agreement knob s=1e6, 32 new tokens incl. prefill (CUDA graphs reused from the warm-up request's serving session), then run_vanilla AR; model init and the warm-up request excluded via --profile-from-start off)\n"
            "# ncu --metrics gpu__time_duration.sum --clock-control none  (per-launch times are cold-cache and\n"
            "# serialised: compare SHARES of the step, not absolute times)\n" + summary(recs))
     open(os.path.join(DST, f"{tag}_launches_card.txt"), "w").write(txt + "\n")
