@@ -281,6 +281,14 @@ int card_verify_argmax(card_engine_state* E, const int32_t* cand, const int32_t*
 int card_verify_probs(card_engine_state* E, const int32_t* cand, const double* probs, int V,
                       const double* qcond, const double* uniforms, void* stream);
 int card_commit(card_engine_state* E, int32_t* committed, void* stream);
+/* Outcome of the last verify + commit (replaces the return of
+ * verify.py:65-132 and the rollback the reference leaves implicit in
+ * engine.py:247-262): out = device int32[6] {accepted prefix
+ * n, correction token, uniforms consumed (the host advances its PCG64 by
+ * this), kv_keep (target KV rows [0, kv_keep) stay valid = C_prev + n for an
+ * unclipped commit), KV rows rolled back (L - n unclipped), tokens
+ * committed}. */
+int card_verify_result(const card_engine_state* E, int32_t* out, void* stream);
 /* KV rollback / roll-forward of the draft: promote accepted-chain tree KV
  * rows into the prefix; move surviving tree rows after an arena compaction. */
 int card_draft_promote(card_engine_state* E, card_cache* h, void** k_layers, void** v_layers,

@@ -67,8 +67,9 @@ class RefLlama:
         x1, x2 = x[..., :h], x[..., h:]
         return torch.cat([x1 * cos - x2 * sin, x2 * cos + x1 * sin], dim=-1)
 
-    def _extend(self, new_tokens: list[int]) -> torch.Tensor:
-        """Append tokens to the cached stream; returns logits [n_new, V]."""
+    def _extend(self, new_tokens: list[int], out: str = "all") -> torch.Tensor | None:
+        """Append tokens to the cached stream; returns logits [n_new, V]
+        (out="all"), of the last token only [1, V] ("last"), or None."""
         c = self.cfg
         n0 = len(self.tokens)
         n = len(new_tokens)
@@ -106,8 +107,12 @@ class RefLlama:
             gg = h @ self.w[p + "wg"].T
             uu = h @ self.w[p + "wu"].T
             x = x + (torch.nn.functional.silu(gg) * uu) @ self.w[p + "wd"].T
-        x = self._rms(x, self.w["norm"])
         self.tokens.extend(int(t) for t in new_tokens)
+        if out == "none":
+            return None
+        if out == "last":
+            x = x[-1:]
+        x = self._rms(x, self.w["norm"])
         return x @ self.w["lm_head"].T
 
     def logits_for(self, context: list[int]) -> torch.Tensor:
@@ -121,7 +126,7 @@ class RefLlama:
             c -= 1
         self.tokens = self.tokens[:c]
         self.kv = [(k[:c], v[:c]) for k, v in self.kv]
-        return self._extend(ctx[c:])[-1]
+        return self._extend(ctx[c:], "last")[-1]
 
     def full_logits(self, tokens: list[int]) -> torch.Tensor:
         self.tokens, self.kv = [], []

@@ -89,6 +89,7 @@ SIGNATURES = {
     "card_verify_argmax": (c_int, [_P, _P, _P, _P]),
     "card_verify_probs": (c_int, [_P, _P, _P, c_int, _P, _P, _P]),
     "card_commit": (c_int, [_P, _P, _P]),
+    "card_verify_result": (c_int, [_P, _P, _P]),
     "card_draft_promote": (c_int, [_P, _P, _P, _P, c_int, c_int, c_int, c_int, c_int, _P]),
     "card_kv_compact": (c_int, [_P, _P, _P, _P, c_int, c_int, c_int, c_int, _P, c_int, _P]),
     "card_cycle_end": (c_int, [_P, _P, _P]),
@@ -104,7 +105,8 @@ class EngineState(ctypes.Structure):
         "rec_acc", "rec_lnew", "cursor", "n_uni", "base_len", "C_prev", "order", "sampling",
         "rec_n_widths", "rec_hit", "rec_L", "rec_n_acc", "rec_corr", "rec_done", "n_commit", "anchor_origin")] + [
         ("widths", c_int32 * 64), ("rec_widths", c_int32 * 64), ("acc", c_int32 * 64),
-        ("committed_now", c_int32 * 72), ("rec_depth", c_int32), ("rec_alive", c_int32), ("spare", c_int32 * 6)]
+        ("committed_now", c_int32 * 72), ("rec_depth", c_int32), ("rec_alive", c_int32), ("kv_keep", c_int32), ("kv_drop", c_int32),
+        ("consumed", c_int32), ("cursor_prev", c_int32), ("spare", c_int32 * 2)]
 
 
 # kernels launched per C-ABI call (for the bench's gpu_launches count)
@@ -115,7 +117,7 @@ LAUNCHES = {
     "card_cache_clear_status": 1, "card_embed": 1, "card_rmsnorm": 1, "card_rope_kv": 1, "card_attention": lambda a: 1 if (a[10] == 0 and a[17] == 0 and a[13] in (64, 128) and a[4] and _attn_fits(a)) else 3,
     "card_topk_logits": 2, "card_lmhead_topk_merge": 1, "card_argmax_logits": 2, "card_softmax64": 1, "card_logit_bias": 1,
     "card_draft_rows": 1, "card_target_rows": 1, "card_eos_fix": 1, "card_record_width": 1,
-    "card_verify_argmax": 1, "card_verify_probs": 1, "card_commit": 1, "card_draft_promote": 2,
+    "card_verify_argmax": 1, "card_verify_probs": 1, "card_commit": 1, "card_verify_result": 1, "card_draft_promote": 2,
     "card_kv_compact": 2, "card_cycle_end": 1, "card_engine_handoff": 1,
 }
 launch_count = [0]

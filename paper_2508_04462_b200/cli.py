@@ -189,12 +189,13 @@ def cmd_ablate(args) -> int:
     for variant in ("vanilla", "cache_only", "cache_plus_correct"):
         cfg = engine_config({**raw, "correction_enabled": variant != "cache_only"}, draft, target, overrides)
         per = []
-        for _, prompt in corpus:
+        for rid, prompt in corpus:
             res = run_vanilla(target, prompt, cfg) if variant == "vanilla" else \
                 run_speculative(draft, target, prompt, cfg, use_graphs=False)
             per.append(res.metrics)
+            records.append({"id": rid, "variant": variant, "metrics": res.metrics.to_dict()})
         total = aggregate(per)
-        records.append({"variant": variant, "config": cfg.to_dict(), "metrics": total.to_dict()})
+        records.append({"id": "__aggregate__", "variant": variant, "metrics": total.to_dict()})
         rows.append([variant] + _cells(total))
     if args.out:
         _dump(args.out, records)

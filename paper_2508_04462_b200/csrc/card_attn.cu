@@ -428,7 +428,6 @@ static cudaError_t launch_qt(cudaLaunchConfig_t& cfg, const float* q, const int3
 }
 
 static int attn_qt(int m_max, int G) {
-    if (getenv("CARD_ATTN_QT")) return atoi(getenv("CARD_ATTN_QT")) == 128 ? 128 : 64;   // tuning knob
     return (m_max * G >= 512) ? 128 : 64;
 }
 
@@ -455,7 +454,6 @@ int launch_attn_fused(const float* q, const int32_t* dM, int m_max, const int32_
     // than 8); the wide draft tree forward is fastest with 4 (measured 4 <
     // 8 < 2 < 16 on the 1B draft at 116 rows)
     int S = QT == 128 ? 4 : n_qt * nkv <= 18 ? 16 : n_qt * nkv <= 37 ? 8 : 4;
-    if (getenv("CARD_ATTN_S")) S = atoi(getenv("CARD_ATTN_S"));   // tuning knob (power of two <= 16)
     while (S > 1 && S > n_ch) S >>= 1;
     const int smem = attn_fused_smem(hd, S, QT);
     cudaLaunchConfig_t cfg = {};

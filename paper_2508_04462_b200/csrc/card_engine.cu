@@ -36,7 +36,11 @@ typedef struct card_engine_state {
     int32_t rec_widths[64];
     int32_t acc[64];
     int32_t committed_now[72];
-    int32_t rec_depth, rec_alive, spare[6];
+    int32_t rec_depth, rec_alive;
+    // target KV rollback of the last verify: KV rows [0, kv_keep)
+    // stay valid, the kv_drop rows written above them are dead; uniforms
+    // the verify consumed (verify.py:104-132 draw order)
+    int32_t kv_keep, kv_drop, consumed, cursor_prev, spare[2];
 } card_engine_state;
 }
 
@@ -193,6 +197,7 @@ __global__ void record_width_kernel(card_engine_state* E, const card_cache_state
 
 // ---------------------------------------------------------------- verification
 __device__ void finish_verify(card_engine_state* E, const int32_t* q_tok, int n, int corr) {
+    E->cursor_prev = E->cursor;
     E->n_acc = n;
     E->corr = corr;
     for (int i = 0; i < n; ++i) E->acc[i] = q_tok[i];
@@ -400,6 +405,12 @@ __global__ void commit_kernel(card_engine_state* E, int32_t* committed) {
     E->done = done;
     E->rec_acc = cnt > 0 ? cnt - 1 : 0;
     E->rec_lnew = cnt;
+    // the verify wrote KV for positions C_prev-1 .. C_prev-1+L (root + L
+    // candidates); the committed root and accepted tokens keep theirs, the
+    // last committed token (the correction) has none yet
+    E->kv_keep = E->C_prev + cnt - 1;
+    E->kv_drop = E->L + 1 - cnt;
+    E->consumed = E->cursor - E->cursor_prev;
     if (!E->anchor_origin) E->base_len = E->C;
 }
 
@@ -601,6 +612,26 @@ int card_verify_probs(card_engine_state* E, const int32_t* cand, const double* p
 
 int card_commit(card_engine_state* E, int32_t* committed, void* stream) {
     commit_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(E, committed);
+    CARD_LAUNCH_CHECK();
+    return CARD_OK;
+}
+
+// the last verify's outcome in the reference's terms: out[0] accepted
+// prefix n, out[1] correction, out[2] uniforms consumed, out[3] kv_keep,
+// out[4] KV rows rolled back, out[5] tokens committed (device int32[6])
+__global__ void verify_result_kernel(const card_engine_state* E, int32_t* out) {
+    if (threadIdx.x != 0) return;
+    out[0] = E->n_acc;
+    out[1] = E->corr;
+    out[2] = E->consumed;
+    out[3] = E->kv_keep;
+    out[4] = E->kv_drop;
+    out[5] = E->n_commit;
+}
+
+int card_verify_result(const card_engine_state* E, int32_t* out, void* stream) {
+    if (!E || !out) return CARD_E_INPUT;
+    verify_result_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(E, out);
     CARD_LAUNCH_CHECK();
     return CARD_OK;
 }

@@ -1164,13 +1164,11 @@ static cudaError_t launch_tc(const card_linear* h, const TcArgs& a, cudaStream_t
 // buffer fits in the freed pipeline stages.
 template <int EPI>
 static int choose_cluster(int n_tiles, int kb_total, int Mpad, int slots, int smem, int stage_smem, int ctas_per_sm) {
-    if (getenv("CARD_NO_CLUSTER") || 2 * n_tiles > slots) return 1;
+    if (2 * n_tiles > slots) return 1;
     int S = 8;
     const size_t red_bytes = (Mpad > 16 ? 1 : 2) * (size_t)kTileN * (Mpad + 4) * 4;   // recv (+ send) regions
     while (S > 1 && (n_tiles * S > slots || S > kb_total || red_bytes > (size_t)stage_smem))
         S >>= 1;
-    if (getenv("CARD_SPLITS")) S = atoi(getenv("CARD_SPLITS"));   // tuning knob (must divide 128)
-    if (getenv("CARD_CLUSTER_FORCE")) return S;   // tuning knob: skip the one-wave occupancy check
     // cudaOccupancyMaxActiveClusters counts one CTA per SM for this kernel even
     // when two fit (measured: 33 clusters of 4 at 105 KB and at 209 KB); with
     // two CTAs per SM the slot count above is the better bound (the verify
@@ -1191,9 +1189,6 @@ static int choose_cluster(int n_tiles, int kb_total, int Mpad, int slots, int sm
         int nc = 0;
         const cudaError_t oe = Mpad > 16 ? cudaOccupancyMaxActiveClusters(&nc, tc_gemm_kernel<EPI, true, 2>, &cfg)
                                          : cudaOccupancyMaxActiveClusters(&nc, tc_gemm_kernel<EPI, true, 1>, &cfg);
-        if (getenv("CARD_CLUSTER_DEBUG"))
-            fprintf(stderr, "choose_cluster: tiles=%d kb=%d Mpad=%d S=%d smem=%d -> max active clusters %d (%s)\n", n_tiles,
-                    kb_total, Mpad, S, smem, nc, cudaGetErrorString(oe));
         if (oe == cudaSuccess && nc >= n_tiles) break;
         cudaGetLastError();
         S >>= 1;
@@ -1288,18 +1283,14 @@ int card_linear_create(const void* W, int N, int K, int wdtype, const void* X, i
     // with the whole shared memory as its ring (measured 0.3 ms faster per
     // draft forward than two CTAs with half the ring each).
     int ctas_per_sm = (cols <= 256 && Mpad < 64) ? 2 : 1;
-    if (getenv("CARD_CTAS_PER_SM")) ctas_per_sm = atoi(getenv("CARD_CTAS_PER_SM"));   // tuning knob
     const int stage_bytes = kTileN * kBK * 2 + Mpad * kBK * 2;
     int budget = (ctas_per_sm == 2 ? 110 : 220) * 1024;
-    if (getenv("CARD_GEMM_SMEM_KB")) budget = atoi(getenv("CARD_GEMM_SMEM_KB")) * 1024;   // tuning knob
     const int extra = 1024 + 64 * 8 + (Mpad > 16 ? 2 : 1) * 16 * 128 * 4 + 3 * 256 * 4 + 2 * 256 * 8 + 64;
     int stages = (budget - extra) / stage_bytes;
     if (stages > 8) stages = 8;
     if (stages < 2) stages = 2;
     a.stages = stages;
-    a.bulk_pieces = 1;
-    if (getenv("CARD_BULK_PIECES")) a.bulk_pieces = atoi(getenv("CARD_BULK_PIECES"));   // tuning knob (1, 2, 4, 8)
-    if (a.bulk_pieces != 2 && a.bulk_pieces != 4 && a.bulk_pieces != 8) a.bulk_pieces = 1;
+    a.bulk_pieces = 1;   // one 16 KB bulk copy per stage (2-8 pieces measured slower)
     h->smem = stages * stage_bytes + extra;
     const int slots = num_sms() * ctas_per_sm;
     cudaError_t e;

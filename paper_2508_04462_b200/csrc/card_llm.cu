@@ -990,7 +990,7 @@ int card_attention(const float* q, const int32_t* dM, int m_max, const int32_t* 
         cudaFuncSetAttribute(attn_prefix_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
         attr = true;
     }
-    if (kvdtype == 0 && odtype == 0 && (hd == 64 || hd == 128) && !getenv("CARD_ATTN_SPLITKV") &&
+    if (kvdtype == 0 && odtype == 0 && (hd == 64 || hd == 128) &&
         attn_fused_fits(m_max, nh, nkv, extra_max))
         if (slot) return launch_attn_fused(q, dM, m_max, plen, slot, n_extra, extra, extra_max, kc, vc, nh, nkv, hd,
                                            max_plen, o, s);

@@ -14,14 +14,7 @@
 namespace card {
 
 static thread_local char g_cuda_err[256] = {0};
-bool pdl_enabled() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("CARD_PDL");
-        v = (e && e[0] == '0') ? 0 : 1;
-    }
-    return v != 0;
-}
+bool pdl_enabled() { return true; }   // programmatic dependent launch on every chained kernel
 void set_cuda_error(cudaError_t e) {
     snprintf(g_cuda_err, sizeof(g_cuda_err), "%s: %s", cudaGetErrorName(e), cudaGetErrorString(e));
 }

@@ -28,7 +28,6 @@ from __future__ import annotations
 
 import ctypes
 import math
-import os
 import time
 from dataclasses import asdict, dataclass, field
 from typing import Sequence
@@ -296,18 +295,13 @@ class _LlamaAdapter:
 
     def _fused_lm_head(self):
         """The bf16 tcgen05 lm_head of the draft plan (None on the fp32 path)."""
-        if os.environ.get("CARD_NO_FUSED_KGRAM"):   # A/B knob: bias in the top-k reader instead
-            return None
         lm = self.rt.plans[self.rows_max].get("lm_head") if self.rt.fused else None
         return lm if lm is not None and lm.info["kind"] == 0 else None
 
     def _topk_head(self):
-        """The fused lm_head + softmax + top-k linear (bf16 path, k <= 4), opt-in
-        with CARD_FUSED_TOPK=1.  Measured slower than logits + top-k reader at
-        M = 116 (217 + 14 us vs 115 + 52 us, tools/topk_probe.py): its
-        per-element insertion chains run at two warps per scheduler and do
-        not hide under the weight stream."""
-        if not os.environ.get("CARD_FUSED_TOPK") or self.k > 4:
+        """The fused lm_head + softmax + top-k linear (bf16 path, k <= 4) when
+        the model asks for it (``LlamaModel.fused_topk``)."""
+        if not getattr(self.m, "fused_topk", False) or self.k > 4:
             return None
         return self.rt.lm_topk_head(self.rows_max)
 
@@ -805,6 +799,11 @@ class _ConcurrentDriver:
         self.replays[0] += 1
         return ev
 
+    def _now(self, t0) -> float:
+        """Trace clock in latency units: wall seconds / time_scale, as the
+        reference's concurrent mode stamps its events (engine.py:330-331)."""
+        return (time.perf_counter() - t0) / self.run.cfg.time_scale
+
     def _draft_done(self, t0):
         """Read the finished draft step's record: width (trace) and stop flag."""
         run = self.run
@@ -812,7 +811,7 @@ class _ConcurrentDriver:
         n = Ed.n_widths
         w = Ed.widths[n - 1] if 0 < n <= 64 else 0
         if w > 0:
-            run._emit(time.perf_counter() - t0, False, w, 0, 0, "draft_expand")
+            run._emit(self._now(t0), False, w, 0, 0, "draft_expand")
         return bool(Ed.stop)
 
     def run_loop(self):
@@ -850,7 +849,7 @@ class _ConcurrentDriver:
                 if d_ev is None and not paused:
                     d_ev = self._draft()
             E = EngineState.from_buffer_copy(run._host.numpy().tobytes())
-            now = time.perf_counter() - t0
+            now = self._now(t0)
             hit = bool(E.rec_hit)
             run.output.extend(E.committed_now[i] for i in range(E.n_commit))
             run._emit_target(now, hit, E)
@@ -868,7 +867,7 @@ class _ConcurrentDriver:
                 q_ev.record(self.D)
             self.replays[3] += 1
             paused = False
-            run._emit(time.perf_counter() - t0, hit, 0, 0, 0, "correct")
+            run._emit(self._now(t0), hit, 0, 0, 0, "correct")
         for dev in {run.dev_d, run.dev_t}:
             torch.cuda.synchronize(dev)
 
@@ -877,10 +876,17 @@ class _ConcurrentDriver:
 
 
 def _validate_run_config(draft, target, config):
-    if config.max_depth > 30:
-        raise ConfigError("max_depth > 30 is not supported by the device tree attention")
+    """Limits of the device engine only (host-table pairs run the reference
+    algorithm on the host and take any depth): the engine state keeps 64
+    accepted tokens per verify (card_engine_state.acc), and the transformer
+    tree attention gathers at most 31 ancestor slots per row."""
+    kinds = {getattr(draft, "engine_kind", "host"), getattr(target, "engine_kind", "host")}
+    if "host" in kinds:
+        return
     if config.query_depth > 62:
-        raise ConfigError("query_depth too large")
+        raise ConfigError(f"query_depth {config.query_depth} > 62: the device engine state holds 64 accepted tokens")
+    if "llama" in kinds and config.max_depth > 30:
+        raise ConfigError(f"max_depth {config.max_depth} > 30 is not supported by the device tree attention")
 
 
 def enable_peer_access(a: int, b: int):

@@ -94,15 +94,24 @@ def verify_sampling(target_dists: Sequence, draft_conditionals: Sequence[float],
     if len(draft_conditionals) != len(candidate):
         raise InputError(f"need one draft conditional per candidate token, got {len(draft_conditionals)} "
                          f"for {len(candidate)}")
-    for i, q in enumerate(draft_conditionals):
-        q = float(q)
-        if not np.isfinite(q) or q <= 0.0:
-            raise ProtocolError(f"draft conditional {q!r} at position {i}: the cache proposed a token it "
-                                f"assigned no probability")
+    # the reference checks a conditional only when the walk reaches its
+    # position (verify.py:104-112): verify up to the first invalid one and
+    # raise only if every position before it was accepted
+    bad = next((i for i, q in enumerate(draft_conditionals) if not np.isfinite(float(q)) or float(q) <= 0.0),
+               None)
+    cand = list(candidate) if bad is None else list(candidate[:bad])
+    dists = list(target_dists) if bad is None else list(target_dists[:bad + 1])
+    qs = [float(q) for q in draft_conditionals[:len(cand)]]
     saved = rng.bit_generator.state
-    uni = rng.random(len(candidate) + 2)
-    acc, corr, used = _run(target_dists, list(candidate), True, q=list(draft_conditionals), uniforms=uni)
+    uni = rng.random(len(cand) + 2)
+    acc, corr, used = _run(dists, cand, True, q=qs, uniforms=uni)
     rng.bit_generator.state = saved
+    if bad is not None and len(acc) == bad:
+        if bad:
+            rng.random(bad)   # the coins of the accepted positions were drawn before the check
+        q = float(draft_conditionals[bad])
+        raise ProtocolError(f"draft conditional {q!r} at position {bad}: the cache proposed a token it "
+                            f"assigned no probability")
     if used:
         rng.random(used)   # advance by exactly what the kernel consumed
     return VerifyOutcome(accepted=acc, correction=corr, accepted_len=len(acc), lnew=len(acc) + 1)

@@ -81,7 +81,11 @@ def test_cli_run_and_ablate_on_device(tmp_path, capsys):
     assert sum(1 for _ in open(trace)) == len(want.trace) + len(
         card.run_speculative(draft, target, [5, 9], card.EngineConfig(K=16, k=3, ratio=5, max_new_tokens=40)).trace)
     assert main(["ablate", "--models", m, "--corpus", c, "--config", cfg, "--out", out]) == 0
-    ab = {r["variant"]: r["metrics"] for r in map(json.loads, open(out))}
+    recs = [json.loads(x) for x in open(out)]
+    # the reference's record shape (cli.py:278-288): per prompt, then an aggregate per variant
+    assert [(r["id"], r["variant"]) for r in recs] == [(i, v) for v in ("vanilla", "cache_only", "cache_plus_correct")
+                                                         for i in ("p0", "p1", "__aggregate__")]
+    ab = {r["variant"]: r["metrics"] for r in recs if r["id"] == "__aggregate__"}
     assert ab["vanilla"]["mean_acceptance_length"] == 1.0
     assert ab["cache_plus_correct"]["mean_acceptance_length"] >= ab["cache_only"]["mean_acceptance_length"] > 1.0
 

@@ -73,3 +73,30 @@ def test_ref_llama_incremental_equals_full():
         assert torch.allclose(inc.logits_for(toks[:n]), full[n - 1], atol=1e-5)
     branch = toks[:20] + [7, 8]
     assert torch.allclose(inc.logits_for(branch), RefLlama(cfg, w).full_logits(branch)[-1], atol=1e-5)
+
+
+def test_safetensors_checkpoint_round_trip_and_hf(tmp_path):
+    """checkpoint.load_llama_safetensors reads what HF save_pretrained writes
+    (HF names, tied and untied heads) and what save_llama_safetensors writes,
+    and the loaded weights give the oracle the same logits."""
+    from paper_2508_04462_b200.checkpoint import load_llama_safetensors, save_llama_safetensors
+    from paper_2508_04462_b200.errors import ConfigError
+    from paper_2508_04462_b200.llama import init_weights
+
+    for which in (0, 1):
+        cfg = _cfgs()[which]
+        w = init_weights(cfg, seed=11 + which)
+        p = tmp_path / f"m{which}.safetensors"
+        save_llama_safetensors(str(p), cfg, w)
+        got = load_llama_safetensors(str(p), cfg)
+        assert set(got) == set(w)
+        assert all(torch.equal(got[k], w[k]) for k in w)
+        d = tmp_path / f"hf{which}"
+        _hf_model(cfg, w).save_pretrained(str(d), safe_serialization=True)
+        hf = load_llama_safetensors(str(d), cfg)
+        toks = list(range(3, 40))
+        assert torch.equal(RefLlama(cfg, hf).full_logits(toks), RefLlama(cfg, w).full_logits(toks))
+    bad = tmp_path / "bad.safetensors"
+    bad.write_bytes(b"\x01\x00")
+    with pytest.raises(ConfigError):
+        load_llama_safetensors(str(bad), _cfgs()[0])
