@@ -141,62 +141,120 @@ def traffic_from_profiles():
 
 
 # ---------------------------------------------------------------- CPU baseline (oracle)
-def cpu_baseline(args, V_cfg):
-    """The CPU oracle (oracle/llama_ref.py + card_oracle) on the host cores:
-    target-only AR decode (engine.py:392-423) of the same random-init target
-    architecture in fp32, a bounded sample under a wall-clock budget."""
-    import numpy as np
-    import torch
+class CpuCard:
+    """The reference's CPU path on the bench workload: the oracle restatement
+    of ``_run_serial`` (engine.py:290-317, oracle/card_oracle.serial_cycles,
+    pinned to the reference's goldens) and ``run_vanilla`` (engine.py:392-423)
+    driving the fp32 CPU transformers (oracle/llama_ref.py) of the same
+    random-init draft/target, agreement bias, prompt and K/k/ratio.  Weights
+    are initialised once; the 512-token prompt is prefilled once (each model
+    keeps a KV-cached token stream, so every tree path and verify chain
+    reuses the prompt's KV: the prefix memo of SURVEY §8d).  A sample is one
+    CARD cycle (<= ratio draft layers of <= K tree rows + one verify)."""
 
-    from oracle import card_oracle as O
-    from oracle.llama_ref import RefModel
-    from paper_2508_04462_b200.llama import PRESETS, init_weights
+    def __init__(self, args):
+        import torch
 
-    cores = os.cpu_count() or 1
-    torch.set_num_threads(cores)
-    cfg = PRESETS[args.target]
-    w = init_weights(cfg, seed=2, device="cpu", dtype=torch.float32)
-    model = RefModel(cfg, w, forward_latency=1.0)
-    prompt = [int(x) for x in np.random.default_rng(1000).integers(0, cfg.vocab_size, 16)]
-    t0 = time.perf_counter()
-    ctx = list(prompt)
-    n = 0
-    model.next_distribution(ctx)           # prompt prefill (not counted)
-    t1 = time.perf_counter()
-    while time.perf_counter() - t1 < args.cpu_seconds:
-        d = model.next_distribution(ctx)
-        ctx.append(O.argmax_token(d))
-        n += 1
-    dt = time.perf_counter() - t1
-    del w, model
-    return {"value": n / dt, "unit": UNIT, "cores": cores, "kind": "port",
-            "sample": f"oracle run_vanilla of random-init {args.target} (fp32 torch CPU, KV-cached), 16-token prompt, "
-                      f"{n} tokens decoded in {dt:.1f} s (prefill {t1 - t0:.1f} s excluded); the CPU CARD loop at "
-                      f"K={args.K} is slower per token (100-row draft tree forwards)"}
+        from oracle import card_oracle as O
+        from oracle.llama_ref import RefModel
+        from paper_2508_04462_b200.llama import PRESETS, init_weights
+        from paper_2508_04462_b200.lm import LogitBias
+
+        self.cores = os.cpu_count() or 1
+        torch.set_num_threads(self.cores)
+        bias = LogitBias(seed=11, order=2, sharpness=args.bias_sharpness, mix_seed=131, mix_weight=args.bias_mix)
+        tcfg, dcfg = PRESETS[args.target], PRESETS[args.draft]
+        t0 = time.perf_counter()
+        self.target = RefModel(tcfg, init_weights(tcfg, seed=2), forward_latency=7.0, bias=bias)
+        self.draft = RefModel(dcfg, init_weights(dcfg, seed=1), forward_latency=1.0, bias=bias)
+        self.init_s = time.perf_counter() - t0
+        self.prompt = prompts(1, tcfg.vocab_size, args.prompt_len)[0]
+        t0 = time.perf_counter()
+        for m in (self.target, self.draft):
+            m.llama._extend(self.prompt[:-1], "none")
+        self.prefill_s = time.perf_counter() - t0
+        self.args = args
+        self.gen = O.serial_cycles(self.draft, self.target, self.prompt, K=args.K, k=args.k, ratio=args.ratio,
+                                   temperature=args.temperature, max_new_tokens=args.new_tokens, seed=0)
+        t0 = time.perf_counter()
+        self.out, _ = next(self.gen)   # warm-up expansions (query_depth draft layers)
+        self.warm_s = time.perf_counter() - t0
+        self.n_prev = 0
+        self.O = O
+
+    def cycle(self) -> tuple[int, float]:
+        """One CARD cycle: (tokens committed, seconds)."""
+        t0 = time.perf_counter()
+        try:
+            out, _ = next(self.gen)
+        except StopIteration:
+            return 0, 0.0
+        dt = time.perf_counter() - t0
+        n = len(out) - self.n_prev
+        self.n_prev = len(out)
+        return n, dt
+
+    def ar(self, n_tokens: int) -> float:
+        """Vanilla AR tokens/s on the same KV-cached target (engine.py:392-423)."""
+        ctx = list(self.prompt)
+        self.target.next_distribution(ctx)   # re-anchor the stream on the prompt
+        t0 = time.perf_counter()
+        for _ in range(n_tokens):
+            ctx.append(self.O.argmax_token(self.target.next_distribution(ctx)))
+        return n_tokens / (time.perf_counter() - t0)
+
+    def describe(self, n_cycles, n_tok, secs) -> str:
+        a = self.args
+        return (f"oracle CARD loop (card_oracle.serial_cycles = reference _run_serial) + run_vanilla, fp32 torch CPU, "
+                f"{a.draft} draft + {a.target} target, {a.prompt_len}-token prompt (prefilled once, "
+                f"{self.prefill_s:.1f} s, excluded), K={a.K} k={a.k} r={a.ratio} T={a.temperature}: {n_cycles} cycles, "
+                f"{n_tok} tokens in {secs:.1f} s; weights initialised once ({self.init_s:.1f} s)")
+
+
+def cpu_baseline(args):
+    """Bounded sample (~args.cpu_seconds of CARD cycles) of CpuCard on rank 0."""
+    cc = CpuCard(args)
+    n_tok, secs, n_cyc = 0, 0.0, 0
+    while secs < args.cpu_seconds or n_cyc == 0:
+        n, dt = cc.cycle()
+        if dt == 0.0:
+            break
+        n_tok, secs, n_cyc = n_tok + n, secs + dt, n_cyc + 1
+    ar = cc.ar(2)
+    return {"value": n_tok / secs if secs else None, "unit": UNIT, "cores": cc.cores, "kind": "port",
+            "ar_value": round(ar, 4), "sample": cc.describe(n_cyc, n_tok, secs)}
 
 
 def run_reference_arm(args):
+    """--impl reference: the reference's CPU path (CpuCard) on this box's host
+    cores, rank 0 only.  Warm-up steps are untimed cycles; each timed step is
+    one CARD cycle; value = committed tokens / seconds over the timed steps."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    import torch  # noqa: F401
-
-    samples = []
+    cc = CpuCard(args)
     for _ in range(args.warmup):
-        pass   # the CPU oracle has no warm-up state beyond weight init, done inside
-    cb = None
+        cc.cycle()
+    n_tok, secs, done = 0, 0.0, 0
     for _ in range(max(1, args.steps)):
-        cb = cpu_baseline(args, None)
-        samples.append(cb["value"])
-    value = sum(samples) / len(samples)
-    cb["value"] = value
-    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": 1000.0 / value if value else None, "higher_is_better": True,
+        n, dt = cc.cycle()
+        if dt == 0.0:
+            break
+        n_tok, secs, done = n_tok + n, secs + dt, done + 1
+    value = n_tok / secs if secs else 0.0
+    ar = cc.ar(2)
+    cb = {"value": value, "unit": UNIT, "cores": cc.cores, "kind": "port", "ar_value": round(ar, 4),
+          "sample": cc.describe(done, n_tok, secs)}
+    line = {"metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": args.gpus, "steps": done,
+            "warmup": args.warmup, "ms_per_step": round(1000.0 * secs / max(1, done), 1), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
             "impl": "reference",
-            "config": {"workload": f"{args.draft} draft + {args.target} target (CPU oracle AR sample)",
-                       "prompt_len": 16, "new_tokens": "time-bounded", "parallelism": "cpu"},
-            "cpu_baseline": cb, "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "config": {"workload": f"CARD {args.draft} draft + {args.target} target (CPU oracle)",
+                       "prompt_len": args.prompt_len, "K": args.K, "k": args.k, "ratio": args.ratio,
+                       "temperature": args.temperature, "step": "one CARD cycle", "parallelism": "cpu"},
+            "ar_tokens_per_s": round(ar, 4), "speedup_vs_ar": round(value / ar, 3) if ar else None,
+            "cpu_baseline": cb, "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0,
+                                        "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
@@ -437,7 +495,7 @@ def main():
         del draft, target
         torch.cuda.empty_cache()
         try:
-            line["cpu_baseline"] = cpu_baseline(args, tcfg)
+            line["cpu_baseline"] = cpu_baseline(args)
         except Exception as exc:   # the baseline is reported, never gating
             line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
                                     "sample": f"failed: {exc!r}"}

@@ -543,6 +543,17 @@ def run_serial(draft, target, prompt, K=50, k=3, ratio=5, temperature=0.0, max_n
                correction_enabled=True, seed=0, query_depth=None, max_depth=None):
     """Deterministic lockstep schedule (engine.py:290-317).  Returns
     (output tokens, list[Event])."""
+    res = None
+    for res in serial_cycles(draft, target, prompt, K, k, ratio, temperature, max_new_tokens, correction_enabled,
+                             seed, query_depth, max_depth):
+        pass
+    return res
+
+
+def serial_cycles(draft, target, prompt, K=50, k=3, ratio=5, temperature=0.0, max_new_tokens=64,
+                  correction_enabled=True, seed=0, query_depth=None, max_depth=None):
+    """run_serial as a generator: yields (output, trace) after the warm-up
+    expansions and after every cycle (the bench's bounded CPU samples)."""
     qd = ratio if query_depth is None else query_depth
     md = 2 * ratio if max_depth is None else max_depth
     prompt = [int(t) for t in prompt]
@@ -618,6 +629,7 @@ def run_serial(draft, target, prompt, K=50, k=3, ratio=5, temperature=0.0, max_n
             break
         clock += d_lat
         emit(clock, False, w, 0, 0, "draft_expand")
+    yield out, trace
     while not st["done"]:
         start, n_exp = clock, 0
         for _ in range(ratio):
@@ -633,7 +645,7 @@ def run_serial(draft, target, prompt, K=50, k=3, ratio=5, temperature=0.0, max_n
         if not st["done"]:
             update(acc, corr)
             emit(clock, hit, 0, 0, 0, "correct")
-    return out, trace
+        yield out, trace
 
 
 def run_vanilla(target, prompt, temperature=0.0, max_new_tokens=64, seed=0):

@@ -126,7 +126,7 @@ class RefLlama:
             c -= 1
         self.tokens = self.tokens[:c]
         self.kv = [(k[:c], v[:c]) for k, v in self.kv]
-        return self._extend(ctx[c:], "last")[-1]
+        return self._extend(ctx[c:])[-1]
 
     def full_logits(self, tokens: list[int]) -> torch.Tensor:
         self.tokens, self.kv = [], []

@@ -288,10 +288,12 @@ class _LlamaAdapter:
             return
         if self.prefill_rows is None:
             self.prefill_rows = RowBlock(PREFILL_CHUNK, 1, self.rt.dev)
+        nbytes = 0
         for s in range(0, len(tokens), PREFILL_CHUNK):
             chunk = tokens[s:s + PREFILL_CHUNK]
-            self.prefill_rows.set_chain(chunk, s)
+            nbytes += self.prefill_rows.set_chain(chunk, s)
             self.rt.forward(self.prefill_rows, PREFILL_CHUNK)
+        return nbytes
 
     def _fused_lm_head(self):
         """The bf16 tcgen05 lm_head of the draft plan (None on the fp32 path)."""
@@ -429,6 +431,8 @@ class DeviceRun:
         self.trt = _RowsAndTail(self.t_rows_max, 1, order, self.dev_t)
         self.committed = torch.zeros(self.max_ctx + 8, dtype=torch.int32, device=self.dev_t)
         self.committed[:C0] = torch.tensor(self.prompt, dtype=torch.int32)
+        # host<->device bytes of the current request (the bench's e2e record)
+        self.io = {"h2d": 4 * C0, "d2h": 0}
         rng = np.random.default_rng(cfg.seed)   # engine.py:162; the only randomness
         n_uni = (cfg.max_new_tokens + 2) * (cfg.query_depth + 2) + 16 if self.sampling else 1
         self.uni = torch.from_numpy(rng.random(n_uni)).to(self.dev_t)
@@ -443,6 +447,7 @@ class DeviceRun:
         st.anchor_origin = int(not cfg.correction_enabled)
         st.n_uni = n_uni
         self.E = torch.frombuffer(bytearray(bytes(st)), dtype=torch.int32).to(self.dev_t)
+        self.io["h2d"] += self.uni.numel() * 8 + self.E.numel() * 4
         self._E0 = self.E.clone()   # initial state, for rebind()
         self.E_ptr = ptr(self.E)
         # draft-side state: the same buffer in the lockstep drivers; a separate
@@ -478,6 +483,7 @@ class DeviceRun:
             self.cache.clear(prompt[-1])
         self.committed.zero_()
         self.committed[:C0] = torch.tensor(prompt, dtype=torch.int32)
+        self.io = {"h2d": 4 * C0, "d2h": 0}
         self.E.copy_(self._E0)
         if self.Ed is not self.E:
             self.Ed.copy_(self._E0)
@@ -498,22 +504,25 @@ class DeviceRun:
 
     def read_state(self) -> EngineState:
         self._host.copy_(self.E, non_blocking=True)
+        self.io["d2h"] += self.E.numel() * 4
         torch.cuda.current_stream().synchronize()
         return EngineState.from_buffer_copy(self._host.numpy().tobytes())
 
     def _set_field(self, name: str, value: int):
         self.E[self._field[name]] = int(value)
+        self.io["h2d"] += 4
         if self.Ed is not self.E:
             self.Ed[self._field[name]] = int(value)
+            self.io["h2d"] += 4
 
     def prefill(self):
         """Prompt KV for both models: target gets prompt[:-1] (its last token is
         the first verify input), the draft likewise (its flat step computes the root)."""
         body = self.prompt[:-1]
         with torch.cuda.device(self.dev_d):
-            self.da.prefill(self, body)
+            self.io["h2d"] += self.da.prefill(self, body) or 0
         with torch.cuda.device(self.dev_t):
-            self.ta.prefill(self, body)
+            self.io["h2d"] += self.ta.prefill(self, body) or 0
         self._set_field("Pd", len(body))
 
     # ---------------------------------------------------------------- sequences
@@ -545,6 +554,7 @@ class DeviceRun:
                          "cycle_end")
         if readback:
             self._host.copy_(self.E, non_blocking=True)
+            self.io["d2h"] += self.E.numel() * 4
 
     # ---------------------------------------------------------------- helpers
     def _alive(self) -> int:
@@ -680,6 +690,7 @@ class DeviceRun:
             g_d.replay()
             self.replays[0] += 1
         self._host.copy_(self.E, non_blocking=True)
+        self.io["d2h"] += self.E.numel() * 4
         ev = torch.cuda.Event()
         ev.record()
         yield ev
@@ -700,6 +711,7 @@ class DeviceRun:
             for _ in range(n_exp):
                 g_d.replay()
             g_t.replay()   # ends with the record copy into self._host
+            self.io["d2h"] += self.E.numel() * 4
             self.replays[0] += n_exp
             self.replays[1] += 1
             ev = torch.cuda.Event()
@@ -797,6 +809,7 @@ class _ConcurrentDriver:
             ev = torch.cuda.Event()
             ev.record(self.D)
         self.replays[0] += 1
+        self.run.io["d2h"] += self.run.Ed.numel() * 4   # the captured width-record readback
         return ev
 
     def _now(self, t0) -> float:
@@ -842,6 +855,7 @@ class _ConcurrentDriver:
                 v_ev = torch.cuda.Event()
                 v_ev.record(self.T)
             self.replays[2] += 1
+            run.io["d2h"] += run.E.numel() * 4
             while not v_ev.query():
                 if d_ev is not None and d_ev.query():
                     paused = self._draft_done(t0)
@@ -966,6 +980,7 @@ def run_speculative(draft, target, prompt: Sequence[TokenId], config: EngineConf
         run.timing["gpu_launches"] = drv.launches()
         run.timing["draft_steps"], run.timing["target_steps"] = drv.replays[0], drv.replays[2]
         run.timing["wall_s"] = time.perf_counter() - t0
+        run.timing["h2d_bytes"], run.timing["d2h_bytes"] = run.io["h2d"], run.io["d2h"]
         return RunResult(output=run.output, metrics=finalize(run.trace, target.spec, draft.spec), trace=run.trace,
                          wall=run.timing)
     if use_graphs:
@@ -990,6 +1005,7 @@ def run_speculative(draft, target, prompt: Sequence[TokenId], config: EngineConf
     else:
         run.run_stepwise()
     run.timing["wall_s"] = time.perf_counter() - t0
+    run.timing["h2d_bytes"], run.timing["d2h_bytes"] = run.io["h2d"], run.io["d2h"]
     return RunResult(output=run.output, metrics=finalize(run.trace, target.spec, draft.spec), trace=run.trace,
                      wall=run.timing)
 

@@ -487,8 +487,9 @@ class RowBlock:
         self.out_rows = b[2 + 5 * R:2 + 6 * R]
         self.extra = b[2 + 6 * R:]
 
-    def set_chain(self, tokens, start_pos: int, out_last_only=True):
-        """Host helper: causal chain rows (prefill / AR decode)."""
+    def set_chain(self, tokens, start_pos: int, out_last_only=True) -> int:
+        """Host helper: causal chain rows (prefill / AR decode); returns the
+        bytes copied to the device."""
         n = len(tokens)
         assert n <= self.rows_max
         host = torch.zeros(2 + 6 * self.rows_max, dtype=torch.int32)
@@ -505,3 +506,4 @@ class RowBlock:
         else:
             host[2 + 5 * R:2 + 5 * R + n] = torch.arange(n, dtype=torch.int32)
         self.block[: 2 + 6 * R].copy_(host, non_blocking=False)
+        return host.numel() * 4   # host->device bytes

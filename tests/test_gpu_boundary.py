@@ -80,9 +80,9 @@ def test_verify_result_kv_rollback_and_uniforms(card, temperature):
     from paper_2508_04462_b200.engine import DeviceRun
 
     doc = {"vocab_size": 48, "eos_token": None,
-           "draft": {"type": "kgram", "seed": 11, "order": 2, "sharpness": 30.0, "mix_seed": 131,
-                     "mix_weight": 0.1, "forward_latency": 1.0},
-           "target": {"type": "kgram", "seed": 11, "order": 2, "sharpness": 30.0, "forward_latency": 5.0}}
+           "draft": {"type": "kgram", "seed": 11, "order": 2, "sharpness": 80.0, "mix_seed": 131,
+                     "mix_weight": 0.02, "forward_latency": 1.0},
+           "target": {"type": "kgram", "seed": 11, "order": 2, "sharpness": 80.0, "forward_latency": 5.0}}
     d, t = card.models_from_dict(doc)
     cfg = card.EngineConfig(K=8, k=2, ratio=5, max_new_tokens=90, temperature=temperature, seed=4)
     run = DeviceRun(d, t, [3, 9, 27], cfg)

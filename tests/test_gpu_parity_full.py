@@ -84,10 +84,15 @@ def _prefill(rt, toks):
 
 
 def _check_rows(got, want, what):
+    """1e-2 relative over the logits of the block (the north-star bf16
+    bound), every single row within 2e-2, and the top-3 rule below."""
     got, want = got.double(), want.double()
+    total = float((got - want).norm() / want.norm())
+    rows = [float((got[i] - want[i]).norm() / want[i].norm()) for i in range(want.shape[0])]
+    print(f"{what}: block rel {total:.4g}, rows mean {np.mean(rows):.4g} max {max(rows):.4g}")
+    assert total < REL, (what, total)
     for i in range(want.shape[0]):
-        err = (got[i] - want[i]).norm() / want[i].norm()
-        assert err < REL, (what, i, float(err))
+        assert rows[i] < 2 * REL, (what, i, rows[i])
         # top-3 must agree wherever the oracle's ranking is separated by more
         # than the row's worst absolute error
         bound = 2.0 * float((got[i] - want[i]).abs().max())
