@@ -235,6 +235,16 @@ int card_attention(const float* q, const int32_t* dM, int m_max, const int32_t* 
                    const int32_t* n_extra, const int32_t* extra, int extra_max, const void* k_cache,
                    const void* v_cache, int kvdtype, int nh, int nkv, int hd, int max_plen, float* work,
                    void* o, int odtype, void* stream);
+/* Tree / chain attention over a paged KV cache (bf16 K/V and output, head_dim
+ * 64 or 128): prefix position p of every row lives in KV slot
+ * page_table[p / 64] * 64 + p % 64 (page_table NULL: slot p); extra slots are
+ * physical.  tcgen05 (S = QK^T and O = PV in TMEM) — the kernel card_attention
+ * uses for bf16 models.  Replaces the tree-mask forward of mask.py:173-217 /
+ * lm.py:155-196. */
+int card_attention_paged(const float* q, const int32_t* dM, int m_max, const int32_t* plen,
+                         const int32_t* n_extra, const int32_t* extra, int extra_max, const void* k_cache,
+                         const void* v_cache, const int32_t* page_table, int nh, int nkv, int hd, int max_plen,
+                         void* o, void* stream);
 /* draft lm_head epilogue: per-row top-k by (logit desc, token asc) with
  * log-probs logit/T - logsumexp (replaces extension_pool's rows_topk+log).
  * If ctx_tail != NULL the k-gram logit bias of card_logit_bias is applied on

@@ -72,6 +72,8 @@ SIGNATURES = {
     "card_attention_trace": (c_int, [_P]),
     "card_attention": (c_int, [_P, _P, c_int, _P, _P, _P, _P, c_int, _P, _P, c_int, c_int, c_int, c_int, c_int, _P,
                                _P, c_int, _P]),
+    "card_attention_paged": (c_int, [_P, _P, c_int, _P, _P, _P, c_int, _P, _P, _P, c_int, c_int, c_int, c_int, _P,
+                                     _P]),
     "card_lmhead_work_floats": (c_int, [c_int, c_int]),
     "card_topk_logits": (c_int, [_P, _P, c_int, c_int, c_int, c_double, _P, _P, _P, _P, _P, c_int, c_int, c_uint64,
                                  c_uint64, ctypes.c_float, ctypes.c_float, _P]),
@@ -117,17 +119,20 @@ LAUNCHES = {
     "card_cache_clear_status": 1, "card_embed": 1, "card_rmsnorm": 1, "card_rope_kv": 1, "card_attention": lambda a: 1 if (a[10] == 0 and a[17] == 0 and a[13] in (64, 128) and a[4] and _attn_fits(a)) else 3,
     "card_topk_logits": 2, "card_lmhead_topk_merge": 1, "card_argmax_logits": 2, "card_softmax64": 1, "card_logit_bias": 1,
     "card_draft_rows": 1, "card_target_rows": 1, "card_eos_fix": 1, "card_record_width": 1,
-    "card_verify_argmax": 1, "card_verify_probs": 1, "card_commit": 1, "card_verify_result": 1, "card_draft_promote": 2,
+    "card_attention_paged": 1, "card_verify_argmax": 1, "card_verify_probs": 1, "card_commit": 1, "card_verify_result": 1, "card_draft_promote": 2,
     "card_kv_compact": 2, "card_cycle_end": 1, "card_engine_handoff": 1,
 }
 launch_count = [0]
 
 
 def _attn_fits(a) -> bool:
-    """Mirror of attn_fused_fits (card_attn.cu): the fused attention gathers at
-    most 1024 extra slots per tile of 64/128 query-heads."""
-    m_max, nh, nkv, extra_max = a[2], a[11], a[12], a[7]
+    """Mirror of attn_tc_fits / attn_fused_fits (card_attn_tc.cu, card_attn.cu):
+    the one-launch kernels gather at most 1024 extra slots per query tile."""
+    m_max, nh, nkv, extra_max, hd = a[2], a[11], a[12], a[7], a[13]
     G = nh // nkv
+    rows_tc = 128 // G + 2
+    if m_max * G >= 256 and hd in (64, 128) and rows_tc <= 136 and rows_tc * extra_max <= 1024:
+        return True
     qt = 128 if m_max * G >= 512 else 64
     rows = qt // G + 2
     return rows <= 136 and rows * extra_max <= 1024

@@ -969,7 +969,10 @@ int card_rope_kv(const float* qkv, const int32_t* dM, int m_max, const int32_t* 
     return CARD_OK;
 }
 
-int card_attention_trace(unsigned long long* buf) { return attn_set_trace(buf); }
+int card_attention_trace(unsigned long long* buf) {
+    const int rc = attn_set_trace(buf);
+    return rc != CARD_OK ? rc : attn_tc_set_trace(buf);
+}
 
 int card_attention_work_floats(int m_max, int nh, int hd, int max_plen) {
     const int n_splits = (max_plen + kChunk - 1) / kChunk;
@@ -990,6 +993,16 @@ int card_attention(const float* q, const int32_t* dM, int m_max, const int32_t* 
         cudaFuncSetAttribute(attn_prefix_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
         attr = true;
     }
+    // Wide forwards (draft tree rows, prefill chunks: >= 256 query-heads per KV
+    // head) run the tcgen05 kernel.  Narrow ones (verify chains, AR steps) keep
+    // the register-resident mma.sync kernel: at 60 KB of shared memory it
+    // co-resides with the QKV GEMM's tail and starts under it, which the
+    // 200 KB tcgen05 kernel cannot; same-box A/B: 3.25 / 3.33 ms vs 3.49 /
+    // 3.62 ms per AR / verify forward of Llama-3.1-8B, equal draft forwards
+    // (tools/ab_lib.sh, profiles/r02_attention.txt).
+    if (kvdtype == 0 && odtype == 0 && m_max * (nh / nkv) >= 256 && attn_tc_fits(m_max, nh, nkv, hd, extra_max))
+        return launch_attn_tc(q, dM, m_max, plen, n_extra, extra, extra_max, kc, vc, nullptr, nh, nkv, hd, max_plen,
+                              o, s);
     if (kvdtype == 0 && odtype == 0 && (hd == 64 || hd == 128) &&
         attn_fused_fits(m_max, nh, nkv, extra_max))
         if (slot) return launch_attn_fused(q, dM, m_max, plen, slot, n_extra, extra, extra_max, kc, vc, nh, nkv, hd,
@@ -1019,6 +1032,18 @@ int card_attention(const float* q, const int32_t* dM, int m_max, const int32_t* 
     else CARD_PDL((attn_combine_kernel<float>), dim3(g3), dim3(64), 0, s, dM, plen, nh, hd, n_splits, work, (float*)o);
     CARD_LAUNCH_CHECK();
     return CARD_OK;
+}
+
+int card_attention_paged(const float* q, const int32_t* dM, int m_max, const int32_t* plen,
+                         const int32_t* n_extra, const int32_t* extra, int extra_max, const void* kc,
+                         const void* vc, const int32_t* page_table, int nh, int nkv, int hd, int max_plen,
+                         void* o, void* stream) {
+    if (!q || !dM || !plen || !kc || !vc || !o || m_max <= 0 || nkv <= 0 || nh % nkv) return CARD_E_INPUT;
+    if (!attn_tc_fits(m_max, nh, nkv, hd, extra_max)) return CARD_E_CONFIG;
+    const int rc = launch_attn_tc(q, dM, m_max, plen, n_extra, extra, extra_max, kc, vc, page_table, nh, nkv, hd,
+                                  max_plen, o, (cudaStream_t)stream);
+    if (rc == CARD_OK) CARD_LAUNCH_CHECK();
+    return rc;
 }
 
 // vocab splits of the lm_head readers: about six CTAs per SM (the logits are

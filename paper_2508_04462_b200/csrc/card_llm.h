@@ -14,6 +14,12 @@ int launch_attn_fused(const float* q, const int32_t* dM, int m_max, const int32_
                       int max_plen, void* o, cudaStream_t s);
 int attn_set_trace(unsigned long long* buf);
 bool attn_fused_fits(int m_max, int nh, int nkv, int extra_max);
+// tcgen05 attention over a paged KV cache (card_attn_tc.cu)
+bool attn_tc_fits(int m_max, int nh, int nkv, int hd, int extra_max);
+int attn_tc_set_trace(unsigned long long* buf);
+int launch_attn_tc(const float* q, const int32_t* dM, int m_max, const int32_t* plen, const int32_t* n_extra,
+                   const int32_t* extra, int extra_max, const void* kc, const void* vc, const int32_t* page_table,
+                   int nh, int nkv, int hd, int max_plen, void* o, cudaStream_t s);
 }  // namespace card
 
 // GEMM epilogues (card_gemm.cu)

@@ -232,3 +232,44 @@ def test_attention_with_extras_matches_torch(card, hd, nh, nkv, M):
         got = o[r].float()
         err = (got - want).norm() / want.norm()
         assert err < 1e-2, (r, float(err))
+
+
+@pytest.mark.parametrize("hd,M", [(64, 116), (128, 8), (128, 40)])
+def test_paged_attention_matches_torch(card, hd, M):
+    """card_attention_paged: prefix positions resolved through a shuffled page
+    table (64-slot pages), tree extras as physical slots; fp32 reference
+    reads the same logical sequence."""
+    from paper_2508_04462_b200._device import ptr, stream_ptr
+    from paper_2508_04462_b200._lib import lib
+    from paper_2508_04462_b200.llama import RowBlock
+
+    nh, nkv, XM = 32, 8, 16
+    g = torch.Generator(device="cuda").manual_seed(hd * 3 + M)
+    rng = np.random.default_rng(hd * 5 + M)
+    n_pages, P = 24, 1000
+    perm = torch.tensor(rng.permutation(n_pages)[: (P + 63) // 64], dtype=torch.int32, device="cuda")
+    slots = n_pages * 64 + 256
+    kc = torch.randn(slots, nkv, hd, device="cuda", generator=g).to(torch.bfloat16)
+    vc = torch.randn(slots, nkv, hd, device="cuda", generator=g).to(torch.bfloat16)
+    q = torch.randn(M, nh, hd, device="cuda", generator=g) / hd ** 0.5
+    plen = [int(x) for x in rng.integers(1, P + 1, M)]
+    extras = [sorted(set(int(x) for x in rng.integers(n_pages * 64, slots, int(rng.integers(0, XM)))))
+              for _ in range(M)]
+    rows = RowBlock(M, XM, "cuda")
+    _fill(rows, [0] * M, [0] * M, [0] * M, plen, extras, [])
+    o = torch.zeros(M, nh * hd, device="cuda", dtype=torch.bfloat16)
+    rc = lib().card_attention_paged(ptr(q), ptr(rows.M), M, ptr(rows.plen), ptr(rows.n_extra), ptr(rows.extra), XM,
+                                    ptr(kc), ptr(vc), ptr(perm), nh, nkv, hd, P, ptr(o), stream_ptr())
+    assert rc == 0
+    torch.cuda.synchronize()
+    logical = (perm.long().cpu()[:, None] * 64 + torch.arange(64)[None]).reshape(-1)
+    G = nh // nkv
+    Kf, Vf = kc.float(), vc.float()
+    for r in range(M):
+        vis = logical[:plen[r]].tolist() + extras[r]
+        k = Kf[vis].repeat_interleave(G, dim=1)
+        v = Vf[vis].repeat_interleave(G, dim=1)
+        s = torch.einsum("hd,thd->ht", q[r], k)
+        want = torch.einsum("ht,thd->hd", torch.softmax(s, -1), v).reshape(-1)
+        err = (o[r].float() - want).norm() / want.norm()
+        assert err < 1e-2, (r, float(err))

@@ -37,7 +37,7 @@ lib().card_attention_trace(None)
 t = buf.view(-1, 8).cpu().numpy().astype(np.float64)
 t = t[t[:, 0] > 0]
 t0 = t[:, 0].min()
-names = ["entry", "pdl", "prologue", "chunk0", "loop_end", "pushed", "clsync", "end"]
+names = ["entry", "setup", "pdl", "q_ready", "loop_end", "clsync1", "clsync2", "end"]
 print(f"{which}: {len(t)} CTAs")
 for k, nm in enumerate(names):
     v = t[:, k][t[:, k] > 0] - t0
