@@ -53,6 +53,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--ar-steps", type=int, default=2)
+    ap.add_argument("--tp", action="store_true",
+                    help="under torchrun: one request, target tensor-parallel over all ranks (NCCL), draft "
+                         "replicated (BASELINE configs[3] with --target llama-3.1-70b)")
     return ap.parse_args()
 
 
@@ -314,7 +317,8 @@ def measure_roofline(target, rows_max, ctx_len, peak):
     rt.forward(rows, rows_max)
     torch.cuda.synchronize()
     t_gemm = replay_ms(graph_of(run_gemms))
-    t_fwd = replay_ms(graph_of(lambda: rt.forward(rows, rows_max)))
+    # a tensor-parallel forward carries collectives: time its GEMM chain only
+    t_fwd = replay_ms(graph_of(lambda: rt.forward(rows, rows_max))) if rt.tp is None else float("nan")
     # isolated: each launch alone after an L2 flush (no PDL overlap)
     stream = torch.cuda.current_stream()
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
@@ -401,15 +405,21 @@ def main():
     tcfg, dcfg = PRESETS[args.target], PRESETS[args.draft]
     bias = LogitBias(seed=11, order=2, sharpness=args.bias_sharpness, mix_seed=131, mix_weight=args.bias_mix)
     t_init = time.perf_counter()
+    tp = None
+    if args.tp and world > 1:
+        from paper_2508_04462_b200.tp import TPComm
+
+        tp = TPComm()
     target = card.LlamaModel(tcfg, seed=2, dtype="bf16", bias=bias,
-                             spec=card.ModelSpec(tcfg.total_params() / 1e9, 7.0))
+                             spec=card.ModelSpec(tcfg.total_params() / 1e9, 7.0), tp=tp)
     draft = card.LlamaModel(dcfg, seed=1, dtype="bf16", bias=bias,
                             spec=card.ModelSpec(dcfg.total_params() / 1e9, 1.0))
     torch.cuda.synchronize()
     init_s = time.perf_counter() - t_init
     cfg = card.EngineConfig(K=args.K, k=args.k, ratio=args.ratio, temperature=args.temperature,
                             max_new_tokens=args.new_tokens, seed=0, mode=args.mode)
-    P = prompts(args.warmup + args.steps, tcfg.vocab_size, args.prompt_len, rank)
+    # DP replicas: every rank its own requests; TP: every rank the same request
+    P = prompts(args.warmup + args.steps, tcfg.vocab_size, args.prompt_len, 0 if tp else rank)
 
     def barrier():
         torch.cuda.synchronize()
@@ -446,6 +456,8 @@ def main():
     clk = clocks.stop()
     # whole-job aggregate: tokens over all ranks / max device time over ranks
     all_tokens, max_ms, max_e2e = aggregate_ranks(tokens, dec_ms, e2e_s, world, "cuda")
+    if tp is not None:   # one request decoded by all ranks together
+        all_tokens = float(tokens)
     value = all_tokens / (max_ms / 1000.0)
     # same-box GPU autoregressive baseline (same kernels; M = 1 rows)
     ar_tok = 0
@@ -474,7 +486,7 @@ def main():
         "config": {"workload": f"CARD {args.draft} draft + {args.target} target, 1 request/GPU (time-shared)",
                    "model": f"{args.draft}+{args.target}", "global_batch": world, "seq_len": args.prompt_len,
                    "new_tokens": args.new_tokens, "K": args.K, "k": args.k, "ratio": args.ratio,
-                   "temperature": args.temperature, "mode": args.mode, "parallelism": f"dp{world} replicas",
+                   "temperature": args.temperature, "mode": args.mode, "parallelism": f"tp{world} target + replicated draft" if tp else f"dp{world} replicas",
                    "agreement_knob": {"kgram_logit_bias_sharpness": args.bias_sharpness, "mix_weight": args.bias_mix},
                    "l2": "weights 17.5 GB >> 126 MB L2: streamed from HBM every step (no flush needed)"},
         "speedup_vs_ar": round(value / ar_value, 3),

@@ -219,6 +219,11 @@ int card_linear_destroy(card_linear* h);
 
 /* x[r] = E[tok[r]] (fp32 residual); if xb != NULL also its bf16 copy and the
  * per-16-column sums of squares ssq[(col/16)*ssq_ld + r] (fused-norm input) */
+/* Tensor-parallel target: after the NCCL all-reduce of a
+ * row-parallel o / down projection partial, x += part and refresh the bf16
+ * residual copy + per-16-column sums of squares (ssq[H/16][ssq_ld]). */
+int card_resid_add(const int32_t* dM, int m_max, int H, float* x, const float* part, void* xb, float* ssq, int ssq_ld,
+                   void* stream);
 int card_embed(const int32_t* tok, const int32_t* dM, int m_max, const void* E, int wdtype, int H,
                float* x, void* xb, float* ssq, int ssq_ld, void* stream);
 int card_rmsnorm(const float* x, const float* w, int H, float eps, const int32_t* dM, int m_max,

@@ -66,6 +66,7 @@ SIGNATURES = {
     "card_lmhead_topk_merge": (c_int, [_P, _P, c_int, c_int, c_int, c_int, _P, _P, _P, _P]),
     "card_linear_destroy": (c_int, [_P]),
     "card_embed": (c_int, [_P, _P, c_int, _P, c_int, c_int, _P, _P, _P, c_int, _P]),
+    "card_resid_add": (c_int, [_P, c_int, c_int, _P, _P, _P, _P, c_int, _P]),
     "card_rmsnorm": (c_int, [_P, _P, c_int, ctypes.c_float, _P, c_int, _P, _P, c_int, _P]),
     "card_rope_kv": (c_int, [_P, _P, c_int, _P, _P, _P, _P, c_int, c_int, c_int, _P, _P, _P, c_int, _P]),
     "card_attention_work_floats": (c_int, [c_int, c_int, c_int, c_int]),
@@ -116,7 +117,7 @@ LAUNCHES = {
     "card_kgram_dist": 1, "card_rows_topk": 1, "card_log_cr": 1, "card_exp_cr": 1,
     "card_cache_reset": 2, "card_cache_clear": 3, "card_cache_expand": 2, "card_cache_expand_topk": 1, "card_cache_pool": 2,
     "card_cache_query": 1, "card_cache_correct": 1, "card_cache_advance_root": 1, "card_cache_count_alive": 1,
-    "card_cache_clear_status": 1, "card_embed": 1, "card_rmsnorm": 1, "card_rope_kv": 1, "card_attention": lambda a: 1 if (a[10] == 0 and a[17] == 0 and a[13] in (64, 128) and a[4] and _attn_fits(a)) else 3,
+    "card_cache_clear_status": 1, "card_embed": 1, "card_resid_add": 1, "card_rmsnorm": 1, "card_rope_kv": 1, "card_attention": lambda a: 1 if (a[10] == 0 and a[17] == 0 and a[13] in (64, 128) and a[4] and _attn_fits(a)) else 3,
     "card_topk_logits": 2, "card_lmhead_topk_merge": 1, "card_argmax_logits": 2, "card_softmax64": 1, "card_logit_bias": 1,
     "card_draft_rows": 1, "card_target_rows": 1, "card_eos_fix": 1, "card_record_width": 1,
     "card_attention_paged": 1, "card_verify_argmax": 1, "card_verify_probs": 1, "card_commit": 1, "card_verify_result": 1, "card_draft_promote": 2,

@@ -454,7 +454,7 @@ __global__ void __launch_bounds__(Roles<NG>::kThreads, 1) tc_gemm_kernel(const _
     uint64_t* rbar = tempty + 2;    // split-K: every rank's slice of my rows landed (bulk DSMEM copies)
     uint32_t* tmem_slot = (uint32_t*)(rbar + 2);
     float* xch = (float*)(tmem_slot + 4);   // [groups][16][128] (group 1's only when Mpad > 16)
-    float* invs = xch + (a.Mpad > 16 ? 2 : 1) * 16 * 128;   // [256] per-token rsqrt(mean x^2 + eps)
+    float* invs = xch + NG * 16 * 128;   // [256] per-token rsqrt(mean x^2 + eps)
     int* tpos = (int*)(invs + 256);          // [256] QKV: RoPE position of each token row
     int* tslot = tpos + 256;                 // [256] QKV: KV-cache slot of each token row
     uint64_t* kgs = (uint64_t*)(tslot + 256);   // [256][2] lm_head: k-gram stream state of each output row
@@ -1124,15 +1124,22 @@ static cudaError_t set_tc_attr(int smem) {
     (void)smem;
     set_tc_attr_ng<EPI, 1>();
     set_tc_attr_ng<EPI, 2>();
+    if constexpr (EPI == EPI_TOPK)
+        cudaFuncSetAttribute(tc_gemm_kernel<EPI_TOPK, false, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             227 * 1024);
     return cudaGetLastError();
 }
+// epilogue groups of a plan: the fused top-k lm_head's per-element work
+// (bias hash, sum-exp, top-4 insertion) needs four groups to hide under the
+// wide tile's weight stream; other wide epilogues two; narrow tiles one
+static int epi_groups(int epi, int Mpad) { return Mpad > 16 ? (epi == EPI_TOPK ? 4 : 2) : 1; }
 
 template <int EPI>
 static cudaError_t launch_tc(const card_linear* h, const TcArgs& a, cudaStream_t s) {
     cudaLaunchConfig_t cfg = {};
-    const int ng = a.Mpad > 16 ? 2 : 1;
+    const int ng = epi_groups(EPI, a.Mpad);
     cfg.gridDim = dim3(h->grid);
-    cfg.blockDim = dim3(ng == 2 ? Roles<2>::kThreads : Roles<1>::kThreads);
+    cfg.blockDim = dim3(ng == 4 ? Roles<4>::kThreads : ng == 2 ? Roles<2>::kThreads : Roles<1>::kThreads);
     cfg.dynamicSmemBytes = h->smem;
     cfg.stream = s;
     cudaLaunchAttribute attr[2];
@@ -1148,6 +1155,8 @@ static cudaError_t launch_tc(const card_linear* h, const TcArgs& a, cudaStream_t
     }
     cfg.attrs = attr;
     cfg.numAttrs = n;
+    if constexpr (EPI == EPI_TOPK)
+        if (ng == 4) return cudaLaunchKernelEx(&cfg, tc_gemm_kernel<EPI_TOPK, false, 4>, h->tmW, h->tmX, a);
     if (ng == 2) {
         if (a.cluster > 1) return cudaLaunchKernelEx(&cfg, tc_gemm_kernel<EPI, true, 2>, h->tmW, h->tmX, a);
         return cudaLaunchKernelEx(&cfg, tc_gemm_kernel<EPI, false, 2>, h->tmW, h->tmX, a);
@@ -1285,7 +1294,7 @@ int card_linear_create(const void* W, int N, int K, int wdtype, const void* X, i
     int ctas_per_sm = (cols <= 256 && Mpad < 64) ? 2 : 1;
     const int stage_bytes = kTileN * kBK * 2 + Mpad * kBK * 2;
     int budget = (ctas_per_sm == 2 ? 110 : 220) * 1024;
-    const int extra = 1024 + 64 * 8 + (Mpad > 16 ? 2 : 1) * 16 * 128 * 4 + 3 * 256 * 4 + 2 * 256 * 8 + 64;
+    const int extra = 1024 + 64 * 8 + epi_groups(epi, Mpad) * 16 * 128 * 4 + 3 * 256 * 4 + 2 * 256 * 8 + 64;
     int stages = (budget - extra) / stage_bytes;
     if (stages > 8) stages = 8;
     if (stages < 2) stages = 2;

@@ -78,6 +78,30 @@ __global__ void embed_kernel(const int32_t* __restrict__ tok, const int32_t* dM,
     }
 }
 
+// ---------------------------------------------------------------- tensor-parallel residual
+// x += part (the all-reduced partial of a row-parallel o / down projection),
+// then the bf16 copy and the per-16-column sums of squares the next fused
+// RMSNorm consumes (what the RESID GEMM epilogue does on one GPU)
+__global__ void resid_add_kernel(const int32_t* dM, int H, float* __restrict__ x, const float* __restrict__ part,
+                                 __nv_bfloat16* __restrict__ xb, float* __restrict__ ssq, int ssq_ld) {
+    pdl_wait();
+    pdl_trigger();
+    const int r = blockIdx.x;
+    if (r >= *dM) return;
+    for (int g16 = threadIdx.x; g16 < H / 16; g16 += blockDim.x) {
+        float acc = 0.f;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            const int64_t c = (int64_t)r * H + g16 * 16 + i;
+            const float v = x[c] + part[c];
+            x[c] = v;
+            xb[c] = __float2bfloat16(v);
+            acc = fmaf(v, v, acc);
+        }
+        ssq[(int64_t)g16 * ssq_ld + r] = acc;
+    }
+}
+
 // ---------------------------------------------------------------- rmsnorm
 template <typename Y>
 __global__ void rmsnorm_kernel(const float* __restrict__ x, const float* __restrict__ w, int H, float eps,
@@ -941,6 +965,15 @@ int card_embed(const int32_t* tok, const int32_t* dM, int m_max, const void* E, 
         CARD_PDL((embed_kernel<__nv_bfloat16>), dim3(m_max), dim3(256), 0, s, tok, dM, (const __nv_bfloat16*)E, H, x, xbb,
                  ssq, ssq_ld);
     else CARD_PDL((embed_kernel<float>), dim3(m_max), dim3(256), 0, s, tok, dM, (const float*)E, H, x, xbb, ssq, ssq_ld);
+    CARD_LAUNCH_CHECK();
+    return CARD_OK;
+}
+
+int card_resid_add(const int32_t* dM, int m_max, int H, float* x, const float* part, void* xb, float* ssq, int ssq_ld,
+                   void* stream) {
+    if (!dM || !x || !part || !xb || !ssq || H % 16 != 0 || m_max <= 0) return CARD_E_INPUT;
+    CARD_PDL(resid_add_kernel, dim3(m_max), dim3(128), 0, (cudaStream_t)stream, dM, H, x, part, (__nv_bfloat16*)xb,
+             ssq, ssq_ld);
     CARD_LAUNCH_CHECK();
     return CARD_OK;
 }

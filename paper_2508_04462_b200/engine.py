@@ -245,6 +245,8 @@ class _LlamaAdapter:
         self.lm_work = torch.zeros(lib().card_lmhead_work_floats(rows_max, self.k), dtype=torch.float32, device=dev)
         self.probs = torch.zeros((rows_max, V), dtype=torch.float64, device=dev) if run.sampling else None
         self.prefill_rows = None
+        if role == "draft" and getattr(model, "fused_topk", False) and self.k <= 4:
+            self.rt.lm_topk_head(rows_max)   # built before any graph capture
         if role == "draft":
             nL = model.cfg.n_layers
             row_bytes = self.rt.kv_row_elems() * self.rt.kv_esize()
@@ -914,7 +916,7 @@ _SESSIONS_PER_TARGET = 2
 def _model_sig(model) -> tuple:
     """What a captured run depends on besides the weights: identity, EOS and
     the agreement-bias / k-gram parameters (all baked into the graphs)."""
-    fields = ("eos_token", "bias", "seed", "mix_seed", "mix_weight", "sharpness", "order")
+    fields = ("eos_token", "bias", "seed", "mix_seed", "mix_weight", "sharpness", "order", "fused_topk")
     return (id(model),) + tuple(repr(getattr(model, f, None)) for f in fields)
 
 
@@ -954,7 +956,10 @@ def run_speculative(draft, target, prompt: Sequence[TokenId], config: EngineConf
 
         return run_host_models(draft, target, prompt, config)
     if use_graphs is None:
-        use_graphs = "llama" in kinds and config.correction_enabled
+        # a tensor-parallel target's collectives go through torch.distributed
+        # (NCCL or gloo) and run eagerly: the stepwise driver
+        tp = getattr(target, "tp", None) is not None or getattr(draft, "tp", None) is not None
+        use_graphs = "llama" in kinds and config.correction_enabled and not tp
     if trace_alive is None:
         trace_alive = not use_graphs
     concurrent = config.mode == "concurrent" and config.correction_enabled and use_graphs
@@ -1026,6 +1031,8 @@ def run_speculative_batch(draft, target, prompts: Sequence[Sequence[TokenId]], c
     kinds = {getattr(draft, "engine_kind", "host"), getattr(target, "engine_kind", "host")}
     if kinds != {"llama"}:
         raise ConfigError("run_speculative_batch needs a transformer draft/target pair")
+    if getattr(target, "tp", None) is not None:
+        raise ConfigError("run_speculative_batch does not take a tensor-parallel target")
     if not config.correction_enabled or config.mode != "serial_sim":
         raise ConfigError("run_speculative_batch runs the serial_sim schedule with correction enabled")
     _validate_run_config(draft, target, config)
@@ -1152,7 +1159,7 @@ def run_vanilla(target, prompt: Sequence[TokenId], config: EngineConfig, *, use_
         return run_vanilla_host(target, prompt, config)
     run = VanillaRun(target, prompt, config)
     if use_graph is None:
-        use_graph = getattr(target, "engine_kind", "") == "llama"
+        use_graph = getattr(target, "engine_kind", "") == "llama" and getattr(target, "tp", None) is None
     t0 = time.perf_counter()
     run.prefill()
     if use_graph:

@@ -88,6 +88,8 @@ PRESETS = {
     # BASELINE.json configs[1]
     "llama-3.2-1b": LlamaConfig(128256, 2048, 16, 32, 8, 64, 8192, 500000.0, 1e-5, True, False, _LLAMA3_SCALING_1B),
     "llama-3.1-8b": LlamaConfig(128256, 4096, 32, 32, 8, 128, 14336, 500000.0, 1e-5, False, False, _LLAMA3_SCALING_8B),
+    # BASELINE.json configs[3] (tensor-parallel target, tp.py)
+    "llama-3.1-70b": LlamaConfig(128256, 8192, 80, 64, 8, 128, 28672, 500000.0, 1e-5, False, False, _LLAMA3_SCALING_8B),
     # BASELINE.json configs[2].  The two checkpoints pad their embedding tables
     # differently (151936 vs 152064 rows) over one 151665-token tokenizer; the
     # engine needs one vocabulary (engine.py:127-136), so the draft is padded
@@ -124,10 +126,10 @@ def rope_tables(cfg: LlamaConfig, max_pos: int) -> tuple[torch.Tensor, torch.Ten
     return freqs.cos().contiguous(), freqs.sin().contiguous()
 
 
-def init_weights(cfg: LlamaConfig, seed: int, device="cpu", dtype=torch.float32) -> dict:
-    """Canonical (HF-layout) random-init weights: Normal(0, init_std), norms 1,
-    biases 0.  Same seed + same device => identical tensors (the oracle and
-    the device model are built from one call on the CPU for parity runs)."""
+def iter_weights(cfg: LlamaConfig, seed: int, device="cpu", dtype=torch.float32):
+    """(name, tensor) of the canonical random-init weights in generation
+    order (one seeded generator): Normal(0, init_std), norms 1, biases 0.
+    A tied lm_head is not yielded (it is the embedding)."""
     g = torch.Generator(device=device)
     g.manual_seed(int(seed))
 
@@ -137,24 +139,34 @@ def init_weights(cfg: LlamaConfig, seed: int, device="cpu", dtype=torch.float32)
         return t.to(dtype)
 
     H, hd = cfg.hidden, cfg.head_dim
-    w = {"embed": normal(cfg.vocab_size, H)}
+    yield "embed", normal(cfg.vocab_size, H)
     for i in range(cfg.n_layers):
         p = f"l{i}."
-        w[p + "wq"] = normal(cfg.n_heads * hd, H)
-        w[p + "wk"] = normal(cfg.n_kv_heads * hd, H)
-        w[p + "wv"] = normal(cfg.n_kv_heads * hd, H)
+        yield p + "wq", normal(cfg.n_heads * hd, H)
+        yield p + "wk", normal(cfg.n_kv_heads * hd, H)
+        yield p + "wv", normal(cfg.n_kv_heads * hd, H)
         if cfg.qkv_bias:
-            w[p + "bq"] = torch.zeros(cfg.n_heads * hd, device=device)
-            w[p + "bk"] = torch.zeros(cfg.n_kv_heads * hd, device=device)
-            w[p + "bv"] = torch.zeros(cfg.n_kv_heads * hd, device=device)
-        w[p + "wo"] = normal(H, cfg.n_heads * hd)
-        w[p + "wg"] = normal(cfg.ffn, H)
-        w[p + "wu"] = normal(cfg.ffn, H)
-        w[p + "wd"] = normal(H, cfg.ffn)
-        w[p + "attn_norm"] = torch.ones(H, device=device)
-        w[p + "mlp_norm"] = torch.ones(H, device=device)
-    w["norm"] = torch.ones(H, device=device)
-    w["lm_head"] = w["embed"] if cfg.tie_embeddings else normal(cfg.vocab_size, H)
+            yield p + "bq", torch.zeros(cfg.n_heads * hd, device=device)
+            yield p + "bk", torch.zeros(cfg.n_kv_heads * hd, device=device)
+            yield p + "bv", torch.zeros(cfg.n_kv_heads * hd, device=device)
+        yield p + "wo", normal(H, cfg.n_heads * hd)
+        yield p + "wg", normal(cfg.ffn, H)
+        yield p + "wu", normal(cfg.ffn, H)
+        yield p + "wd", normal(H, cfg.ffn)
+        yield p + "attn_norm", torch.ones(H, device=device)
+        yield p + "mlp_norm", torch.ones(H, device=device)
+    yield "norm", torch.ones(H, device=device)
+    if not cfg.tie_embeddings:
+        yield "lm_head", normal(cfg.vocab_size, H)
+
+
+def init_weights(cfg: LlamaConfig, seed: int, device="cpu", dtype=torch.float32) -> dict:
+    """Canonical (HF-layout) random-init weights (iter_weights).  Same seed +
+    same device => identical tensors (the oracle and the device model are
+    built from one call on the CPU for parity runs)."""
+    w = dict(iter_weights(cfg, seed, device, dtype))
+    if cfg.tie_embeddings:
+        w["lm_head"] = w["embed"]
     return w
 
 
@@ -276,8 +288,13 @@ class DeviceLlama:
     """
 
     def __init__(self, cfg: LlamaConfig, packed: dict, *, max_ctx: int, tree_slots: int = 0,
-                 row_budgets=(1,), extra_max: int = 32):
+                 row_budgets=(1,), extra_max: int = 32, tp=None):
+        """tp: (comm, shards, full_vocab) of a tensor-parallel target rank (tp.py):
+        cfg is then the rank's shard; o / down write partials that are
+        all-reduced before the residual add, and the vocabulary slices of
+        the lm_head are summed into full-vocabulary logits."""
         self.dev = require_cuda()
+        self.tp = tp
         dtype = packed["dtype"]
         self.cfg = cfg
         self.dtype = dtype
@@ -315,6 +332,12 @@ class DeviceLlama:
         self.g = torch.zeros((P, c.ffn), dtype=act, device=dev)
         self.hf = torch.zeros((P, H), dtype=act, device=dev)
         self.logits = torch.zeros((P, c.vocab_size), dtype=torch.float32, device=dev)
+        if tp is not None:
+            comm, shards, V_full = tp
+            self.tp_vocab = shards[comm.rank].vocab
+            self.logits_local = self.logits                        # [P, this rank's padded slice]
+            self.logits = torch.zeros((P, V_full), dtype=torch.float32, device=dev)
+            self.part = torch.zeros((P, H), dtype=torch.float32, device=dev)
         # fused-norm path (bf16): bf16 residual copy + per-16-column sums of squares
         self.fused = bool(packed.get("folded")) and H % 16 == 0 and hd in (64, 128) and \
             (c.qkv_dim % 128 == 0) and (c.n_heads * hd) % 128 == 0 and (c.n_kv_heads * hd) % 128 == 0
@@ -325,6 +348,8 @@ class DeviceLlama:
         # per-layer KV base pointer arrays for the engine's KV movers
         self.k_ptrs = torch.tensor([t.data_ptr() for t in self.k_cache], dtype=torch.int64, device=dev)
         self.v_ptrs = torch.tensor([t.data_ptr() for t in self.v_cache], dtype=torch.int64, device=dev)
+        if tp is not None and not self.fused:
+            raise ConfigError("the tensor-parallel target runs the fused bf16 path (head_dim 64/128, 128-aligned shards)")
         self.plans = {m: self._make_plan(m) for m in sorted(set(row_budgets))}
 
     # ------------------------------------------------------------ plans
@@ -355,15 +380,38 @@ class DeviceLlama:
         for li, L in enumerate(self.layers):
             qkv = _Linear(L["wqkv"], self.xb, m_max, EPI_QKV_ROPE, self.qkv, c.qkv_dim, L["bqkv"])
             qkv.fuse_norm(self.ssq, parts, P, c.rms_eps, H)
-            o = _Linear(L["wo"], self.o, m_max, EPI_RESID_F32, self.x, H)
-            o.fuse_resid(self.ssq, P, self.xb)
+            if self.tp is None:
+                o = _Linear(L["wo"], self.o, m_max, EPI_RESID_F32, self.x, H)
+                o.fuse_resid(self.ssq, P, self.xb)
+            else:   # row-parallel: partial -> all-reduce -> card_resid_add
+                o = _Linear(L["wo"], self.o, m_max, EPI_STORE_F32, self.part, H)
             gu = _Linear(L["wgu"], self.xb, m_max, EPI_SWIGLU_BF16, self.g, c.ffn)
             gu.fuse_norm(self.ssq, parts, P, c.rms_eps, H)
-            d = _Linear(L["wd"], self.g, m_max, EPI_RESID_F32, self.x, H)
-            d.fuse_resid(self.ssq, P, self.xb)
+            if self.tp is None:
+                d = _Linear(L["wd"], self.g, m_max, EPI_RESID_F32, self.x, H)
+                d.fuse_resid(self.ssq, P, self.xb)
+            else:
+                d = _Linear(L["wd"], self.g, m_max, EPI_STORE_F32, self.part, H)
             plan["layers"].append({"qkv": qkv, "o": o, "gu": gu, "d": d})
-        plan["lm_head"] = _Linear(self.lm_head, self.xb, m_max, EPI_STORE_F32, self.logits, c.vocab_size)
+        plan["lm_head"] = _Linear(self.lm_head, self.xb, m_max, EPI_STORE_F32,
+                                  self.logits if self.tp is None else self.logits_local, c.vocab_size)
         return plan
+
+    def _tp_reduce(self, dM, mm):
+        """All-reduce the row-parallel partial, then x += part (+ bf16 copy, ssq)."""
+        comm = self.tp[0]
+        comm.all_reduce(self.part)
+        raise_for_status(lib().card_resid_add(ptr(dM), mm, self.cfg.hidden, ptr(self.x), ptr(self.part), ptr(self.xb),
+                                              ptr(self.ssq), self.mpad, stream_ptr()), "card_resid_add")
+
+    def _tp_gather_logits(self):
+        """Vocabulary slices -> full logits on every rank: each rank writes its
+        slice into zeros and an all-reduce sums them (exact: x + 0 = x)."""
+        comm = self.tp[0]
+        v0, v1 = self.tp_vocab
+        self.logits.zero_()
+        self.logits[:, v0:v1].copy_(self.logits_local[:, :v1 - v0])
+        comm.all_reduce(self.logits)
 
     def _bind_rows(self, plan: dict, rows: "RowBlock"):
         """Row-dependent epilogue pointers (positions, KV slots, lm_head row offset)."""
@@ -458,9 +506,17 @@ class DeviceLlama:
                                   c.n_heads, c.n_kv_heads, c.head_dim, self.prefix_slots, ptr(self.work), ptr(self.o),
                                   self.code, s), "attention")
             P["o"].run(dM)
+            if self.tp is not None:
+                self._tp_reduce(dM, mm)
             P["gu"].run(dM)
             P["d"].run(dM)
+            if self.tp is not None:
+                self._tp_reduce(dM, mm)
         plan["lm_head_topk" if topk else "lm_head"].run(rows.n_out)
+        if self.tp is not None:
+            if topk:
+                raise ConfigError("the fused top-k lm_head is a draft path; a tensor-parallel target gathers logits")
+            self._tp_gather_logits()
 
     def launches_per_forward(self) -> int:
         gu_extra = 0
