@@ -243,8 +243,10 @@ int card_attention(const float* q, const int32_t* dM, int m_max, const int32_t* 
 /* Tree / chain attention over a paged KV cache (bf16 K/V and output, head_dim
  * 64 or 128): prefix position p of every row lives in KV slot
  * page_table[p / 64] * 64 + p % 64 (page_table NULL: slot p); extra slots are
- * physical.  tcgen05 (S = QK^T and O = PV in TMEM) — the kernel card_attention
- * uses for bf16 models.  Replaces the tree-mask forward of mask.py:173-217 /
+ * physical.  Wide forwards (>= 256 query-heads per KV head: draft tree rows,
+ * prefill) run the tcgen05 kernel (S = QK^T and O = PV in TMEM); verify / AR
+ * rows the register-resident mma.sync kernel.  The bf16 model forward's
+ * attention.  Replaces the tree-mask forward of mask.py:173-217 /
  * lm.py:155-196. */
 int card_attention_paged(const float* q, const int32_t* dM, int m_max, const int32_t* plen,
                          const int32_t* n_extra, const int32_t* extra, int extra_max, const void* k_cache,
@@ -280,10 +282,14 @@ int card_logit_bias(float* logits, const int32_t* dM, int m_max, int V, const in
  * extra[R*E]] with R = rows_max, E = extra_max. */
 typedef struct card_engine_state card_engine_state;
 int card_engine_state_bytes(void);
+/* page_table (NULL: identity): the run's prefix pages, 64 KV slots each —
+ * chain rows write their K/V to slot page_table[p / 64] * 64 + p % 64. */
 int card_draft_rows(card_engine_state* E, card_cache* h, const int32_t* committed, int32_t* rows,
-                    int rows_max, int extra_max, int tree_base, int32_t* ctx_tail, int order, void* stream);
+                    int rows_max, int extra_max, int tree_base, int32_t* ctx_tail, int order,
+                    const int32_t* page_table, void* stream);
 int card_target_rows(card_engine_state* E, card_cache* h, const int32_t* committed, int32_t* rows,
-                     int rows_max, int extra_max, int32_t* ctx_tail, int order, void* stream);
+                     int rows_max, int extra_max, int32_t* ctx_tail, int order, const int32_t* page_table,
+                     void* stream);
 int card_eos_fix(const int32_t* n_rows, int m_max, const int32_t* ctx_tail, int order, int eos, int V,
                  double* probs, void* stream);
 int card_record_width(card_engine_state* E, card_cache* h, const int32_t* n_out, void* stream);
@@ -307,7 +313,8 @@ int card_verify_result(const card_engine_state* E, int32_t* out, void* stream);
 /* KV rollback / roll-forward of the draft: promote accepted-chain tree KV
  * rows into the prefix; move surviving tree rows after an arena compaction. */
 int card_draft_promote(card_engine_state* E, card_cache* h, void** k_layers, void** v_layers,
-                       int n_layers, int row_elems, int esize, int tree_base, int max_chain, void* stream);
+                       int n_layers, int row_elems, int esize, int tree_base, int max_chain,
+                       const int32_t* page_table, void* stream);
 int card_kv_compact(card_engine_state* E, card_cache* h, void** k_layers, void** v_layers, int n_layers,
                     int row_elems, int esize, int tree_base, void** scratch_kv, int capacity, void* stream);
 int card_cycle_end(card_engine_state* E, card_cache* h, void* stream);

@@ -85,15 +85,15 @@ SIGNATURES = {
                                 ctypes.c_float, _P]),
     # engine
     "card_engine_state_bytes": (c_int, []),
-    "card_draft_rows": (c_int, [_P, _P, _P, _P, c_int, c_int, c_int, _P, c_int, _P]),
-    "card_target_rows": (c_int, [_P, _P, _P, _P, c_int, c_int, _P, c_int, _P]),
+    "card_draft_rows": (c_int, [_P, _P, _P, _P, c_int, c_int, c_int, _P, c_int, _P, _P]),
+    "card_target_rows": (c_int, [_P, _P, _P, _P, c_int, c_int, _P, c_int, _P, _P]),
     "card_eos_fix": (c_int, [_P, c_int, _P, c_int, c_int, c_int, _P, _P]),
     "card_record_width": (c_int, [_P, _P, _P, _P]),
     "card_verify_argmax": (c_int, [_P, _P, _P, _P]),
     "card_verify_probs": (c_int, [_P, _P, _P, c_int, _P, _P, _P]),
     "card_commit": (c_int, [_P, _P, _P]),
     "card_verify_result": (c_int, [_P, _P, _P]),
-    "card_draft_promote": (c_int, [_P, _P, _P, _P, c_int, c_int, c_int, c_int, c_int, _P]),
+    "card_draft_promote": (c_int, [_P, _P, _P, _P, c_int, c_int, c_int, c_int, c_int, _P, _P]),
     "card_kv_compact": (c_int, [_P, _P, _P, _P, c_int, c_int, c_int, c_int, _P, c_int, _P]),
     "card_cycle_end": (c_int, [_P, _P, _P]),
     "card_engine_handoff": (c_int, [_P, _P, _P]),

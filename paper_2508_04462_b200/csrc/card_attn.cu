@@ -98,6 +98,7 @@ template <int HD, int QT>
 __global__ void __launch_bounds__(QT * 2) attn_fused_kernel(const float* __restrict__ q, const int32_t* dM,
                                                              const int32_t* __restrict__ plen,
                                                              const int32_t* __restrict__ slot,
+                                                             const int32_t* __restrict__ page_table,
                                                              const int32_t* __restrict__ n_extra,
                                                              const int32_t* __restrict__ extra, int extra_max,
                                                              const __nv_bfloat16* __restrict__ kc,
@@ -186,11 +187,16 @@ __global__ void __launch_bounds__(QT * 2) attn_fused_kernel(const float* __restr
     const int n_ch = (s_kmax + kCh - 1) / kCh;
     const int n_xch = (s_nx + kCh - 1) / kCh;
     const int n_all = n_ch + n_xch;
+    // prefix position k -> KV slot (pages of 64 slots when page_table is set)
+    auto pslot = [&](int k) { return (int64_t)(page_table ? page_table[k >> 6] * 64 + (k & 63) : k); };
     // this rank's first chunk can be staged before the wait when it is a
-    // prefix chunk below every KV slot this forward writes (slot[0] is the
-    // lowest: catch-up / chain rows come first, tree slots lie above the prefix)
-    const bool prestaged = rank < n_ch && (rank + 1) * kCh <= slot[0];
-    if (prestaged) stage_rows(rank, 0, [](int k) { return (int64_t)k; });
+    // prefix chunk below every position this forward writes (row 0 is the
+    // lowest: catch-up / chain rows come first at position plen - 1; a tree
+    // row 0 means the whole prefix is old)
+    const int old_lim = (n_extra && n_extra[0] > 0) ? 0x7fffffff : plen[0] - 1;
+    (void)slot;
+    const bool prestaged = rank < n_ch && (rank + 1) * kCh <= old_lim;
+    if (prestaged) stage_rows(rank, 0, pslot);
     pdl_wait();
     pdl_trigger();
     at_stamp(1);
@@ -235,7 +241,7 @@ __global__ void __launch_bounds__(QT * 2) attn_fused_kernel(const float* __restr
         if (c >= n_ch)
             stage_rows(c - n_ch, b, [&](int k) { return (int64_t)xs[k < nx ? k : 0]; });
         else
-            stage_rows(c, b, [](int k) { return (int64_t)k; });
+            stage_rows(c, b, pslot);
     };
     if (rank < n_all && !prestaged) stage(rank, 0);
     int buf = 0;
@@ -415,15 +421,16 @@ int attn_fused_smem(int hd, int S, int qt) { return 4 * kCh * (hd + 8) * 2 + S *
 
 template <int HD, int QT>
 static cudaError_t launch_qt(cudaLaunchConfig_t& cfg, const float* q, const int32_t* dM, const int32_t* plen,
-                             const int32_t* slot, const int32_t* n_extra, const int32_t* extra, int extra_max,
-                             const void* kc, const void* vc, int nh, int nkv, void* o) {
+                             const int32_t* slot, const int32_t* page_table, const int32_t* n_extra,
+                             const int32_t* extra, int extra_max, const void* kc, const void* vc, int nh, int nkv,
+                             void* o) {
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(attn_fused_kernel<HD, QT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         cudaFuncSetAttribute(attn_fused_kernel<HD, QT>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         attr = true;
     }
-    return cudaLaunchKernelEx(&cfg, attn_fused_kernel<HD, QT>, q, dM, plen, slot, n_extra, extra, extra_max,
+    return cudaLaunchKernelEx(&cfg, attn_fused_kernel<HD, QT>, q, dM, plen, slot, page_table, n_extra, extra, extra_max,
                               (const __nv_bfloat16*)kc, (const __nv_bfloat16*)vc, nh, nkv, (__nv_bfloat16*)o);
 }
 
@@ -442,6 +449,7 @@ bool attn_fused_fits(int m_max, int nh, int nkv, int extra_max) {
 }
 
 int launch_attn_fused(const float* q, const int32_t* dM, int m_max, const int32_t* plen, const int32_t* slot,
+                      const int32_t* page_table,
                       const int32_t* n_extra, const int32_t* extra, int extra_max, const void* kc, const void* vc,
                       int nh, int nkv, int hd, int max_plen, void* o, cudaStream_t s) {
     const int G = nh / nkv;
@@ -472,11 +480,11 @@ int launch_attn_fused(const float* q, const int32_t* dM, int m_max, const int32_
     cfg.numAttrs = 2;
     cudaError_t e;
     if (hd == 64)
-        e = QT == 128 ? launch_qt<64, 128>(cfg, q, dM, plen, slot, n_extra, extra, extra_max, kc, vc, nh, nkv, o)
-                      : launch_qt<64, 64>(cfg, q, dM, plen, slot, n_extra, extra, extra_max, kc, vc, nh, nkv, o);
+        e = QT == 128 ? launch_qt<64, 128>(cfg, q, dM, plen, slot, page_table, n_extra, extra, extra_max, kc, vc, nh, nkv, o)
+                      : launch_qt<64, 64>(cfg, q, dM, plen, slot, page_table, n_extra, extra, extra_max, kc, vc, nh, nkv, o);
     else
-        e = QT == 128 ? launch_qt<128, 128>(cfg, q, dM, plen, slot, n_extra, extra, extra_max, kc, vc, nh, nkv, o)
-                      : launch_qt<128, 64>(cfg, q, dM, plen, slot, n_extra, extra, extra_max, kc, vc, nh, nkv, o);
+        e = QT == 128 ? launch_qt<128, 128>(cfg, q, dM, plen, slot, page_table, n_extra, extra, extra_max, kc, vc, nh, nkv, o)
+                      : launch_qt<128, 64>(cfg, q, dM, plen, slot, page_table, n_extra, extra, extra_max, kc, vc, nh, nkv, o);
     if (e != cudaSuccess) {
         set_cuda_error(e);
         return CARD_E_CUDA;

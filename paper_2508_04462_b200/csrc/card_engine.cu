@@ -46,11 +46,15 @@ typedef struct card_engine_state {
 
 namespace card {
 
+// prefix position -> KV slot: pages of 64 slots through the run's page table
+// (NULL: identity); tree slots are tree_base + node id
+__device__ __forceinline__ int pslot(const int32_t* pt, int p) { return pt ? pt[p >> 6] * 64 + (p & 63) : p; }
+
 // ---------------------------------------------------------------- row builders
 __global__ void draft_rows_kernel(card_engine_state* E, const card_cache_state* S, const int32_t* __restrict__ ntoken,
                                   const int32_t* __restrict__ nparent, const int32_t* __restrict__ nlayer,
                                   const int32_t* __restrict__ frontier, const int32_t* __restrict__ committed,
-                                  CardRows R, int tree_base, int32_t* ctx_tail, int order) {
+                                  CardRows R, int tree_base, int32_t* ctx_tail, int order, const int32_t* pt) {
     // one thread per catch-up row and per frontier row (the ancestor walks of
     // the frontier nodes run in parallel)
     const int tid = threadIdx.x;
@@ -73,7 +77,7 @@ __global__ void draft_rows_kernel(card_engine_state* E, const card_cache_state* 
             const int m = p - start;
             R.tok[m] = committed[p];
             R.pos[m] = p;
-            R.slot[m] = p;
+            R.slot[m] = pslot(pt, p);
             R.plen[m] = p + 1;
             R.n_extra[m] = 0;
         }
@@ -96,7 +100,7 @@ __global__ void draft_rows_kernel(card_engine_state* E, const card_cache_state* 
         const int p = Pd + i;
         R.tok[i] = committed[p];
         R.pos[i] = p;
-        R.slot[i] = p;
+        R.slot[i] = pslot(pt, p);
         R.plen[i] = p + 1;
         R.n_extra[i] = 0;
     }
@@ -140,7 +144,8 @@ __global__ void draft_rows_kernel(card_engine_state* E, const card_cache_state* 
 }
 
 __global__ void target_rows_kernel(card_engine_state* E, const card_cache_state* S, const int32_t* __restrict__ q_tok,
-                                   const int32_t* __restrict__ committed, CardRows R, int32_t* ctx_tail, int order) {
+                                   const int32_t* __restrict__ committed, CardRows R, int32_t* ctx_tail, int order,
+                                   const int32_t* pt) {
     if (threadIdx.x != 0) return;
     if (E->done) {
         *R.M = 0;
@@ -155,7 +160,7 @@ __global__ void target_rows_kernel(card_engine_state* E, const card_cache_state*
         const int p = C - 1 + i;
         R.tok[i] = i == 0 ? committed[C - 1] : q_tok[i - 1];
         R.pos[i] = p;
-        R.slot[i] = p;
+        R.slot[i] = pslot(pt, p);
         R.plen[i] = p + 1;
         R.n_extra[i] = 0;
         R.out_rows[i] = i;
@@ -438,14 +443,14 @@ __device__ __forceinline__ void copy_row(const KVPtrs& P, int layer, int64_t src
 // grid (n_layers, max_chain): run length of KV-bearing chain nodes starting
 // at the current draft prefix end is promoted into the prefix region.
 __global__ void draft_promote_kernel(card_engine_state* E, const card_cache_state* S, const int32_t* chain,
-                                     const int32_t* chain_kv, KVPtrs P, int tree_base) {
+                                     const int32_t* chain_kv, KVPtrs P, int tree_base, const int32_t* pt) {
     if (E->done) return;
     const int j = blockIdx.y;
     const int clen = S->chain_len;
     if (E->Pd != E->C_prev || j >= clen) return;
     for (int i = 0; i <= j; ++i)
         if (!chain_kv[i]) return;
-    copy_row(P, blockIdx.x, (int64_t)tree_base + chain[j], (int64_t)E->C_prev + j);
+    copy_row(P, blockIdx.x, (int64_t)tree_base + chain[j], (int64_t)pslot(pt, E->C_prev + j));
 }
 
 __global__ void draft_promote_finish_kernel(card_engine_state* E, const card_cache_state* S, const int32_t* chain_kv) {
@@ -550,7 +555,8 @@ int card_engine_state_bytes(void) { return (int)sizeof(card_engine_state); }
 
 // rows: int32 block [M, n_out, tok[rm], pos[rm], slot[rm], plen[rm], n_extra[rm], out_rows[rm], extra[rm*em]]
 int card_draft_rows(card_engine_state* E, card_cache* h, const int32_t* committed, int32_t* rows, int rows_max,
-                    int extra_max, int tree_base, int32_t* ctx_tail, int order, void* stream) {
+                    int extra_max, int tree_base, int32_t* ctx_tail, int order, const int32_t* page_table,
+                    void* stream) {
     card_cache_state* S;
     int32_t *tok, *par, *lay, *fr;
     int rc = card_cache_device_ptrs(h, &S, &tok, &par, &lay, &fr, nullptr, nullptr, nullptr);
@@ -559,13 +565,13 @@ int card_draft_rows(card_engine_state* E, card_cache* h, const int32_t* committe
     CardRows R = make_rows(rows, rows + 1, rows + 2, rows + 2 + rm, rows + 2 + 2 * rm, rows + 2 + 3 * rm,
                            rows + 2 + 4 * rm, rows + 2 + 6 * rm, rows + 2 + 5 * rm, rm, extra_max);
     draft_rows_kernel<<<1, 128, 0, (cudaStream_t)stream>>>(E, S, tok, par, lay, fr, committed, R, tree_base, ctx_tail,
-                                                         order);
+                                                         order, page_table);
     CARD_LAUNCH_CHECK();
     return CARD_OK;
 }
 
 int card_target_rows(card_engine_state* E, card_cache* h, const int32_t* committed, int32_t* rows, int rows_max,
-                     int extra_max, int32_t* ctx_tail, int order, void* stream) {
+                     int extra_max, int32_t* ctx_tail, int order, const int32_t* page_table, void* stream) {
     card_cache_state* S;
     int rc = card_cache_device_ptrs(h, &S, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr);
     if (rc) return rc;
@@ -575,7 +581,7 @@ int card_target_rows(card_engine_state* E, card_cache* h, const int32_t* committ
     const int rm = rows_max;
     CardRows R = make_rows(rows, rows + 1, rows + 2, rows + 2 + rm, rows + 2 + 2 * rm, rows + 2 + 3 * rm,
                            rows + 2 + 4 * rm, rows + 2 + 6 * rm, rows + 2 + 5 * rm, rm, extra_max);
-    target_rows_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(E, S, qt, committed, R, ctx_tail, order);
+    target_rows_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(E, S, qt, committed, R, ctx_tail, order, page_table);
     CARD_LAUNCH_CHECK();
     return CARD_OK;
 }
@@ -637,13 +643,14 @@ int card_verify_result(const card_engine_state* E, int32_t* out, void* stream) {
 }
 
 int card_draft_promote(card_engine_state* E, card_cache* h, void** k_layers, void** v_layers, int n_layers,
-                       int row_elems, int esize, int tree_base, int max_chain, void* stream) {
+                       int row_elems, int esize, int tree_base, int max_chain, const int32_t* page_table,
+                       void* stream) {
     card_cache_state* S;
     int32_t *chain, *chain_kv;
     card_cache_device_ptrs(h, &S, nullptr, nullptr, nullptr, nullptr, nullptr, &chain, &chain_kv);
     KVPtrs P{k_layers, v_layers, n_layers, row_elems, esize};
     dim3 g(n_layers, max_chain);
-    draft_promote_kernel<<<g, 128, 0, (cudaStream_t)stream>>>(E, S, chain, chain_kv, P, tree_base);
+    draft_promote_kernel<<<g, 128, 0, (cudaStream_t)stream>>>(E, S, chain, chain_kv, P, tree_base, page_table);
     draft_promote_finish_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(E, S, chain_kv);
     CARD_LAUNCH_CHECK();
     return CARD_OK;

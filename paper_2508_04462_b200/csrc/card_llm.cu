@@ -1038,7 +1038,7 @@ int card_attention(const float* q, const int32_t* dM, int m_max, const int32_t* 
                               o, s);
     if (kvdtype == 0 && odtype == 0 && (hd == 64 || hd == 128) &&
         attn_fused_fits(m_max, nh, nkv, extra_max))
-        if (slot) return launch_attn_fused(q, dM, m_max, plen, slot, n_extra, extra, extra_max, kc, vc, nh, nkv, hd,
+        if (slot) return launch_attn_fused(q, dM, m_max, plen, slot, nullptr, n_extra, extra, extra_max, kc, vc, nh, nkv, hd,
                                            max_plen, o, s);
     dim3 g1(nkv, n_splits);
     const int ew = (m_max * nh + 7) / 8;
@@ -1072,9 +1072,20 @@ int card_attention_paged(const float* q, const int32_t* dM, int m_max, const int
                          const void* vc, const int32_t* page_table, int nh, int nkv, int hd, int max_plen,
                          void* o, void* stream) {
     if (!q || !dM || !plen || !kc || !vc || !o || m_max <= 0 || nkv <= 0 || nh % nkv) return CARD_E_INPUT;
-    if (!attn_tc_fits(m_max, nh, nkv, hd, extra_max)) return CARD_E_CONFIG;
-    const int rc = launch_attn_tc(q, dM, m_max, plen, n_extra, extra, extra_max, kc, vc, page_table, nh, nkv, hd,
-                                  max_plen, o, (cudaStream_t)stream);
+    cudaStream_t s = (cudaStream_t)stream;
+    int rc;
+    // same shape dispatch as card_attention (wide -> tcgen05, narrow -> mma.sync)
+    if (m_max * (nh / nkv) >= 256 && attn_tc_fits(m_max, nh, nkv, hd, extra_max))
+        rc = launch_attn_tc(q, dM, m_max, plen, n_extra, extra, extra_max, kc, vc, page_table, nh, nkv, hd, max_plen,
+                            o, s);
+    else if ((hd == 64 || hd == 128) && attn_fused_fits(m_max, nh, nkv, extra_max))
+        rc = launch_attn_fused(q, dM, m_max, plen, nullptr, page_table, n_extra, extra, extra_max, kc, vc, nh, nkv, hd,
+                               max_plen, o, s);
+    else if (attn_tc_fits(m_max, nh, nkv, hd, extra_max))
+        rc = launch_attn_tc(q, dM, m_max, plen, n_extra, extra, extra_max, kc, vc, page_table, nh, nkv, hd, max_plen,
+                            o, s);
+    else
+        return CARD_E_CONFIG;
     if (rc == CARD_OK) CARD_LAUNCH_CHECK();
     return rc;
 }

@@ -9,6 +9,7 @@
 namespace card {
 // fused attention (card_attn.cu): prefix chunks + tree extras + cluster combine
 int launch_attn_fused(const float* q, const int32_t* dM, int m_max, const int32_t* plen, const int32_t* slot,
+                      const int32_t* page_table,
                       const int32_t* n_extra,
                       const int32_t* extra, int extra_max, const void* kc, const void* vc, int nh, int nkv, int hd,
                       int max_plen, void* o, cudaStream_t s);

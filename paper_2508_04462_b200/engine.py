@@ -227,14 +227,17 @@ class _LlamaAdapter:
             if getattr(run, "private_runtimes", False):   # batched requests: own KV cache and buffers, shared weights
                 from .llama import DeviceLlama
 
-                self.rt = DeviceLlama(model.cfg, model.packed, max_ctx=run.max_ctx, tree_slots=tree_slots,
-                                      row_budgets=sorted(budgets))
+                self.rt = DeviceLlama(model.shard_cfg, model.packed, max_ctx=run.max_ctx, tree_slots=tree_slots,
+                                      row_budgets=sorted(budgets), pool_requests=1)
             else:
                 self.rt = model.runtime(run.max_ctx, tree_slots, budgets)
         if self.rt.dev != dev:
             raise ConfigError(f"the {role} model lives on {self.rt.dev}, the run places it on {dev}")
         if self.rt.extra_max < run.cfg.max_depth + 1:
             raise ConfigError("max_depth too large for the tree-attention extra-slot budget")
+        # this request's prefix KV pages (returned to the runtime's pool with the adapter)
+        with torch.cuda.device(dev):
+            self.pages = self.rt.page_table(dev)
         V = model.vocab.size
         self.V = V
         self.k = run.cfg.k
@@ -293,8 +296,8 @@ class _LlamaAdapter:
         nbytes = 0
         for s in range(0, len(tokens), PREFILL_CHUNK):
             chunk = tokens[s:s + PREFILL_CHUNK]
-            nbytes += self.prefill_rows.set_chain(chunk, s)
-            self.rt.forward(self.prefill_rows, PREFILL_CHUNK)
+            nbytes += self.prefill_rows.set_chain(chunk, s, pages=self.pages)
+            self.rt.forward(self.prefill_rows, PREFILL_CHUNK, pages=self.pages)
         return nbytes
 
     def _fused_lm_head(self):
@@ -319,7 +322,7 @@ class _LlamaAdapter:
             L_ = lib()
             raise_for_status(L_.card_linear_fuse_kgram(head.h, *bias), "fuse_kgram")
             raise_for_status(L_.card_linear_fuse_topk(head.h, self.V, 1.0 / run.t_score), "fuse_topk")
-            self.rt.forward(rows, self.rows_max, topk=True)
+            self.rt.forward(rows, self.rows_max, topk=True, pages=self.pages)
             raise_for_status(L_.card_lmhead_topk_merge(ptr(head.work), ptr(rows.n_out), self.rows_max, head.n_tiles,
                                                        self.k, self.V, ptr(self.tok), ptr(self.logp), ptr(self.cnt),
                                                        stream_ptr()), "lmhead_topk_merge")
@@ -330,7 +333,7 @@ class _LlamaAdapter:
             # only: the plan is shared by every run of this model)
             raise_for_status(lib().card_linear_fuse_kgram(lm.h, *bias), "fuse_kgram")
         try:
-            self.rt.forward(rows, self.rows_max)
+            self.rt.forward(rows, self.rows_max, pages=self.pages)
         finally:
             if lm is not None:
                 raise_for_status(lib().card_linear_fuse_kgram(lm.h, None, 0, 0, 0, 0, 0.0, 0.0), "fuse_kgram")
@@ -344,7 +347,7 @@ class _LlamaAdapter:
 
     def target(self, run):
         rows = run.trt.rows
-        self.rt.forward(rows, self.rows_max)
+        self.rt.forward(rows, self.rows_max, pages=self.pages)
         L_ = lib()
         if run.sampling:
             self._bias(run.trt)
@@ -368,10 +371,16 @@ class _LlamaAdapter:
         nL = self.m.cfg.n_layers
         raise_for_status(L_.card_draft_promote(run.Ed_ptr, run.cache.handle, ptr(rt.k_ptrs), ptr(rt.v_ptrs), nL,
                                                rt.kv_row_elems(), rt.kv_esize(), rt.tree_base, run.cfg.max_depth + 2,
-                                               stream_ptr()), "draft_promote")
+                                               _pt(self), stream_ptr()), "draft_promote")
         raise_for_status(L_.card_kv_compact(run.Ed_ptr, run.cache.handle, ptr(rt.k_ptrs), ptr(rt.v_ptrs), nL,
                                             rt.kv_row_elems(), rt.kv_esize(), rt.tree_base, ptr(self.scratch_ptrs),
                                             run.cache_capacity, stream_ptr()), "kv_compact")
+
+
+def _pt(adapter):
+    """Device page table of an adapter's request (None: identity / no KV)."""
+    pages = getattr(adapter, "pages", None)
+    return ptr(pages.dev) if pages is not None else None
 
 
 def _adapter(model, role, run, rows_max):
@@ -534,7 +543,7 @@ class DeviceRun:
         raise_for_status(L_.card_draft_rows(self.Ed_ptr, self.cache.handle, ptr(self.committed), ptr(self.drt.rows.block),
                                             self.d_rows_max, self.drt.rows.extra_max,
                                             getattr(self.da, "rt", None).tree_base if hasattr(self.da, "rt") else 0,
-                                            ptr(self.drt.tail), self.drt.order, s), "draft_rows")
+                                            ptr(self.drt.tail), self.drt.order, _pt(self.da), s), "draft_rows")
         tok, val, cnt, probs = self.da.draft(self)
         raise_for_status(L_.card_cache_expand_topk(self.cache.handle, ptr(tok), ptr(val), ptr(cnt), -1, probs,
                                                    self._fptr("stop", True), s), "expand")
@@ -547,7 +556,7 @@ class DeviceRun:
             raise_for_status(L_.card_cache_query(self.cache.handle, self.cfg.query_depth, s), "query")
         raise_for_status(L_.card_target_rows(self.E_ptr, self.cache.handle, ptr(self.committed),
                                              ptr(self.trt.rows.block), self.t_rows_max, 1, ptr(self.trt.tail),
-                                             self.trt.order, s), "target_rows")
+                                             self.trt.order, _pt(self.ta), s), "target_rows")
         self.ta.target(self)
         raise_for_status(L_.card_commit(self.E_ptr, ptr(self.committed), s), "commit")
         if with_correct:
@@ -1114,7 +1123,8 @@ class VanillaRun:
         L_ = lib()
         s = stream_ptr()
         raise_for_status(L_.card_target_rows(self.E_ptr, self.cache.handle, ptr(self.committed),
-                                             ptr(self.trt.rows.block), 1, 1, ptr(self.trt.tail), self.trt.order, s),
+                                             ptr(self.trt.rows.block), 1, 1, ptr(self.trt.tail), self.trt.order,
+                                             _pt(self.ta), s),
                          "target_rows")
         self.ta.target(self)
         raise_for_status(L_.card_commit(self.E_ptr, ptr(self.committed), s), "commit")

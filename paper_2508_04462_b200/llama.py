@@ -278,6 +278,56 @@ class _Linear:
             pass
 
 
+PAGE = 64   # KV slots per page
+
+
+class PagePool:
+    """Free list of the prefix KV pages of one runtime.  Every request
+    (DeviceRun / VanillaRun) takes the pages of its context from here and
+    returns them when it is dropped; its page table maps logical page i of
+    its context to a physical page.  Pages come out lowest-first, so a
+    fragmented pool hands a request scattered, out-of-order pages — which
+    the kernels (row builders, attention, KV promotion) only ever see
+    through the table."""
+
+    def __init__(self, n_pages: int):
+        self.n_pages = n_pages
+        self.free = list(range(n_pages))
+
+    def alloc(self, n: int) -> list[int]:
+        if n > len(self.free):
+            import gc
+
+            gc.collect()   # runs that died in reference cycles give their pages back
+        if n > len(self.free):
+            raise ConfigError(f"KV page pool exhausted: {n} pages wanted, {len(self.free)} of {self.n_pages} free")
+        self.free.sort()
+        out, self.free = self.free[:n], self.free[n:]
+        return out
+
+    def release(self, pages) -> None:
+        self.free.extend(int(p) for p in pages)
+
+
+class PageTable:
+    """One request's pages (host list + device int32 table); returns them to
+    the pool when collected."""
+
+    def __init__(self, pool: PagePool, n_pages: int, device):
+        self.pool = pool
+        self.pages = pool.alloc(n_pages)
+        self.dev = torch.tensor(self.pages, dtype=torch.int32, device=device)
+
+    def slot(self, p: int) -> int:
+        return self.pages[p // PAGE] * PAGE + p % PAGE
+
+    def __del__(self):
+        try:
+            self.pool.release(self.pages)
+        except Exception:
+            pass
+
+
 class DeviceLlama:
     """One draft or target model resident in HBM with its KV cache.
 
@@ -288,7 +338,7 @@ class DeviceLlama:
     """
 
     def __init__(self, cfg: LlamaConfig, packed: dict, *, max_ctx: int, tree_slots: int = 0,
-                 row_budgets=(1,), extra_max: int = 32, tp=None):
+                 row_budgets=(1,), extra_max: int = 32, tp=None, pool_requests: int = 8):
         """tp: (comm, shards, full_vocab) of a tensor-parallel target rank (tp.py):
         cfg is then the rank's shard; o / down write partials that are
         all-reduced before the residual add, and the vocabulary slices of
@@ -301,9 +351,13 @@ class DeviceLlama:
         self.wdt = torch.bfloat16 if dtype == "bf16" else torch.float32
         self.code = 0 if dtype == "bf16" else 1
         self.max_ctx = max_ctx
-        self.prefix_slots = ((max_ctx + 63) // 64) * 64
-        self.tree_base = self.prefix_slots
-        self.n_slots = self.prefix_slots + tree_slots
+        self.prefix_slots = ((max_ctx + 63) // 64) * 64      # longest context (logical positions)
+        # paged prefix KV (bf16 path): a pool for pool_requests contexts, handed
+        # out page by page to the requests on this runtime (PagePool)
+        self.pool_pages = (self.prefix_slots // PAGE) * pool_requests
+        self.page_pool = PagePool(self.pool_pages)
+        self.tree_base = self.pool_pages * PAGE
+        self.n_slots = self.tree_base + tree_slots
         self.tree_slots = tree_slots
         self.extra_max = extra_max
         c = cfg
@@ -434,16 +488,25 @@ class DeviceLlama:
         return 2 if self.dtype == "bf16" else 4
 
     # ------------------------------------------------------------ forward
-    def forward(self, rows: "RowBlock", m_max: int, topk: bool = False):
+    def page_table(self, device=None) -> "PageTable | None":
+        """Pages for one request's context (bf16 path); None on the fp32 parity
+        path, which addresses its KV by position."""
+        if not self.fused:
+            return None
+        return PageTable(self.page_pool, self.prefix_slots // PAGE, device or self.dev)
+
+    def forward(self, rows: "RowBlock", m_max: int, topk: bool = False, pages: "PageTable | None" = None):
         """Run the forward over the device rows; logits for the output rows
         land in self.logits[:n_out] (topk=True: the lm_head_topk records
-        instead, see lm_topk_head).  Asynchronous, graph-capturable."""
+        instead, see lm_topk_head).  pages: the request's page table (the
+        rows' KV slots were built through it); None = identity.
+        Asynchronous, graph-capturable."""
         c = self.cfg
         L_ = lib()
         s = stream_ptr()
         plan = self.plans[m_max]
         if self.fused:
-            return self._forward_fused(rows, plan, topk)
+            return self._forward_fused(rows, plan, topk, pages)
         if topk:
             raise ConfigError("the fused top-k lm_head needs the bf16 path")
         dM, dOut = rows.M, rows.n_out
@@ -489,7 +552,7 @@ class DeviceLlama:
             plan["bound_rows"] = None   # rebind the row offset of the new head
         return lin
 
-    def _forward_fused(self, rows: "RowBlock", plan: dict, topk: bool = False):
+    def _forward_fused(self, rows: "RowBlock", plan: dict, topk: bool = False, pages: "PageTable | None" = None):
         c = self.cfg
         L_ = lib()
         s = stream_ptr()
@@ -501,10 +564,10 @@ class DeviceLlama:
                           ptr(self.ssq), self.mpad, s), "embed")
         for li, P in enumerate(plan["layers"]):
             P["qkv"].run(dM)
-            chk(L_.card_attention(ptr(self.q), ptr(dM), mm, ptr(rows.plen), ptr(rows.slot), ptr(rows.n_extra), ptr(rows.extra),
-                                  rows.extra_max, ptr(self.k_cache[li]), ptr(self.v_cache[li]), self.code,
-                                  c.n_heads, c.n_kv_heads, c.head_dim, self.prefix_slots, ptr(self.work), ptr(self.o),
-                                  self.code, s), "attention")
+            chk(L_.card_attention_paged(ptr(self.q), ptr(dM), mm, ptr(rows.plen), ptr(rows.n_extra), ptr(rows.extra),
+                                        rows.extra_max, ptr(self.k_cache[li]), ptr(self.v_cache[li]),
+                                        ptr(pages.dev) if pages is not None else None, c.n_heads, c.n_kv_heads,
+                                        c.head_dim, self.prefix_slots, ptr(self.o), s), "attention")
             P["o"].run(dM)
             if self.tp is not None:
                 self._tp_reduce(dM, mm)
@@ -543,9 +606,10 @@ class RowBlock:
         self.out_rows = b[2 + 5 * R:2 + 6 * R]
         self.extra = b[2 + 6 * R:]
 
-    def set_chain(self, tokens, start_pos: int, out_last_only=True) -> int:
-        """Host helper: causal chain rows (prefill / AR decode); returns the
-        bytes copied to the device."""
+    def set_chain(self, tokens, start_pos: int, out_last_only=True, pages: "PageTable | None" = None) -> int:
+        """Host helper: causal chain rows (prefill / AR decode), KV slots
+        through the request's page table; returns the bytes copied to the
+        device."""
         n = len(tokens)
         assert n <= self.rows_max
         host = torch.zeros(2 + 6 * self.rows_max, dtype=torch.int32)
@@ -555,7 +619,8 @@ class RowBlock:
         host[2:2 + n] = torch.tensor(tokens, dtype=torch.int32)
         pos = torch.arange(start_pos, start_pos + n, dtype=torch.int32)
         host[2 + R:2 + R + n] = pos
-        host[2 + 2 * R:2 + 2 * R + n] = pos
+        host[2 + 2 * R:2 + 2 * R + n] = pos if pages is None else \
+            torch.tensor([pages.slot(p) for p in range(start_pos, start_pos + n)], dtype=torch.int32)
         host[2 + 3 * R:2 + 3 * R + n] = pos + 1
         if out_last_only:
             host[2 + 5 * R] = n - 1
