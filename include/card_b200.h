@@ -217,6 +217,38 @@ int card_lmhead_topk_merge(const float* work, const int32_t* dM, int m_max, int 
 int card_linear_trace(card_linear* h, unsigned long long* trace);
 int card_linear_destroy(card_linear* h);
 
+/* Persistent wide forward (draft tree steps, 16 < m_max <= 128 rows; bf16,
+ * folded norms).  One CTA per SM walks steps = (layer, phase), phase 0 qkv,
+ * 1 attention, 2 o, 3 gate/up, 4 down: weight blocks stream into a ring across
+ * step boundaries, split-K partials meet in an L2 workspace and are reduced
+ * in fixed split order with the qkv (RoPE, KV write) / residual / SwiGLU
+ * epilogues of card_linear_fuse_*.  Replaces the per-GEMM launches of the
+ * draft forward behind lm.py:155-196 batch_tree_forward (engine.py:198-221).
+ * layer_w: host array [n_layers*4] of pre-tiled wqkv, wo, wgu (interleaved),
+ * wd; bqkv: host array [n_layers] (NULL: no bias); kv: [n_layers*2] k, v
+ * caches [slots, nkv, hd] bf16.  Buffers as the fused forward's (x fp32
+ * [rows,H], xb bf16 [rows,H], ssq [H/16][ssq_ld], q fp32 [rows, nh*hd],
+ * o bf16 [rows, nh*hd], g bf16 [rows, F]); act_rows = their row count.
+ * card_pfwd_run executes steps [step_begin, step_end) on the stream (a
+ * cooperative launch); attention steps are run by card_attention_paged between
+ * runs, so a range must not contain one (CARD_E_CONFIG). */
+typedef struct card_pfwd card_pfwd;
+int card_pfwd_create(int n_layers, int H, int F, int nh, int nkv, int hd, int m_max, const void* const* layer_w,
+                     const float* const* bqkv, void* const* kv, float* x, void* xb, float* ssq, int ssq_ld, float* q,
+                     void* o, void* g, int act_rows, const int32_t* pos, const int32_t* slot, const float* cos_t,
+                     const float* sin_t, float eps, card_pfwd** out);
+int card_pfwd_run(card_pfwd* h, const int32_t* dM, int step_begin, int step_end, void* stream);
+/* rebind the row block's positions and KV slots (qkv epilogue) */
+int card_pfwd_bind(card_pfwd* h, const int32_t* pos, const int32_t* slot);
+/* info16: grid, smem, weight stages, activation stages, Mpad, then (splits,
+ * units) per phase */
+int card_pfwd_info(card_pfwd* h, int32_t* info16);
+/* tuning: per-CTA %globaltimer stamps [grid][2 + 4 * steps] of the next runs (NULL disables) */
+int card_pfwd_trace(card_pfwd* h, unsigned long long* trace);
+/* tuning: split-K ways (1..10) of one GEMM phase (0 qkv, 2 o, 4 down) */
+int card_pfwd_tune(card_pfwd* h, int phase, int splits);
+int card_pfwd_destroy(card_pfwd* h);
+
 /* x[r] = E[tok[r]] (fp32 residual); if xb != NULL also its bf16 copy and the
  * per-16-column sums of squares ssq[(col/16)*ssq_ld + r] (fused-norm input) */
 /* Tensor-parallel target: after the NCCL all-reduce of a

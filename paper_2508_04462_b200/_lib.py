@@ -65,6 +65,14 @@ SIGNATURES = {
     "card_linear_fuse_topk": (c_int, [_P, c_int, ctypes.c_float]),
     "card_lmhead_topk_merge": (c_int, [_P, _P, c_int, c_int, c_int, c_int, _P, _P, _P, _P]),
     "card_linear_destroy": (c_int, [_P]),
+    "card_pfwd_create": (c_int, [c_int, c_int, c_int, c_int, c_int, c_int, c_int, _P, _P, _P, _P, _P, _P, c_int, _P,
+                                 _P, _P, c_int, _P, _P, _P, _P, ctypes.c_float, POINTER(c_void_p)]),
+    "card_pfwd_run": (c_int, [_P, _P, c_int, c_int, _P]),
+    "card_pfwd_info": (c_int, [_P, _P]),
+    "card_pfwd_bind": (c_int, [_P, _P, _P]),
+    "card_pfwd_trace": (c_int, [_P, _P]),
+    "card_pfwd_tune": (c_int, [_P, c_int, c_int]),
+    "card_pfwd_destroy": (c_int, [_P]),
     "card_embed": (c_int, [_P, _P, c_int, _P, c_int, c_int, _P, _P, _P, c_int, _P]),
     "card_resid_add": (c_int, [_P, c_int, c_int, _P, _P, _P, _P, c_int, _P]),
     "card_rmsnorm": (c_int, [_P, _P, c_int, ctypes.c_float, _P, c_int, _P, _P, c_int, _P]),

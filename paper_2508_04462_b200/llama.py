@@ -328,6 +328,55 @@ class PageTable:
             pass
 
 
+class _PFwd:
+    """Persistent wide forward (csrc/card_pfwd.cu): the o / gate-up / down /
+    next-qkv GEMMs of a layer in one cooperative launch, weights streaming
+    across the step boundaries.  Used for wide row budgets (draft tree steps)."""
+
+    PHASES = 5   # qkv, attention, o, gate/up, down
+
+    def __init__(self, rt: "DeviceLlama", m_max: int):
+        c = rt.cfg
+        n = c.n_layers
+        W = (ctypes.c_void_p * (4 * n))()
+        B = (ctypes.c_void_p * n)()
+        KV = (ctypes.c_void_p * (2 * n))()
+        for i, L in enumerate(rt.layers):
+            for j, key in enumerate(("wqkv", "wo", "wgu", "wd")):
+                W[4 * i + j] = ptr(L[key])
+            B[i] = ptr(L["bqkv"]) if L["bqkv"] is not None else None
+            KV[2 * i], KV[2 * i + 1] = ptr(rt.k_cache[i]), ptr(rt.v_cache[i])
+        h = ctypes.c_void_p()
+        rc = lib().card_pfwd_create(n, c.hidden, c.ffn, c.n_heads, c.n_kv_heads, c.head_dim, m_max,
+                                    ctypes.cast(W, ctypes.c_void_p), ctypes.cast(B, ctypes.c_void_p),
+                                    ctypes.cast(KV, ctypes.c_void_p), ptr(rt.x), ptr(rt.xb), ptr(rt.ssq), rt.mpad,
+                                    ptr(rt.q), ptr(rt.o), ptr(rt.g), rt.mpad, ptr(rt.rows_placeholder),
+                                    ptr(rt.rows_placeholder), ptr(rt.cos), ptr(rt.sin), c.rms_eps, ctypes.byref(h))
+        raise_for_status(rc, f"card_pfwd_create(m_max={m_max})")
+        self.h = h
+        self.n_layers = n
+
+    def bind(self, rows: "RowBlock"):
+        raise_for_status(lib().card_pfwd_bind(self.h, ptr(rows.pos), ptr(rows.slot)), "card_pfwd_bind")
+
+    def run(self, dM: torch.Tensor, step_begin: int, step_end: int):
+        raise_for_status(lib().card_pfwd_run(self.h, ptr(dM), step_begin, step_end, stream_ptr()), "card_pfwd_run")
+
+    def info(self) -> dict:
+        buf = (ctypes.c_int32 * 16)()
+        lib().card_pfwd_info(self.h, ctypes.cast(buf, ctypes.c_void_p))
+        names = ("qkv", "attn", "o", "gu", "d")
+        return {"grid": buf[0], "smem": buf[1], "w_stages": buf[2], "x_stages": buf[3], "Mpad": buf[4],
+                "splits": {names[p]: buf[5 + 2 * p] for p in range(5) if p != 1}}
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                lib().card_pfwd_destroy(self.h)
+        except Exception:
+            pass
+
+
 class DeviceLlama:
     """One draft or target model resident in HBM with its KV cache.
 
@@ -338,13 +387,16 @@ class DeviceLlama:
     """
 
     def __init__(self, cfg: LlamaConfig, packed: dict, *, max_ctx: int, tree_slots: int = 0,
-                 row_budgets=(1,), extra_max: int = 32, tp=None, pool_requests: int = 8):
+                 row_budgets=(1,), extra_max: int = 32, tp=None, pool_requests: int = 8,
+                 persistent: bool = True):
         """tp: (comm, shards, full_vocab) of a tensor-parallel target rank (tp.py):
         cfg is then the rank's shard; o / down write partials that are
         all-reduced before the residual add, and the vocabulary slices of
         the lm_head are summed into full-vocabulary logits."""
         self.dev = require_cuda()
         self.tp = tp
+        # wide row budgets (draft tree steps) run the persistent forward (_PFwd)
+        self.persistent = persistent
         dtype = packed["dtype"]
         self.cfg = cfg
         self.dtype = dtype
@@ -404,6 +456,7 @@ class DeviceLlama:
         self.v_ptrs = torch.tensor([t.data_ptr() for t in self.v_cache], dtype=torch.int64, device=dev)
         if tp is not None and not self.fused:
             raise ConfigError("the tensor-parallel target runs the fused bf16 path (head_dim 64/128, 128-aligned shards)")
+        self.rows_placeholder = torch.zeros(P, dtype=torch.int32, device=dev)
         self.plans = {m: self._make_plan(m) for m in sorted(set(row_budgets))}
 
     # ------------------------------------------------------------ plans
@@ -449,6 +502,8 @@ class DeviceLlama:
             plan["layers"].append({"qkv": qkv, "o": o, "gu": gu, "d": d})
         plan["lm_head"] = _Linear(self.lm_head, self.xb, m_max, EPI_STORE_F32,
                                   self.logits if self.tp is None else self.logits_local, c.vocab_size)
+        if self.persistent and self.tp is None and 16 < m_max <= 128:
+            plan["pfwd"] = _PFwd(self, m_max)
         return plan
 
     def _tp_reduce(self, dM, mm):
@@ -477,6 +532,8 @@ class DeviceLlama:
             P_["qkv"].fuse_rope(rows, self.cos, self.sin, c.n_heads, c.n_kv_heads, c.head_dim, self.q,
                                 self.k_cache[li], self.v_cache[li])
         plan["lm_head"].fuse_norm(self.ssq, c.hidden // 16, self.mpad, c.rms_eps, c.hidden, rows.out_rows)
+        if "pfwd" in plan:
+            plan["pfwd"].bind(rows)
         if "lm_head_topk" in plan:
             plan["lm_head_topk"].fuse_norm(self.ssq, c.hidden // 16, self.mpad, c.rms_eps, c.hidden, rows.out_rows)
         plan["bound_rows"] = key
@@ -562,6 +619,20 @@ class DeviceLlama:
         chk = raise_for_status
         chk(L_.card_embed(ptr(rows.tok), ptr(dM), mm, ptr(self.embed), self.code, c.hidden, ptr(self.x), ptr(self.xb),
                           ptr(self.ssq), self.mpad, s), "embed")
+        pf = plan.get("pfwd")
+        if pf is not None:
+            n5 = _PFwd.PHASES
+            pf.run(dM, 0, 1)   # layer 0 qkv
+            for li in range(c.n_layers):
+                chk(L_.card_attention_paged(ptr(self.q), ptr(dM), mm, ptr(rows.plen), ptr(rows.n_extra),
+                                            ptr(rows.extra), rows.extra_max, ptr(self.k_cache[li]),
+                                            ptr(self.v_cache[li]), ptr(pages.dev) if pages is not None else None,
+                                            c.n_heads, c.n_kv_heads, c.head_dim, self.prefix_slots, ptr(self.o), s),
+                    "attention")
+                # o, gate/up, down of layer li, then the qkv of layer li + 1
+                pf.run(dM, n5 * li + 2, min(n5 * (li + 1) + 1, n5 * c.n_layers))
+            plan["lm_head_topk" if topk else "lm_head"].run(rows.n_out)
+            return
         for li, P in enumerate(plan["layers"]):
             P["qkv"].run(dM)
             chk(L_.card_attention_paged(ptr(self.q), ptr(dM), mm, ptr(rows.plen), ptr(rows.n_extra), ptr(rows.extra),
