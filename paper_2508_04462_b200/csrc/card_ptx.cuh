@@ -31,19 +31,14 @@ __device__ __forceinline__ bool bar_try(uint64_t* b, uint32_t parity) {
         : "memory");
     return ok != 0;
 }
+// Waits back off with a short sleep: a spinning warp shares its SM
+// sub-partition's issue slot with a worker warp (measured: a softmax round
+// ran ~6x slower next to spinning control warps than alone).
 __device__ __forceinline__ void bar_wait(uint64_t* b, uint32_t parity) {
-    asm volatile(
-        "{\n\t.reg .pred P;\n\t"
-        "W_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
-        "@!P bra W_%=;\n\t}" ::"r"(su32(b)),
-        "r"(parity)
-        : "memory");
+    while (!bar_try(b, parity)) __nanosleep(20);
 }
-// waiters that must not steal issue slots from the producer / MMA threads
 __device__ __forceinline__ void bar_wait_polite(uint64_t* b, uint32_t parity) {
-    while (!bar_try(b, parity)) {
-    }
+    while (!bar_try(b, parity)) __nanosleep(40);
 }
 
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
@@ -93,6 +88,15 @@ __device__ __forceinline__ void tmem_ld16_issue(uint32_t taddr, uint32_t* r) {
         : "r"(taddr));
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* r) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+            taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+        "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+        : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
     uint32_t r[16];
     tmem_ld16_issue(taddr, r);
@@ -119,9 +123,15 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
     asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
+__device__ __forceinline__ int ld_relaxed(const int* p) {
+    int v;
+    asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+// poll relaxed (an acquire load invalidates L1 on every try), acquire once
 __device__ __forceinline__ void wait_ge(const int* p, int target) {
-    while (ld_acquire(p) < target) {
-    }
+    while (ld_relaxed(p) < target) __nanosleep(32);
+    (void)ld_acquire(p);
 }
 __device__ __forceinline__ int atom_add_acq_rel(int* p, int v) {
     int old;

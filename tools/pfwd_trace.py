@@ -34,14 +34,18 @@ G = pf.info()["grid"]
 n5 = 5
 L_ = lib()
 c = cfg
-launches = [(0, 1)] + [(n5 * li + 2, min(n5 * (li + 1) + 1, n5 * c.n_layers)) for li in range(c.n_layers)]
-bufs = [torch.zeros(G * (2 + 12 * (e - b)), dtype=torch.int64, device="cuda") for b, e in launches]
+inkernel = pf.bind(rows, None)
+if inkernel:
+    launches = [(0, n5 * c.n_layers)]
+else:
+    launches = [(0, 1)] + [(n5 * li + 2, min(n5 * (li + 1) + 1, n5 * c.n_layers)) for li in range(c.n_layers)]
+bufs = [torch.zeros(G * (2 + 32 * (e - b)), dtype=torch.int64, device="cuda") for b, e in launches]
 rt._bind_rows(plan, rows)
 dM = rows.M
 for rep in range(2):   # second pass warm
     for i, (b, e) in enumerate(launches):
         L_.card_pfwd_trace(pf.h, ptr(bufs[i]))
-        if i > 0:
+        if i > 0 and not inkernel:
             li = i - 1
             L_.card_attention_paged(ptr(rt.q), ptr(dM), plan["m_max"], ptr(rows.plen), ptr(rows.n_extra),
                                     ptr(rows.extra), rows.extra_max, ptr(rt.k_cache[li]), ptr(rt.v_cache[li]), None,
@@ -52,9 +56,9 @@ L_.card_pfwd_trace(pf.h, None)
 names = ["qkv", "attn", "o", "gu", "d"]
 t_first = None
 prev_end = None
-show = {0, 1, 2, c.n_layers}
+show = {0, 1, 2, c.n_layers} if not inkernel else {0}
 for i, (b, e) in enumerate(launches):
-    tr = bufs[i].cpu().numpy().reshape(G, 2 + 12 * (e - b)).astype(np.float64)
+    tr = bufs[i].cpu().numpy().reshape(G, 2 + 32 * (e - b)).astype(np.float64)
     t0 = tr[:, 0].min()
     if t_first is None:
         t_first = t0
@@ -64,9 +68,18 @@ for i, (b, e) in enumerate(launches):
         print(f"launch {i} steps [{b},{e}): start +{(t0 - t_first) / 1e3:8.1f} us  (gap from previous end {gap:6.1f})"
               f"  CTA start spread {(tr[:, 0].max() - t0) / 1e3:5.1f}  duration {(end - t0) / 1e3:6.1f} us")
         for j, st in enumerate(range(b, e)):
-            cols = tr[:, 2 + 12 * j:14 + 12 * j]
+            if inkernel and 10 <= st < n5 * c.n_layers - 5:
+                continue
+            cols = tr[:, 2 + 32 * j:34 + 32 * j]
             desc = []
-            for k, nm in enumerate(("rel", "kb0", "acc", "pub", "drained", "tc+", "tcwait", "reduced", "tmemld", "stored", "ld1", "it1")):
+            nms = ("rel", "kb0", "acc", "pub", "drained", "tc+", "tcwait", "reduced", "tmemld", "stored", "ld1", "it1")
+            if st % n5 == 1:
+                nms = ("-", "-", "-", "pub", "dep", "meta", "S0", "rounds", "merged_wait", "-", "-", "-") + sum(
+                    ((f"S{i}iss", f"PV{i}iss", f"S{i}seen", f"O{i}seen") for i in range(2)), ()) + ("sSeen", "sMax", "sExpA", "sExpB", "sArr", "-", "-", "-") + tuple(
+                    f"kv{i}" for i in range(4))
+            for k, nm in enumerate(nms[:cols.shape[1]]):
+                if nm == "-":
+                    continue
                 v = cols[:, k]
                 v = v[v > 0]
                 if len(v):
@@ -75,5 +88,11 @@ for i, (b, e) in enumerate(launches):
     elif i > 0:
         pass
     prev_end = end
+tr = bufs[0].cpu().numpy().reshape(G, -1).astype(np.float64)
+cols = tr[:, 2 + 32 * 1:34 + 32 * 1]
+ok = (cols[:, 23] > 0) & (cols[:, 22] > 0) & (cols[:, 26] > cols[:, 25])
+if ok.any():
+    f = (cols[ok, 26] - cols[ok, 25]) / (cols[ok, 23] - cols[ok, 22])
+    print(f"SM clock over the softmax half-round: median {np.median(f) * 1e3:.0f} MHz (min {f.min() * 1e3:.0f}, max {f.max() * 1e3:.0f})")
 total = (prev_end - t_first) / 1e3
 print(f"all pfwd launches + attention: {total:.1f} us over {c.n_layers} layers ({total / c.n_layers:.1f} us/layer)")
