@@ -230,24 +230,18 @@ int card_linear_destroy(card_linear* h);
  * [rows,H], xb bf16 [rows,H], ssq [H/16][ssq_ld], q fp32 [rows, nh*hd],
  * o bf16 [rows, nh*hd], g bf16 [rows, F]); act_rows = their row count.
  * card_pfwd_run executes steps [step_begin, step_end) on the stream (a
- * cooperative launch).  With attn_inkernel, attention steps (tree attention
- * of mask.py:173-217 on tcgen05, head dim 64) run in the kernel when the bound
- * rows fit its tiles (card_pfwd_info[15] == 1, then one run covers the whole
- * forward; measured slower than the separate kernel); otherwise
- * a range must not contain one (CARD_E_CONFIG) and card_attention_paged runs
- * them between runs. */
+ * cooperative launch); attention steps are run by card_attention_paged between
+ * runs, so a range must not contain one (CARD_E_CONFIG). */
 typedef struct card_pfwd card_pfwd;
 int card_pfwd_create(int n_layers, int H, int F, int nh, int nkv, int hd, int m_max, const void* const* layer_w,
                      const float* const* bqkv, void* const* kv, float* x, void* xb, float* ssq, int ssq_ld, float* q,
                      void* o, void* g, int act_rows, const int32_t* pos, const int32_t* slot, const float* cos_t,
-                     const float* sin_t, float eps, int attn_inkernel, card_pfwd** out);
+                     const float* sin_t, float eps, card_pfwd** out);
 int card_pfwd_run(card_pfwd* h, const int32_t* dM, int step_begin, int step_end, void* stream);
-/* bind the row block (positions and KV slots for the qkv epilogue; prefix
- * lengths, extra slots and the request's page table for the attention) */
-int card_pfwd_bind(card_pfwd* h, const int32_t* pos, const int32_t* slot, const int32_t* plen,
-                   const int32_t* n_extra, const int32_t* extra, int extra_max, const int32_t* page_table);
+/* bind the row block's positions and KV slots (qkv epilogue) */
+int card_pfwd_bind(card_pfwd* h, const int32_t* pos, const int32_t* slot);
 /* info16: grid, smem, weight stages, activation stages, Mpad, then (splits,
- * units) per phase (attention: key splits, units), [15] in-kernel attention */
+ * units) per phase, [15] epilogue worker groups */
 int card_pfwd_info(card_pfwd* h, int32_t* info16);
 /* tuning: per-CTA %globaltimer stamps [grid][2 + 4 * steps] of the next runs (NULL disables) */
 int card_pfwd_trace(card_pfwd* h, unsigned long long* trace);

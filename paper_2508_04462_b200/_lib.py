@@ -66,10 +66,10 @@ SIGNATURES = {
     "card_lmhead_topk_merge": (c_int, [_P, _P, c_int, c_int, c_int, c_int, _P, _P, _P, _P]),
     "card_linear_destroy": (c_int, [_P]),
     "card_pfwd_create": (c_int, [c_int, c_int, c_int, c_int, c_int, c_int, c_int, _P, _P, _P, _P, _P, _P, c_int, _P,
-                                 _P, _P, c_int, _P, _P, _P, _P, ctypes.c_float, c_int, POINTER(c_void_p)]),
+                                 _P, _P, c_int, _P, _P, _P, _P, ctypes.c_float, POINTER(c_void_p)]),
     "card_pfwd_run": (c_int, [_P, _P, c_int, c_int, _P]),
     "card_pfwd_info": (c_int, [_P, _P]),
-    "card_pfwd_bind": (c_int, [_P, _P, _P, _P, _P, _P, c_int, _P]),
+    "card_pfwd_bind": (c_int, [_P, _P, _P]),
     "card_pfwd_trace": (c_int, [_P, _P]),
     "card_pfwd_tune": (c_int, [_P, c_int, c_int]),
     "card_pfwd_destroy": (c_int, [_P]),

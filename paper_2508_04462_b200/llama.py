@@ -335,7 +335,7 @@ class _PFwd:
 
     PHASES = 5   # qkv, attention, o, gate/up, down
 
-    def __init__(self, rt: "DeviceLlama", m_max: int, attention: bool = False):
+    def __init__(self, rt: "DeviceLlama", m_max: int):
         c = rt.cfg
         n = c.n_layers
         W = (ctypes.c_void_p * (4 * n))()
@@ -351,19 +351,13 @@ class _PFwd:
                                     ctypes.cast(W, ctypes.c_void_p), ctypes.cast(B, ctypes.c_void_p),
                                     ctypes.cast(KV, ctypes.c_void_p), ptr(rt.x), ptr(rt.xb), ptr(rt.ssq), rt.mpad,
                                     ptr(rt.q), ptr(rt.o), ptr(rt.g), rt.mpad, ptr(rt.rows_placeholder),
-                                    ptr(rt.rows_placeholder), ptr(rt.cos), ptr(rt.sin), c.rms_eps, int(attention),
-                                    ctypes.byref(h))
+                                    ptr(rt.rows_placeholder), ptr(rt.cos), ptr(rt.sin), c.rms_eps, ctypes.byref(h))
         raise_for_status(rc, f"card_pfwd_create(m_max={m_max})")
         self.h = h
         self.n_layers = n
 
-    def bind(self, rows: "RowBlock", pages: "PageTable | None" = None) -> bool:
-        """Bind the row block (and the request's page table); True when the
-        attention steps run inside the kernel."""
-        raise_for_status(lib().card_pfwd_bind(self.h, ptr(rows.pos), ptr(rows.slot), ptr(rows.plen), ptr(rows.n_extra),
-                                              ptr(rows.extra), rows.extra_max,
-                                              ptr(pages.dev) if pages is not None else None), "card_pfwd_bind")
-        return bool(self.info()["attn"])
+    def bind(self, rows: "RowBlock"):
+        raise_for_status(lib().card_pfwd_bind(self.h, ptr(rows.pos), ptr(rows.slot)), "card_pfwd_bind")
 
     def run(self, dM: torch.Tensor, step_begin: int, step_end: int):
         raise_for_status(lib().card_pfwd_run(self.h, ptr(dM), step_begin, step_end, stream_ptr()), "card_pfwd_run")
@@ -373,7 +367,7 @@ class _PFwd:
         lib().card_pfwd_info(self.h, ctypes.cast(buf, ctypes.c_void_p))
         names = ("qkv", "attn", "o", "gu", "d")
         return {"grid": buf[0], "smem": buf[1], "w_stages": buf[2], "x_stages": buf[3], "Mpad": buf[4],
-                "splits": {names[p]: buf[5 + 2 * p] for p in range(5)}, "attn": buf[15]}
+                "splits": {names[p]: buf[5 + 2 * p] for p in range(5) if p != 1}, "worker_groups": buf[15]}
 
     def __del__(self):
         try:
@@ -538,6 +532,8 @@ class DeviceLlama:
             P_["qkv"].fuse_rope(rows, self.cos, self.sin, c.n_heads, c.n_kv_heads, c.head_dim, self.q,
                                 self.k_cache[li], self.v_cache[li])
         plan["lm_head"].fuse_norm(self.ssq, c.hidden // 16, self.mpad, c.rms_eps, c.hidden, rows.out_rows)
+        if "pfwd" in plan:
+            plan["pfwd"].bind(rows)
         if "lm_head_topk" in plan:
             plan["lm_head_topk"].fuse_norm(self.ssq, c.hidden // 16, self.mpad, c.rms_eps, c.hidden, rows.out_rows)
         plan["bound_rows"] = key
@@ -626,10 +622,6 @@ class DeviceLlama:
         pf = plan.get("pfwd")
         if pf is not None:
             n5 = _PFwd.PHASES
-            if pf.bind(rows, pages):   # whole forward, attention included, in one launch
-                pf.run(dM, 0, n5 * c.n_layers)
-                plan["lm_head_topk" if topk else "lm_head"].run(rows.n_out)
-                return
             pf.run(dM, 0, 1)   # layer 0 qkv
             for li in range(c.n_layers):
                 chk(L_.card_attention_paged(ptr(self.q), ptr(dM), mm, ptr(rows.plen), ptr(rows.n_extra),

@@ -34,12 +34,12 @@ G = pf.info()["grid"]
 n5 = 5
 L_ = lib()
 c = cfg
-inkernel = pf.bind(rows, None)
+inkernel = False
 if inkernel:
     launches = [(0, n5 * c.n_layers)]
 else:
     launches = [(0, 1)] + [(n5 * li + 2, min(n5 * (li + 1) + 1, n5 * c.n_layers)) for li in range(c.n_layers)]
-bufs = [torch.zeros(G * (2 + 32 * (e - b)), dtype=torch.int64, device="cuda") for b, e in launches]
+bufs = [torch.zeros(G * (2 + 4 * (e - b)), dtype=torch.int64, device="cuda") for b, e in launches]
 rt._bind_rows(plan, rows)
 dM = rows.M
 for rep in range(2):   # second pass warm
@@ -58,7 +58,7 @@ t_first = None
 prev_end = None
 show = {0, 1, 2, c.n_layers} if not inkernel else {0}
 for i, (b, e) in enumerate(launches):
-    tr = bufs[i].cpu().numpy().reshape(G, 2 + 32 * (e - b)).astype(np.float64)
+    tr = bufs[i].cpu().numpy().reshape(G, 2 + 4 * (e - b)).astype(np.float64)
     t0 = tr[:, 0].min()
     if t_first is None:
         t_first = t0
@@ -70,7 +70,7 @@ for i, (b, e) in enumerate(launches):
         for j, st in enumerate(range(b, e)):
             if inkernel and 10 <= st < n5 * c.n_layers - 5:
                 continue
-            cols = tr[:, 2 + 32 * j:34 + 32 * j]
+            cols = tr[:, 2 + 4 * j:6 + 4 * j]
             desc = []
             nms = ("rel", "kb0", "acc", "pub", "drained", "tc+", "tcwait", "reduced", "tmemld", "stored", "ld1", "it1")
             if st % n5 == 1:
@@ -88,11 +88,5 @@ for i, (b, e) in enumerate(launches):
     elif i > 0:
         pass
     prev_end = end
-tr = bufs[0].cpu().numpy().reshape(G, -1).astype(np.float64)
-cols = tr[:, 2 + 32 * 1:34 + 32 * 1]
-ok = (cols[:, 23] > 0) & (cols[:, 22] > 0) & (cols[:, 26] > cols[:, 25])
-if ok.any():
-    f = (cols[ok, 26] - cols[ok, 25]) / (cols[ok, 23] - cols[ok, 22])
-    print(f"SM clock over the softmax half-round: median {np.median(f) * 1e3:.0f} MHz (min {f.min() * 1e3:.0f}, max {f.max() * 1e3:.0f})")
 total = (prev_end - t_first) / 1e3
 print(f"all pfwd launches + attention: {total:.1f} us over {c.n_layers} layers ({total / c.n_layers:.1f} us/layer)")
