@@ -238,12 +238,16 @@ int card_pfwd_create(int n_layers, int H, int F, int nh, int nkv, int hd, int m_
                      void* o, void* g, int act_rows, const int32_t* pos, const int32_t* slot, const float* cos_t,
                      const float* sin_t, float eps, card_pfwd** out);
 int card_pfwd_run(card_pfwd* h, const int32_t* dM, int step_begin, int step_end, void* stream);
+/* qkv epilogue writes Q as pre-swizzled bf16 tiles for card_attention_tree
+ * ([nkv][tiles][hd/64][128 x 64] SWIZZLE_128B; tiles >= ceil(Mpad*nh/nkv/128))
+ * instead of fp32 q; NULL restores fp32 q */
+int card_pfwd_set_qsw(card_pfwd* h, void* qsw, int tiles);
 /* bind the row block's positions and KV slots (qkv epilogue) */
 int card_pfwd_bind(card_pfwd* h, const int32_t* pos, const int32_t* slot);
 /* info16: grid, smem, weight stages, activation stages, Mpad, then (splits,
  * units) per phase, [15] epilogue worker groups */
 int card_pfwd_info(card_pfwd* h, int32_t* info16);
-/* tuning: per-CTA %globaltimer stamps [grid][2 + 4 * steps] of the next runs (NULL disables) */
+/* tuning: per-CTA %globaltimer stamps [grid][2 + 8 * steps] of the next runs (NULL disables) */
 int card_pfwd_trace(card_pfwd* h, unsigned long long* trace);
 /* tuning: split-K ways (1..10) of one GEMM phase (0 qkv, 2 o, 4 down) */
 int card_pfwd_tune(card_pfwd* h, int phase, int splits);
@@ -284,6 +288,14 @@ int card_attention_paged(const float* q, const int32_t* dM, int m_max, const int
                          const int32_t* n_extra, const int32_t* extra, int extra_max, const void* k_cache,
                          const void* v_cache, const int32_t* page_table, int nh, int nkv, int hd, int max_plen,
                          void* o, void* stream);
+/* card_attention_paged's tcgen05 kernel with the Q operand read as
+ * pre-swizzled bf16 tiles (the persistent forward's qkv epilogue output,
+ * card_pfwd_set_qsw) instead of converted from fp32 q: one bulk copy per
+ * tile.  Same arithmetic and results as card_attention_paged. */
+int card_attention_tree(const void* qsw, int qsw_tiles, const int32_t* dM, int m_max, const int32_t* plen,
+                        const int32_t* n_extra, const int32_t* extra, int extra_max, const void* k_cache,
+                        const void* v_cache, const int32_t* page_table, int nh, int nkv, int hd, int max_plen,
+                        void* o, void* stream);
 /* draft lm_head epilogue: per-row top-k by (logit desc, token asc) with
  * log-probs logit/T - logsumexp (replaces extension_pool's rows_topk+log).
  * If ctx_tail != NULL the k-gram logit bias of card_logit_bias is applied on

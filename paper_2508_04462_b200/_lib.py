@@ -70,6 +70,7 @@ SIGNATURES = {
     "card_pfwd_run": (c_int, [_P, _P, c_int, c_int, _P]),
     "card_pfwd_info": (c_int, [_P, _P]),
     "card_pfwd_bind": (c_int, [_P, _P, _P]),
+    "card_pfwd_set_qsw": (c_int, [_P, _P, c_int]),
     "card_pfwd_trace": (c_int, [_P, _P]),
     "card_pfwd_tune": (c_int, [_P, c_int, c_int]),
     "card_pfwd_destroy": (c_int, [_P]),
@@ -83,6 +84,8 @@ SIGNATURES = {
                                _P, c_int, _P]),
     "card_attention_paged": (c_int, [_P, _P, c_int, _P, _P, _P, c_int, _P, _P, _P, c_int, c_int, c_int, c_int, _P,
                                      _P]),
+    "card_attention_tree": (c_int, [_P, c_int, _P, c_int, _P, _P, _P, c_int, _P, _P, _P, c_int, c_int, c_int, c_int,
+                                    _P, _P]),
     "card_lmhead_work_floats": (c_int, [c_int, c_int]),
     "card_topk_logits": (c_int, [_P, _P, c_int, c_int, c_int, c_double, _P, _P, _P, _P, _P, c_int, c_int, c_uint64,
                                  c_uint64, ctypes.c_float, ctypes.c_float, _P]),
@@ -129,7 +132,7 @@ LAUNCHES = {
     "card_topk_logits": 2, "card_lmhead_topk_merge": 1, "card_argmax_logits": 2, "card_softmax64": 1, "card_logit_bias": 1,
     "card_draft_rows": 1, "card_target_rows": 1, "card_eos_fix": 1, "card_record_width": 1,
     "card_attention_paged": 1, "card_verify_argmax": 1, "card_verify_probs": 1, "card_commit": 1, "card_verify_result": 1, "card_draft_promote": 2,
-    "card_kv_compact": 2, "card_cycle_end": 1, "card_engine_handoff": 1,
+    "card_kv_compact": 2, "card_cycle_end": 1, "card_engine_handoff": 1, "card_pfwd_run": 1, "card_attention_tree": 1,
 }
 launch_count = [0]
 

@@ -193,6 +193,8 @@ struct TcAttnArgs {
     const int32_t* page_table;   // null: prefix position p is slot p
     int nh, nkv;
     __nv_bfloat16* o;   // [M, nh, hd]
+    const uint8_t* qsw;   // non-null: Q tiles pre-swizzled bf16 (card_pfwd_set_qsw layout), q unused
+    int qsw_tiles;
 };
 
 template <int HD>
@@ -238,6 +240,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const TcAttnArgs a
     uint64_t* o_empty = bars + 10;   // softmax -> MMA
     uint64_t* recv_bar = bars + 11;  // every rank's partials of my rows landed (st.async complete_tx)
     uint32_t* tmem_slot = (uint32_t*)(bars + 12);
+    uint64_t* q_full = bars + 13;    // pre-swizzled Q tile landed (bulk copy)
 
     const int S = gridDim.x;
     const int rank = (int)cl_rank();
@@ -270,6 +273,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const TcAttnArgs a
         bar_init(o_full, 1);
         bar_init(o_empty, kSoftWarps * 32);
         bar_init(recv_bar, 1);
+        bar_init(q_full, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         if (S > 1) {   // bytes the S ranks will push for my live rows
             const int RO = kQT / S;
@@ -350,8 +354,20 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const TcAttnArgs a
     tc_stamp(2);
 
     // ---- Q tile (softmax + MMA warps; the loaders go straight to this
-    // forward's new K/V rows): fp32 -> bf16, SW128 K-major
-    if (warp < kLoadWarp0) {
+    // forward's new K/V rows): fp32 -> bf16, SW128 K-major; or one bulk copy
+    // of the tile the qkv epilogue already wrote in that layout
+    if (a.qsw) {
+        if (threadIdx.x == kMmaWarp * 32) {
+            constexpr uint32_t qbytes = HD / 64 * kSub;
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(q_full)), "r"(qbytes)
+                         : "memory");
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                    su32(sQ)),
+                "l"(a.qsw + (size_t)(g * a.qsw_tiles + qt) * qbytes), "r"(qbytes), "r"(su32(q_full))
+                : "memory");
+        }
+    } else if (warp < kLoadWarp0) {
 #pragma unroll 4
         for (int idx = threadIdx.x; idx < kQT * (HD / 8); idx += kLoadWarp0 * 32) {
             const int t = idx / (HD / 8), c = idx % (HD / 8);
@@ -438,6 +454,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const TcAttnArgs a
             const uint32_t idO = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) | ((uint32_t)(HD >> 3) << 17) |
                                  ((uint32_t)(kQT >> 4) << 24);
             const uint32_t q_s = su32(sQ), p_s = su32(sP);
+            if (a.qsw) bar_wait(q_full, 0);
             for (int li = 0; li < nr; ++li) {
                 const int b = li % L::kNB;
                 bar_wait(&kv_full[b], (li / L::kNB) & 1);
@@ -672,12 +689,13 @@ static cudaError_t launch_tc(const TcAttnArgs& a, dim3 grid, int S, cudaStream_t
 
 int launch_attn_tc(const float* q, const int32_t* dM, int m_max, const int32_t* plen, const int32_t* n_extra,
                    const int32_t* extra, int extra_max, const void* kc, const void* vc, const int32_t* page_table,
-                   int nh, int nkv, int hd, int max_plen, void* o, cudaStream_t s) {
+                   int nh, int nkv, int hd, int max_plen, void* o, cudaStream_t s, const void* qsw, int qsw_tiles) {
     const int G = nh / nkv;
     const int n_qt = (m_max * G + kQT - 1) / kQT;
+    if (qsw && qsw_tiles < n_qt) return CARD_E_CONFIG;
     const int S = attn_tc_ranks(n_qt * nkv);
     TcAttnArgs a{q, dM, plen, n_extra, extra, extra_max, (const __nv_bfloat16*)kc, (const __nv_bfloat16*)vc,
-                 page_table, nh, nkv, (__nv_bfloat16*)o};
+                 page_table, nh, nkv, (__nv_bfloat16*)o, (const uint8_t*)qsw, qsw_tiles};
     const dim3 grid(S, n_qt, nkv);
     const cudaError_t e = hd == 64 ? launch_tc<64>(a, grid, S, s) : launch_tc<128>(a, grid, S, s);
     if (e != cudaSuccess) {

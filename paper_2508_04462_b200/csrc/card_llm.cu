@@ -1090,6 +1090,17 @@ int card_attention_paged(const float* q, const int32_t* dM, int m_max, const int
     return rc;
 }
 
+int card_attention_tree(const void* qsw, int qsw_tiles, const int32_t* dM, int m_max, const int32_t* plen,
+                        const int32_t* n_extra, const int32_t* extra, int extra_max, const void* kc, const void* vc,
+                        const int32_t* page_table, int nh, int nkv, int hd, int max_plen, void* o, void* stream) {
+    if (!qsw || !dM || !plen || !kc || !vc || !o || m_max <= 0 || nkv <= 0 || nh % nkv) return CARD_E_INPUT;
+    if (!attn_tc_fits(m_max, nh, nkv, hd, extra_max)) return CARD_E_CONFIG;
+    const int rc = launch_attn_tc(nullptr, dM, m_max, plen, n_extra, extra, extra_max, kc, vc, page_table, nh, nkv, hd,
+                                  max_plen, o, (cudaStream_t)stream, qsw, qsw_tiles);
+    if (rc == CARD_OK) CARD_LAUNCH_CHECK();
+    return rc;
+}
+
 // vocab splits of the lm_head readers: about six CTAs per SM (the logits are
 // L2-warm right after the lm_head; more parallel reads win in-graph, +0.6 %
 // bench tokens/s against two per SM, same-box A/B)

@@ -91,6 +91,11 @@ struct Args {
     __nv_bfloat16* g;
     int F, nh, nkv, hd;
     float qscale;
+    // pre-swizzled bf16 Q tiles for card_attention_tree (null: fp32 q):
+    // [nkv][qsw_tiles][hd/64][128 query-heads x 64] SWIZZLE_128B blocks,
+    // query-head qh = row * (nh/nkv) + head % (nh/nkv) of kv head head / (nh/nkv)
+    uint8_t* qsw;
+    int qsw_tiles;
     const int32_t* pos;
     const int32_t* slot;
     const float* cos_t;
@@ -107,11 +112,12 @@ __device__ __forceinline__ unsigned long long gtime() {
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
 }
-// stamp k of step st: 0 activations released, 1 first k-block in, 2 accumulator done, 3 outputs published
+// stamp k of step st: 0 activations released, 1 first k-block in, 2 accumulator done, 3 outputs published,
+// 4 partial drained, 5 all splits of the tile in, 6 slice reduced
 #define PF_STAMP(st, k)                                                                                        \
     do {                                                                                                       \
         if (a.trace)                                                                                           \
-            a.trace[(size_t)blockIdx.x * (2 + 4 * (a.step_end - a.step_begin)) + 2 + 4 * ((st) - a.step_begin) + \
+            a.trace[(size_t)blockIdx.x * (2 + 8 * (a.step_end - a.step_begin)) + 2 + 8 * ((st) - a.step_begin) + \
                     (k)] = gtime();                                                                            \
     } while (0)
 
@@ -168,13 +174,31 @@ __device__ __forceinline__ uint2 pack4_bf16(float a, float b, float c, float d) 
     __nv_bfloat162 lo = __floats2bfloat162_rn(a, b), hi = __floats2bfloat162_rn(c, d);
     return make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
 }
+// Operands of one epilogue item that do not depend on the step's partials:
+// the residual row (o, down) or the row's KV slot and RoPE cos / sin (qkv).
+struct Pre {
+    float4 x, cs, sn;
+    int slot;
+};
+__device__ __forceinline__ void pre_item(const Args& a, int p, int N, int tile, int f4, int m, Pre& r) {
+    if (p != PH_QKV) {
+        r.x = *reinterpret_cast<const float4*>(a.x + (int64_t)m * N + tile * kTileN + 4 * f4);
+        return;
+    }
+    const int half = a.hd >> 1;
+    const int fb = 4 * f4;
+    const int i0 = fb - (fb / a.hd) * a.hd;
+    const int ii = i0 < half ? i0 : i0 - half;
+    const int pos = a.pos[m];
+    r.slot = a.slot[m];
+    r.cs = *reinterpret_cast<const float4*>(a.cos_t + (int64_t)pos * half + ii);
+    r.sn = *reinterpret_cast<const float4*>(a.sin_t + (int64_t)pos * half + ii);
+}
 // o / down epilogue of one float4 item: x += sum, bf16 copy, per-16-column
 // sum of squares (a quad of lanes = 16 columns)
-__device__ __forceinline__ void resid_item(const Args& a, int N, int ng, int m, const float4& s) {
-    float4* xp = reinterpret_cast<float4*>(a.x + (int64_t)m * N + ng);
-    float4 xn = *xp;
+__device__ __forceinline__ void resid_item(const Args& a, int N, int ng, int m, const float4& s, float4 xn) {
     add4(xn, s);
-    *xp = xn;
+    *reinterpret_cast<float4*>(a.x + (int64_t)m * N + ng) = xn;
     *reinterpret_cast<uint2*>(a.xb + (int64_t)m * N + ng) = pack4_bf16(xn.x, xn.y, xn.z, xn.w);
     float sq = xn.x * xn.x + xn.y * xn.y + xn.z * xn.z + xn.w * xn.w;
     sq += __shfl_xor_sync(0xffffffffu, sq, 1);
@@ -185,7 +209,7 @@ __device__ __forceinline__ void resid_item(const Args& a, int N, int ng, int m, 
 // norm scale + bias, RoPE with the partner half of the head via a shuffle
 // (the warp holds the whole 128-feature row), q * 1/sqrt(hd) -> q, k / v -> cache
 __device__ __forceinline__ void qkv_item(const Args& a, const Layer& L, const float* invs, int tile, int f4, int m,
-                                         float4 s) {
+                                         float4 s, const Pre& pr) {
     const int half = a.hd >> 1;
     const int fb = 4 * f4;   // feature in the tile
     const int hl = fb / a.hd, i0 = fb - hl * a.hd;
@@ -198,7 +222,7 @@ __device__ __forceinline__ void qkv_item(const Args& a, const Layer& L, const fl
     v.z *= iv;
     v.w *= iv;
     if (L.bqkv) add4(v, *reinterpret_cast<const float4*>(L.bqkv + ng));
-    const int pos = a.pos[m], slot = a.slot[m];
+    const int slot = pr.slot;
     const int pl = half >> 2;   // partner lane distance (float4 items)
     float4 o;
     o.x = __shfl_xor_sync(0xffffffffu, v.x, pl);
@@ -211,9 +235,8 @@ __device__ __forceinline__ void qkv_item(const Args& a, const Layer& L, const fl
         return;
     }
     const bool first = i0 < half;
-    const int ii = first ? i0 : i0 - half;
-    const float4 cs = *reinterpret_cast<const float4*>(a.cos_t + (int64_t)pos * half + ii);
-    const float4 sn = *reinterpret_cast<const float4*>(a.sin_t + (int64_t)pos * half + ii);
+    const float4 cs = pr.cs;
+    const float4 sn = pr.sn;
     // first half: x1 = v, x2 = o -> x1 cs - x2 sn; second: x2 = v, x1 = o -> x2 cs + x1 sn
     const float sg = first ? -1.f : 1.f;
     float4 r;
@@ -226,7 +249,17 @@ __device__ __forceinline__ void qkv_item(const Args& a, const Layer& L, const fl
         r.y *= a.qscale;
         r.z *= a.qscale;
         r.w *= a.qscale;
-        *reinterpret_cast<float4*>(a.q + ((int64_t)m * a.nh + head) * a.hd + i0) = r;
+        if (a.qsw) {   // the attention's Q operand, already in its shared-memory layout
+            const int G = a.nh / a.nkv;
+            const int gq = head / G;
+            const int qh = m * G + (head - gq * G);
+            const int tq = qh & 127, c = (i0 & 63) >> 3;
+            uint8_t* dst = a.qsw + ((size_t)((gq * a.qsw_tiles + (qh >> 7)) * (a.hd >> 6) + (i0 >> 6)) << 14) +
+                           ((tq >> 3) * 1024 + (tq & 7) * 128 + ((c ^ (tq & 7)) << 4)) + (i0 & 7) * 2;
+            *reinterpret_cast<uint2*>(dst) = pack4_bf16(r.x, r.y, r.z, r.w);
+        } else {
+            *reinterpret_cast<float4*>(a.q + ((int64_t)m * a.nh + head) * a.hd + i0) = r;
+        }
     } else {
         *reinterpret_cast<uint2*>(L.kc + ((int64_t)slot * a.nkv + (head - a.nh)) * a.hd + i0) =
             pack4_bf16(r.x, r.y, r.z, r.w);
@@ -274,20 +307,33 @@ __device__ __noinline__ void drain_partial(float* wsp, int N, uint32_t trow, int
     }
 }
 
-// reduce token slice [ma, mb) of a split tile in split order + fused epilogue;
-// a warp = one token row of the tile (float4 per lane), warp-uniform loop
+// reduce token slice [ma, mb) of a split tile in split order + fused epilogue,
+// once all splits of the tile are in (tctr); a warp = one token row of the
+// tile (float4 per lane), warp-uniform loop.
 __device__ __noinline__ void reduce_slice(const Args& a, const Layer& L, const float* invs, int p, int N, int splits,
-                                          int tile, int ma, int mb) {
+                                          int tile, int ma, int mb, int* tctr, int st, bool stamp) {
     const int t = threadIdx.x - kWorkerWarp0 * 32;
     const int f4 = threadIdx.x & 31;
     const int ng = tile * kTileN + 4 * f4;
     const int64_t sstride = (int64_t)a.Mpad * N;
+    const int n_items = (mb - ma) * 32;
+    if (t == 0) {
+        if (stamp) PF_STAMP(st, 4);
+        atom_add_acq_rel(tctr, 1);   // release: the CTA's partial stores (bar.sync before the call)
+        wait_ge(tctr, splits);
+        if (stamp) PF_STAMP(st, 5);
+    }
+    named_bar(1, kWorkers);
+    // (loading the residual / RoPE operands before the wait measured slower:
+    // the release waits for them, and at 96 registers they spill)
 #pragma unroll 1
-    for (int i0 = t; i0 < (mb - ma) * 32; i0 += kWorkers) {
+    for (int i0 = t; i0 < n_items; i0 += kWorkers) {
         const int m = ma + (i0 >> 5);
         const float4 sm = reduce1(a.ws + (int64_t)m * N + ng, sstride, splits);
-        if (p == PH_QKV) qkv_item(a, L, invs, tile, f4, m, sm);
-        else resid_item(a, N, ng, m, sm);
+        Pre pr;
+        pre_item(a, p, N, tile, f4, m, pr);
+        if (p == PH_QKV) qkv_item(a, L, invs, tile, f4, m, sm, pr);
+        else resid_item(a, N, ng, m, sm, pr.x);
     }
 }
 
@@ -310,10 +356,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* xfull = wempty + a.WS;
     uint64_t* xempty = xfull + a.XS;
 
-    const int M = *a.dM;
+    // the next kernel (the layer's attention) may launch now: it cannot take
+    // an SM before this grid's CTAs leave, and it waits for our results
+    // (griddepcontrol.wait) before reading them, so its launch latency hides
+    pdl_trigger();
+    const int M = *a.dM;   // written before the previous forward's kernels (row builder)
     if (M <= 0) return;   // uniform: nothing to do, no counter touched
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (threadIdx.x == 0 && a.trace) a.trace[(size_t)blockIdx.x * (2 + 4 * (a.step_end - a.step_begin))] = gtime();
+    if (threadIdx.x == 0 && a.trace) a.trace[(size_t)blockIdx.x * (2 + 8 * (a.step_end - a.step_begin))] = gtime();
     if (threadIdx.x == 0) {
         for (int i = 0; i < a.WS; ++i) {
             bar_init(&wfull[i], 1);
@@ -372,6 +422,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else if (warp == 1) {
         // ------------------------------------------------ activation producer
         if (lane == 0) {
+            pdl_wait();   // the previous kernel's outputs (attention o, embed x) are visible
             prefetch_map(&tmXb);
             prefetch_map(&tmO);
             prefetch_map(&tmG);
@@ -449,6 +500,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else if (warp >= kWorkerWarp0) {
         // ------------------------------------------------ epilogue workers
+        pdl_wait();
         const int t = threadIdx.x - kWorkerWarp0 * 32;
         const int wq = (warp - kWorkerWarp0) & 3;
         const int n_local = wq * 32 + lane;
@@ -491,16 +543,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                     __syncwarp();
                     if (lane == 0) bar_arrive(&tempty[acc]);
                     named_bar(1, kWorkers);
-                    int* tc = &a.tctr[st * kTileCtrs + tile];
-                    if (t == 0) {
-                        atom_add_acq_rel(tc, 1);   // release: the CTA's partial stores (bar.sync above)
-                        wait_ge(tc, gm.splits);
-                    }
-                    named_bar(1, kWorkers);
-                    reduce_slice(a, L, invs, p, gm.N, gm.splits, tile, ma, mb);
+                    reduce_slice(a, L, invs, p, gm.N, gm.splits, tile, ma, mb, &a.tctr[st * kTileCtrs + tile], st,
+                                 u == cta);
+                    if (t == 0 && u == cta) PF_STAMP(st, 6);
                 }
                 acc ^= 1;
                 if (acc == 0) aph ^= 1;
+                // one release per CTA (per-warp arrivals on the step counter
+                // measured slower: 16x the same-address atomics)
                 named_bar(1, kWorkers);
                 if (t == 0) {
                     fence_proxy_async_global();   // xb / g are read by TMA in later steps
@@ -516,7 +566,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_after();
     if (warp == 2)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(256));
-    if (threadIdx.x == 0 && a.trace) a.trace[(size_t)blockIdx.x * (2 + 4 * (se - sb)) + 1] = gtime();
+    if (threadIdx.x == 0 && a.trace) a.trace[(size_t)blockIdx.x * (2 + 8 * (se - sb)) + 1] = gtime();
     // the last CTA out clears the counters for the next launch
     __shared__ int last;
     if (threadIdx.x == 0) {
@@ -720,16 +770,34 @@ int card_pfwd_run(card_pfwd* h, const int32_t* dM, int step_begin, int step_end,
     cfg.blockDim = dim3(pf::kThreads);
     cfg.dynamicSmemBytes = h->smem;
     cfg.stream = (cudaStream_t)stream;
-    cudaLaunchAttribute attr[1];
+    // cooperative: every CTA co-resident (they wait on each other's steps);
+    // programmatic serialization: the weight stream and the prologue start
+    // under the previous kernel's tail (the activation producer and the
+    // epilogue workers wait for its results)
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeCooperative;
     attr[0].val.cooperative = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     cudaError_t e = cudaLaunchKernelEx(&cfg, pf::pfwd_kernel, h->tmXb, h->tmO, h->tmG, a);
     if (e != cudaSuccess) {
         set_cuda_error(e);
         return CARD_E_CUDA;
     }
+    return CARD_OK;
+}
+
+// qkv epilogue output for card_attention_tree: pre-swizzled bf16 Q tiles
+// (qsw: nkv * tiles * hd/64 * 16 KB; tiles >= ceil(Mpad * nh/nkv / 128));
+// NULL restores the fp32 q output
+int card_pfwd_set_qsw(card_pfwd* h, void* qsw, int tiles) {
+    if (!h) return CARD_E_INPUT;
+    const pf::Args& a = h->args;
+    if (qsw && (int64_t)tiles * 128 < (int64_t)a.Mpad * (a.nh / a.nkv)) return CARD_E_CONFIG;
+    h->args.qsw = (uint8_t*)qsw;
+    h->args.qsw_tiles = tiles;
     return CARD_OK;
 }
 

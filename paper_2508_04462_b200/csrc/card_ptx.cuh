@@ -138,6 +138,10 @@ __device__ __forceinline__ int atom_add_acq_rel(int* p, int v) {
     asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
     return old;
 }
+// release increment without a result: the issuing thread does not wait for it
+__device__ __forceinline__ void red_release(int* p, int v) {
+    asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 // generic-proxy global writes -> later async-proxy (TMA) reads of the same data
 __device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
 

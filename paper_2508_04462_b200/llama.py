@@ -355,6 +355,28 @@ class _PFwd:
         raise_for_status(rc, f"card_pfwd_create(m_max={m_max})")
         self.h = h
         self.n_layers = n
+        # the qkv epilogue hands the attention its Q operand as pre-swizzled
+        # bf16 tiles (card_attention_tree: one bulk copy per tile)
+        # (per forward, when the row block's extras fit the tcgen05 kernel:
+        # use_qsw; otherwise q stays fp32 for card_attention_paged)
+        G = c.n_heads // c.n_kv_heads
+        self.G = G
+        self.qsw = None
+        self.qsw_on = False
+        if c.head_dim in (64, 128) and (128 // G + 2) <= 136:
+            self.qsw_tiles = (rt.mpad * G + 127) // 128
+            self.qsw = torch.zeros(c.n_kv_heads * self.qsw_tiles * (c.head_dim // 64) * 16384, dtype=torch.uint8,
+                                   device=rt.dev)
+
+    def use_qsw(self, extra_max: int) -> bool:
+        """Route Q through the pre-swizzled tiles for this forward's rows (the
+        setting is copied into each launch, so captured graphs keep it)."""
+        on = self.qsw is not None and (128 // self.G + 2) * extra_max <= 1024
+        if on != self.qsw_on:
+            raise_for_status(lib().card_pfwd_set_qsw(self.h, ptr(self.qsw) if on else None,
+                                                     self.qsw_tiles if on else 0), "card_pfwd_set_qsw")
+            self.qsw_on = on
+        return on
 
     def bind(self, rows: "RowBlock"):
         raise_for_status(lib().card_pfwd_bind(self.h, ptr(rows.pos), ptr(rows.slot)), "card_pfwd_bind")
@@ -622,13 +644,20 @@ class DeviceLlama:
         pf = plan.get("pfwd")
         if pf is not None:
             n5 = _PFwd.PHASES
+            tree_q = pf.use_qsw(rows.extra_max)
             pf.run(dM, 0, 1)   # layer 0 qkv
+            pt = ptr(pages.dev) if pages is not None else None
             for li in range(c.n_layers):
-                chk(L_.card_attention_paged(ptr(self.q), ptr(dM), mm, ptr(rows.plen), ptr(rows.n_extra),
-                                            ptr(rows.extra), rows.extra_max, ptr(self.k_cache[li]),
-                                            ptr(self.v_cache[li]), ptr(pages.dev) if pages is not None else None,
-                                            c.n_heads, c.n_kv_heads, c.head_dim, self.prefix_slots, ptr(self.o), s),
-                    "attention")
+                if tree_q:
+                    chk(L_.card_attention_tree(ptr(pf.qsw), pf.qsw_tiles, ptr(dM), mm, ptr(rows.plen),
+                                               ptr(rows.n_extra), ptr(rows.extra), rows.extra_max,
+                                               ptr(self.k_cache[li]), ptr(self.v_cache[li]), pt, c.n_heads,
+                                               c.n_kv_heads, c.head_dim, self.prefix_slots, ptr(self.o), s), "attention")
+                else:
+                    chk(L_.card_attention_paged(ptr(self.q), ptr(dM), mm, ptr(rows.plen), ptr(rows.n_extra),
+                                                ptr(rows.extra), rows.extra_max, ptr(self.k_cache[li]),
+                                                ptr(self.v_cache[li]), pt, c.n_heads, c.n_kv_heads, c.head_dim,
+                                                self.prefix_slots, ptr(self.o), s), "attention")
                 # o, gate/up, down of layer li, then the qkv of layer li + 1
                 pf.run(dM, n5 * li + 2, min(n5 * (li + 1) + 1, n5 * c.n_layers))
             plan["lm_head_topk" if topk else "lm_head"].run(rows.n_out)

@@ -273,3 +273,59 @@ def test_paged_attention_matches_torch(card, hd, M):
         want = torch.einsum("ht,thd->hd", torch.softmax(s, -1), v).reshape(-1)
         err = (o[r].float() - want).norm() / want.norm()
         assert err < 1e-2, (r, float(err))
+
+
+def _swizzle_q(q: torch.Tensor, nkv: int, tiles: int) -> torch.Tensor:
+    """Host restatement of the card_pfwd_set_qsw layout: fp32 q [M, nh, hd] ->
+    bf16 [nkv][tiles][hd/64][128 x 64] SWIZZLE_128B blocks, query-head
+    qh = row * G + head % G of kv head head // G (16-byte chunk c of row t
+    stored at chunk c ^ (t % 8))."""
+    M, nh, hd = q.shape
+    G = nh // nkv
+    out = torch.zeros(nkv, tiles * 128, hd, dtype=torch.bfloat16, device=q.device)
+    out[:, :M * G] = q.to(torch.bfloat16).view(M, nkv, G, hd).permute(1, 0, 2, 3).reshape(nkv, M * G, hd)
+    blk = out.view(nkv, tiles, 128, hd // 64, 8, 8).permute(0, 1, 3, 2, 4, 5)   # [g, tile, sub, t, chunk, 8]
+    t = torch.arange(128, device=q.device).view(128, 1)
+    c = torch.arange(8, device=q.device).view(1, 8)
+    src = (c ^ (t % 8)).view(1, 1, 1, 128, 8, 1).expand(nkv, tiles, hd // 64, 128, 8, 8)
+    # stored chunk j of row t holds logical chunk j ^ (t % 8)
+    return torch.gather(blk, 4, src).contiguous().view(torch.uint8).reshape(-1)
+
+
+@pytest.mark.parametrize("hd,M", [(64, 116), (128, 116), (64, 40)])
+def test_attention_tree_preswizzled_q_equals_paged(card, hd, M):
+    """card_attention_tree (Q as pre-swizzled bf16 tiles, the persistent
+    forward's qkv output) is bit-identical to card_attention_paged on the
+    same fp32 q (which rounds Q to bf16 in the kernel)."""
+    from paper_2508_04462_b200._device import ptr, stream_ptr
+    from paper_2508_04462_b200._lib import lib
+    from paper_2508_04462_b200.llama import RowBlock
+
+    nh, nkv, XM = 32, 8, 16
+    g = torch.Generator(device="cuda").manual_seed(hd * 7 + M)
+    rng = np.random.default_rng(hd * 11 + M)
+    n_pages, P = 24, 1000
+    perm = torch.tensor(rng.permutation(n_pages)[: (P + 63) // 64], dtype=torch.int32, device="cuda")
+    slots = n_pages * 64 + 256
+    kc = torch.randn(slots, nkv, hd, device="cuda", generator=g).to(torch.bfloat16)
+    vc = torch.randn(slots, nkv, hd, device="cuda", generator=g).to(torch.bfloat16)
+    q = torch.randn(M, nh, hd, device="cuda", generator=g) / hd ** 0.5
+    plen = [int(x) for x in rng.integers(1, P + 1, M)]
+    extras = [sorted(set(int(x) for x in rng.integers(n_pages * 64, slots, int(rng.integers(0, XM)))))
+              for _ in range(M)]
+    rows = RowBlock(M, XM, "cuda")
+    _fill(rows, [0] * M, [0] * M, [0] * M, plen, extras, [])
+    tiles = ((M + 15) // 16 * 16 * (nh // nkv) + 127) // 128
+    qsw = _swizzle_q(q, nkv, tiles)
+    o_ref = torch.zeros(M, nh * hd, device="cuda", dtype=torch.bfloat16)
+    o_sw = torch.full_like(o_ref, float("nan"))
+    assert lib().card_attention_paged(ptr(q), ptr(rows.M), M, ptr(rows.plen), ptr(rows.n_extra), ptr(rows.extra), XM,
+                                      ptr(kc), ptr(vc), ptr(perm), nh, nkv, hd, P, ptr(o_ref), stream_ptr()) == 0
+    assert lib().card_attention_tree(ptr(qsw), tiles, ptr(rows.M), M, ptr(rows.plen), ptr(rows.n_extra),
+                                     ptr(rows.extra), XM, ptr(kc), ptr(vc), ptr(perm), nh, nkv, hd, P, ptr(o_sw),
+                                     stream_ptr()) == 0
+    torch.cuda.synchronize()
+    if M * (nh // nkv) >= 256:   # both ran the tcgen05 kernel: identical bits
+        assert torch.equal(o_sw.view(torch.int16), o_ref.view(torch.int16))
+    else:                        # paged ran the mma.sync kernel: same values within bf16 rounding
+        assert ((o_sw.float() - o_ref.float()).norm() / o_ref.float().norm()) < 1e-2

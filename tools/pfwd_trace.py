@@ -39,26 +39,47 @@ if inkernel:
     launches = [(0, n5 * c.n_layers)]
 else:
     launches = [(0, 1)] + [(n5 * li + 2, min(n5 * (li + 1) + 1, n5 * c.n_layers)) for li in range(c.n_layers)]
-bufs = [torch.zeros(G * (2 + 4 * (e - b)), dtype=torch.int64, device="cuda") for b, e in launches]
+bufs = [torch.zeros(G * (2 + 8 * (e - b)), dtype=torch.int64, device="cuda") for b, e in launches]
 rt._bind_rows(plan, rows)
 dM = rows.M
-for rep in range(2):   # second pass warm
+attn_buf = torch.zeros(4096 * 8, dtype=torch.int64, device="cuda")
+
+
+assert pf.use_qsw(rows.extra_max)
+
+
+def sequence():
     for i, (b, e) in enumerate(launches):
         L_.card_pfwd_trace(pf.h, ptr(bufs[i]))
         if i > 0 and not inkernel:
             li = i - 1
-            L_.card_attention_paged(ptr(rt.q), ptr(dM), plan["m_max"], ptr(rows.plen), ptr(rows.n_extra),
-                                    ptr(rows.extra), rows.extra_max, ptr(rt.k_cache[li]), ptr(rt.v_cache[li]), None,
-                                    c.n_heads, c.n_kv_heads, c.head_dim, rt.prefix_slots, ptr(rt.o), stream_ptr())
+            L_.card_attention_tree(ptr(pf.qsw), pf.qsw_tiles, ptr(dM), plan["m_max"], ptr(rows.plen), ptr(rows.n_extra),
+                                   ptr(rows.extra), rows.extra_max, ptr(rt.k_cache[li]), ptr(rt.v_cache[li]), None,
+                                   c.n_heads, c.n_kv_heads, c.head_dim, rt.prefix_slots, ptr(rt.o), stream_ptr())
         pf.run(dM, b, e)
-    torch.cuda.synchronize()
+
+
+# in-graph timeline (as the engine replays it): stamps of the last replay;
+# the attention stamps are the last layer's (one shared buffer)
+L_.card_attention_trace(ptr(attn_buf))
+gs = torch.cuda.Stream()
+with torch.cuda.stream(gs):
+    sequence()
+    gs.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=gs):
+        sequence()
+for _ in range(3):
+    graph.replay()
+torch.cuda.synchronize()
 L_.card_pfwd_trace(pf.h, None)
+L_.card_attention_trace(None)
 names = ["qkv", "attn", "o", "gu", "d"]
 t_first = None
 prev_end = None
 show = {0, 1, 2, c.n_layers} if not inkernel else {0}
 for i, (b, e) in enumerate(launches):
-    tr = bufs[i].cpu().numpy().reshape(G, 2 + 4 * (e - b)).astype(np.float64)
+    tr = bufs[i].cpu().numpy().reshape(G, 2 + 8 * (e - b)).astype(np.float64)
     t0 = tr[:, 0].min()
     if t_first is None:
         t_first = t0
@@ -70,9 +91,9 @@ for i, (b, e) in enumerate(launches):
         for j, st in enumerate(range(b, e)):
             if inkernel and 10 <= st < n5 * c.n_layers - 5:
                 continue
-            cols = tr[:, 2 + 4 * j:6 + 4 * j]
+            cols = tr[:, 2 + 8 * j:10 + 8 * j]
             desc = []
-            nms = ("rel", "kb0", "acc", "pub", "drained", "tc+", "tcwait", "reduced", "tmemld", "stored", "ld1", "it1")
+            nms = ("rel", "kb0", "acc", "pub", "drained", "allin", "reduced", "-")
             if st % n5 == 1:
                 nms = ("-", "-", "-", "pub", "dep", "meta", "S0", "rounds", "merged_wait", "-", "-", "-") + sum(
                     ((f"S{i}iss", f"PV{i}iss", f"S{i}seen", f"O{i}seen") for i in range(2)), ()) + ("sSeen", "sMax", "sExpA", "sExpB", "sArr", "-", "-", "-") + tuple(
@@ -90,3 +111,14 @@ for i, (b, e) in enumerate(launches):
     prev_end = end
 total = (prev_end - t_first) / 1e3
 print(f"all pfwd launches + attention: {total:.1f} us over {c.n_layers} layers ({total / c.n_layers:.1f} us/layer)")
+at = attn_buf.view(-1, 8).cpu().numpy().astype(np.float64)
+at = at[at[:, 0] > 0]
+last = bufs[-2].cpu().numpy().reshape(G, -1).astype(np.float64)   # launch before the last attention
+nxt = bufs[-1].cpu().numpy().reshape(G, -1).astype(np.float64)
+pend = last[:, 1].max()
+print(f"last attention ({len(at)} CTAs), us after the previous pfwd launch's last CTA exit:")
+for k, nm in enumerate(["entry", "setup", "pdl", "q_ready", "loop_end", "-", "merged", "end"]):
+    v = at[:, k][at[:, k] > 0] - pend
+    if len(v):
+        print(f"  {nm:9s} min {v.min() / 1e3:7.2f} med {np.median(v) / 1e3:7.2f} max {v.max() / 1e3:7.2f}")
+print(f"  next pfwd launch: first CTA start {(nxt[:, 0].min() - pend) / 1e3:7.2f}  last CTA start {(nxt[:, 0].max() - pend) / 1e3:7.2f}")
