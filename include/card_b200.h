@@ -296,6 +296,17 @@ int card_attention_tree(const void* qsw, int qsw_tiles, const int32_t* dM, int m
                         const int32_t* n_extra, const int32_t* extra, int extra_max, const void* k_cache,
                         const void* v_cache, const int32_t* page_table, int nh, int nkv, int hd, int max_plen,
                         void* o, void* stream);
+/* Batched forward of several requests: rows [i*seg_rows,
+ * (i+1)*seg_rows) belong to request i, whose prefix position p lives in KV
+ * slot page_tables[i*pt_stride + p/64]*64 + p%64; extras are physical slots.
+ * Rows with plen = 0 and no extras are padding (output zero).  Always the
+ * tcgen05 kernel; Q from fp32 q, or from pre-swizzled tiles when qsw != NULL
+ * (card_pfwd_set_qsw).  A tile's rows may span requests: each request's
+ * prefix is its own run of key rounds, masked per row. */
+int card_attention_batch(const float* q, const void* qsw, int qsw_tiles, const int32_t* dM, int m_max,
+                         const int32_t* plen, const int32_t* n_extra, const int32_t* extra, int extra_max,
+                         const void* k_cache, const void* v_cache, const int32_t* page_tables, int pt_stride,
+                         int seg_rows, int nh, int nkv, int hd, int max_plen, void* o, void* stream);
 /* draft lm_head epilogue: per-row top-k by (logit desc, token asc) with
  * log-probs logit/T - logsumexp (replaces extension_pool's rows_topk+log).
  * If ctx_tail != NULL the k-gram logit bias of card_logit_bias is applied on
@@ -334,6 +345,20 @@ int card_draft_rows(card_engine_state* E, card_cache* h, const int32_t* committe
 int card_target_rows(card_engine_state* E, card_cache* h, const int32_t* committed, int32_t* rows,
                      int rows_max, int extra_max, int32_t* ctx_tail, int order, const int32_t* page_table,
                      void* stream);
+/* Batched decode (the reference runs one request at a time,
+ * engine.py:275-287): each request builds its rows into its own region
+ * [row_base, row_base + rows_cap) of one combined row block of rows_max rows
+ * (outputs [out_base, out_base + out_cap)) and pads the rest of the region
+ * (plen 0, KV to dead_slot), so one forward serves every request.  The
+ * caller owns the block header (M = all regions, n_out = all output
+ * regions).  A request whose rows overflow its region ends with done = -1
+ * (raised as ProtocolError by the host). */
+int card_draft_rows_at(card_engine_state* E, card_cache* h, const int32_t* committed, int32_t* rows, int rows_max,
+                       int extra_max, int row_base, int rows_cap, int out_base, int out_cap, int dead_slot,
+                       int tree_base, int32_t* ctx_tail, int order, const int32_t* page_table, void* stream);
+int card_target_rows_at(card_engine_state* E, card_cache* h, const int32_t* committed, int32_t* rows, int rows_max,
+                        int extra_max, int row_base, int rows_cap, int dead_slot, int32_t* ctx_tail, int order,
+                        const int32_t* page_table, void* stream);
 int card_eos_fix(const int32_t* n_rows, int m_max, const int32_t* ctx_tail, int order, int eos, int V,
                  double* probs, void* stream);
 int card_record_width(card_engine_state* E, card_cache* h, const int32_t* n_out, void* stream);

@@ -84,6 +84,8 @@ SIGNATURES = {
                                _P, c_int, _P]),
     "card_attention_paged": (c_int, [_P, _P, c_int, _P, _P, _P, c_int, _P, _P, _P, c_int, c_int, c_int, c_int, _P,
                                      _P]),
+    "card_attention_batch": (c_int, [_P, _P, c_int, _P, c_int, _P, _P, _P, c_int, _P, _P, _P, c_int, c_int, c_int,
+                                     c_int, c_int, c_int, _P, _P]),
     "card_attention_tree": (c_int, [_P, c_int, _P, c_int, _P, _P, _P, c_int, _P, _P, _P, c_int, c_int, c_int, c_int,
                                     _P, _P]),
     "card_lmhead_work_floats": (c_int, [c_int, c_int]),
@@ -98,6 +100,9 @@ SIGNATURES = {
     "card_engine_state_bytes": (c_int, []),
     "card_draft_rows": (c_int, [_P, _P, _P, _P, c_int, c_int, c_int, _P, c_int, _P, _P]),
     "card_target_rows": (c_int, [_P, _P, _P, _P, c_int, c_int, _P, c_int, _P, _P]),
+    "card_draft_rows_at": (c_int, [_P, _P, _P, _P, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, _P, c_int,
+                                   _P, _P]),
+    "card_target_rows_at": (c_int, [_P, _P, _P, _P, c_int, c_int, c_int, c_int, c_int, _P, c_int, _P, _P]),
     "card_eos_fix": (c_int, [_P, c_int, _P, c_int, c_int, c_int, _P, _P]),
     "card_record_width": (c_int, [_P, _P, _P, _P]),
     "card_verify_argmax": (c_int, [_P, _P, _P, _P]),
@@ -130,9 +135,10 @@ LAUNCHES = {
     "card_cache_query": 1, "card_cache_correct": 1, "card_cache_advance_root": 1, "card_cache_count_alive": 1,
     "card_cache_clear_status": 1, "card_embed": 1, "card_resid_add": 1, "card_rmsnorm": 1, "card_rope_kv": 1, "card_attention": lambda a: 1 if (a[10] == 0 and a[17] == 0 and a[13] in (64, 128) and a[4] and _attn_fits(a)) else 3,
     "card_topk_logits": 2, "card_lmhead_topk_merge": 1, "card_argmax_logits": 2, "card_softmax64": 1, "card_logit_bias": 1,
-    "card_draft_rows": 1, "card_target_rows": 1, "card_eos_fix": 1, "card_record_width": 1,
+    "card_draft_rows": 1, "card_target_rows": 1, "card_draft_rows_at": 1, "card_target_rows_at": 1, "card_eos_fix": 1, "card_record_width": 1,
     "card_attention_paged": 1, "card_verify_argmax": 1, "card_verify_probs": 1, "card_commit": 1, "card_verify_result": 1, "card_draft_promote": 2,
     "card_kv_compact": 2, "card_cycle_end": 1, "card_engine_handoff": 1, "card_pfwd_run": 1, "card_attention_tree": 1,
+    "card_attention_batch": 1,
 }
 launch_count = [0]
 

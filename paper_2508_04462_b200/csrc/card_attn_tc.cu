@@ -41,6 +41,7 @@ constexpr int kQT = 128;        // query-heads per tile = MMA M = TMEM lanes
 constexpr int kKB = 128;        // keys per round = S MMA N = PV MMA K
 constexpr int kMaxX = 1024;     // gathered extra keys per tile
 constexpr int kMaxRows = 136;   // token rows per tile (GQA group >= 1)
+constexpr int kMaxSeg = 64;     // request segments per tile (batched forwards)
 constexpr int kSoftWarps = 8, kMmaWarp = 8, kLoadWarp0 = 9, kLoadWarps = 4;
 constexpr int kThreads = (kLoadWarp0 + kLoadWarps) * 32;   // 416
 constexpr int kSub = 128 * 64 * 2;   // one [128 rows x 64 bf16] SW128 sub-block (16 KB)
@@ -195,6 +196,10 @@ struct TcAttnArgs {
     __nv_bfloat16* o;   // [M, nh, hd]
     const uint8_t* qsw;   // non-null: Q tiles pre-swizzled bf16 (card_pfwd_set_qsw layout), q unused
     int qsw_tiles;
+    // batched forwards: rows [i * seg_rows, (i + 1) * seg_rows) belong to
+    // request i, whose prefix positions resolve through page_table + i *
+    // pt_stride (seg_rows == 0: one request, page_table as is)
+    int seg_rows, pt_stride;
 };
 
 template <int HD>
@@ -206,8 +211,9 @@ struct Smem {
     static constexpr int kRecvLd = HD + 4;             // merge record [m, l, pad, pad, O[HD]]
     static constexpr int oQ = 0, oK = kQ, oV = oK + kNB * kKV, oP = oV + kNB * kKV, oR = oP + kP;
     static constexpr int oMeta = oR + kQT * kRecvLd * 4;   // recv: one record per query-head row
-    // meta: ext_slot[kMaxX], rplen/rnx/rxo[kMaxRows], xch[2][128], bars, tmem slot
-    static constexpr int kMeta = kMaxX * 4 + 3 * kMaxRows * 4 + 16 + 2 * kQT * 4 + 16 * 8 + 16;
+    // meta: ext_slot[kMaxX], rplen/rnx/rxo[kMaxRows], xch[2][128], bars, tmem slot,
+    // segment table seg_vb[kMaxSeg + 1] / seg_kp[kMaxSeg]
+    static constexpr int kMeta = kMaxX * 4 + 3 * kMaxRows * 4 + 16 + 2 * kQT * 4 + 16 * 8 + 16 + (2 * kMaxSeg + 4) * 4;
     static constexpr int kTotal = oMeta + kMeta + 1024;   // + alignment slack
 };
 
@@ -241,6 +247,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const TcAttnArgs a
     uint64_t* recv_bar = bars + 11;  // every rank's partials of my rows landed (st.async complete_tx)
     uint32_t* tmem_slot = (uint32_t*)(bars + 12);
     uint64_t* q_full = bars + 13;    // pre-swizzled Q tile landed (bulk copy)
+    int32_t* seg_vb = (int32_t*)(bars + 16);   // [n_seg + 1] first virtual key of each segment's prefix rounds
+    int32_t* seg_kp = seg_vb + kMaxSeg + 1;    // [n_seg] prefix keys of the segment (max plen of its rows)
 
     const int S = gridDim.x;
     const int rank = (int)cl_rank();
@@ -305,12 +313,26 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const TcAttnArgs a
         Kx += rnx[i];
     }
     if (Kx > kMaxX) Kx = kMaxX;   // host guarantees rows * extra_max <= kMaxX
+    // request segments of the tile's rows (one unless batched)
+    const bool segm = a.seg_rows > 0;
+    const int s_lo = segm ? r_lo / a.seg_rows : 0;
+    const int n_seg = segm ? (r_hi - 1) / a.seg_rows - s_lo + 1 : 1;
     if (threadIdx.x == 0) {
         int x = 0;
         for (int i = 0; i < n_rows; ++i) {
             rxo[i] = x;
             x += rnx[i];
         }
+        int vb = 0;
+        for (int k = 0; k < n_seg; ++k) {
+            int kp = 0;
+            for (int i = 0; i < n_rows; ++i)
+                if (!segm || (r_lo + i) / a.seg_rows == s_lo + k) kp = max(kp, rplen[i]);
+            seg_vb[k] = vb;
+            seg_kp[k] = kp;
+            vb += (kp + kKB - 1) / kKB * kKB;
+        }
+        seg_vb[n_seg] = vb;
     }
     __syncthreads();
     for (int i = warp; i < n_rows; i += kThreads / 32) {
@@ -324,8 +346,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const TcAttnArgs a
     // 0 whatever the tile's rows, so a row's keys meet the same rounds, ranks
     // and summation order in an M = 1 decode step and in an M = r + 1 verify
     // (greedy CARD emits exactly the AR tokens).
-    const int n_pr = (Kp + kKB - 1) / kKB;
-    const int XB = n_pr * kKB;
+    const int XB = seg_vb[n_seg];   // = 128 ceil(Kp / 128) for one segment
+    const int n_pr = XB / kKB;
     const int n_tot = n_pr + (Kx + kKB - 1) / kKB;
     const int nr = rank < n_tot ? (n_tot - rank + S - 1) / S : 0;
 
@@ -333,7 +355,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const TcAttnArgs a
     if (warp >= kLoadWarp0) {
         // old prefix keys of the first two rounds stream in under the previous kernel's tail
         const int lt = threadIdx.x - kLoadWarp0 * 32;
-        const int old = min(*s_old, Kp);
+        const int old = segm ? 0 : min(*s_old, Kp);
         for (int li = 0; li < min(nr, L::kNB); ++li) {
             const int j0 = (rank + li * S) * kKB;
             const int k_hi = min(kKB, old - j0);
@@ -418,10 +440,18 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const TcAttnArgs a
                 const int kk = idx / (HD / 8), c = idx % (HD / 8);
                 const int j = j0 + kk;
                 const uint32_t off = (uint32_t)((c >> 3) * kSub) + sw_off(kk, c & 7);
-                if (j < XB ? j < Kp : j - XB < Kx) {
+                int sg = 0;   // the key's segment (prefix part)
+                if (j < XB)
+                    while (j >= seg_vb[sg + 1]) ++sg;
+                const int pp = j - seg_vb[sg];
+                if (j < XB ? pp < seg_kp[sg] : j - XB < Kx) {
                     int slot;
-                    if (j < XB) slot = a.page_table ? a.page_table[j >> 6] * 64 + (j & 63) : j;
-                    else slot = ext_slot[j - XB];
+                    if (j < XB) {
+                        const int32_t* pt = a.page_table ? a.page_table + (int64_t)(s_lo + sg) * a.pt_stride : nullptr;
+                        slot = pt ? pt[pp >> 6] * 64 + (pp & 63) : pp;
+                    } else {
+                        slot = ext_slot[j - XB];
+                    }
                     const int64_t e = ((int64_t)slot * a.nkv + g) * HD + c * 8;
                     cp16(kb + off, a.kc + e);
                     cp16(vb + off, a.vc + e);
@@ -432,7 +462,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const TcAttnArgs a
             }
         };
         // rounds 0 and 1: the old prefix keys were issued before the PDL wait
-        const int old = min(*s_old, Kp);
+        const int old = segm ? 0 : min(*s_old, Kp);
         for (int li = 0; li < nr; ++li) {
             const int b = li % L::kNB;
             const int j0 = (rank + li * S) * kKB;
@@ -485,8 +515,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const TcAttnArgs a
         const int qh = q0 + t;
         const bool live = qh < nq;
         const int ri = live ? qh / G - r_lo : 0;
-        // valid keys of this row: [0, plim) prefix, [e0, e1) its own extras
-        const int plim = live ? min(rplen[ri], Kp) : 0;
+        // valid keys of this row: [p0, plim) prefix (its segment's rounds), [e0, e1) its own extras
+        const int sg = segm && live ? (r_lo + ri) / a.seg_rows - s_lo : 0;
+        const int p0 = seg_vb[sg];
+        const int plim = live ? p0 + min(rplen[ri], seg_kp[sg]) : 0;
         const int e0 = live ? XB + rxo[ri] : 0, e1 = live ? XB + rxo[ri] + rnx[ri] : 0;
         const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
         const int pair_bar = 1 + (warp & 3);   // named barrier of warps w and w + 4
@@ -502,6 +534,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const TcAttnArgs a
                 const int jc = j0 + (4 * h + q) * 16;
                 const int lim = plim - jc;
                 uint32_t m = lim >= 16 ? 0xFFFFu : (lim > 0 ? (1u << lim) - 1u : 0u);
+                const int lo = p0 - jc;   // 0 for a single segment
+                if (lo > 0) m &= lo >= 16 ? 0u : ~((1u << lo) - 1u);
                 const int x0 = max(0, e0 - jc), x1 = min(16, e1 - jc);
                 if (x1 > x0) m |= ((1u << x1) - 1u) & ~((1u << x0) - 1u);
                 msk[q] = m;
@@ -654,6 +688,7 @@ bool attn_tc_fits(int m_max, int nh, int nkv, int hd, int extra_max) {
     const int rows = kQT / G + 2;
     return rows <= kMaxRows && (int64_t)rows * extra_max <= kMaxX;
 }
+int attn_tc_max_segments() { return kMaxSeg; }
 
 // ranks per tile: enough CTAs to cover the SMs once.  A function of the tile
 // count alone (not of M or the context length), so a verify row and the same
@@ -689,13 +724,14 @@ static cudaError_t launch_tc(const TcAttnArgs& a, dim3 grid, int S, cudaStream_t
 
 int launch_attn_tc(const float* q, const int32_t* dM, int m_max, const int32_t* plen, const int32_t* n_extra,
                    const int32_t* extra, int extra_max, const void* kc, const void* vc, const int32_t* page_table,
-                   int nh, int nkv, int hd, int max_plen, void* o, cudaStream_t s, const void* qsw, int qsw_tiles) {
+                   int nh, int nkv, int hd, int max_plen, void* o, cudaStream_t s, const void* qsw, int qsw_tiles,
+                   int seg_rows, int pt_stride) {
     const int G = nh / nkv;
     const int n_qt = (m_max * G + kQT - 1) / kQT;
     if (qsw && qsw_tiles < n_qt) return CARD_E_CONFIG;
     const int S = attn_tc_ranks(n_qt * nkv);
     TcAttnArgs a{q, dM, plen, n_extra, extra, extra_max, (const __nv_bfloat16*)kc, (const __nv_bfloat16*)vc,
-                 page_table, nh, nkv, (__nv_bfloat16*)o, (const uint8_t*)qsw, qsw_tiles};
+                 page_table, nh, nkv, (__nv_bfloat16*)o, (const uint8_t*)qsw, qsw_tiles, seg_rows, pt_stride};
     const dim3 grid(S, n_qt, nkv);
     const cudaError_t e = hd == 64 ? launch_tc<64>(a, grid, S, s) : launch_tc<128>(a, grid, S, s);
     if (e != cudaSuccess) {

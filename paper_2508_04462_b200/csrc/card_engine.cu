@@ -51,20 +51,50 @@ namespace card {
 __device__ __forceinline__ int pslot(const int32_t* pt, int p) { return pt ? pt[p >> 6] * 64 + (p & 63) : p; }
 
 // ---------------------------------------------------------------- row builders
+// A request's region of a batched row block: its rows start
+// at row_base of the combined block (R points there), at most rows_cap of
+// them, outputs at most out_cap; the rest of the region is padding rows
+// (plen 0, no extras, KV written to dead_slot) so the combined forward can
+// run over every region.  rows_cap == 0: a single request owning the block
+// header (M, n_out).
+struct RowSlot {
+    int row_base, rows_cap, out_cap, dead_slot;
+};
+
+__device__ void pad_rows(CardRows R, const RowSlot& B, int m0, int o0, int tid, int nt) {
+    for (int m = m0 + tid; m < B.rows_cap; m += nt) {
+        R.tok[m] = 0;
+        R.pos[m] = 0;
+        R.slot[m] = B.dead_slot;
+        R.plen[m] = 0;
+        R.n_extra[m] = 0;
+    }
+    for (int o = o0 + tid; o < B.out_cap; o += nt) R.out_rows[o] = B.row_base + B.rows_cap - 1;
+}
+
 __global__ void draft_rows_kernel(card_engine_state* E, const card_cache_state* S, const int32_t* __restrict__ ntoken,
                                   const int32_t* __restrict__ nparent, const int32_t* __restrict__ nlayer,
                                   const int32_t* __restrict__ frontier, const int32_t* __restrict__ committed,
-                                  CardRows R, int tree_base, int32_t* ctx_tail, int order, const int32_t* pt) {
+                                  CardRows R, int tree_base, int32_t* ctx_tail, int order, const int32_t* pt,
+                                  RowSlot B) {
     // one thread per catch-up row and per frontier row (the ancestor walks of
     // the frontier nodes run in parallel)
     const int tid = threadIdx.x;
-    if (E->stop || E->done) {
-        if (tid == 0) {
+    const bool batch = B.rows_cap > 0;
+    // batched: spare[0] = expansions left in this cycle (set by the host,
+    // min(ratio, max_depth - depth) as engine.py:303-310); spent -> stop
+    const bool spent = batch && !E->stop && !E->done && E->spare[0] <= 0;
+    __syncthreads();
+    if (E->stop || E->done || spent) {
+        if (batch) pad_rows(R, B, 0, 0, tid, blockDim.x);
+        else if (tid == 0) {
             *R.M = 0;
             *R.n_out = 0;
         }
+        if (spent && tid == 0) E->stop = 1;
         return;
     }
+    if (batch && tid == 0) E->spare[0] -= 1;
     const int C = E->C;
     const int nf = S->n_frontier;
     const int anchor = E->anchor_origin ? 0 : S->root;
@@ -73,6 +103,11 @@ __global__ void draft_rows_kernel(card_engine_state* E, const card_cache_state* 
     if (nf == 0) {
         // flat forward of the committed context (engine.py:210-213)
         const int start = Pd < C - 1 ? Pd : C - 1;
+        if (batch && C - start > B.rows_cap) {   // region too small: fail loudly
+            if (tid == 0) E->done = -1;
+            pad_rows(R, B, 0, 0, tid, blockDim.x);
+            return;
+        }
         for (int p = start + tid; p < C; p += blockDim.x) {
             const int m = p - start;
             R.tok[m] = committed[p];
@@ -86,16 +121,24 @@ __global__ void draft_rows_kernel(card_engine_state* E, const card_cache_state* 
                 const int p = C - order + j;
                 ctx_tail[j] = p >= 0 ? committed[p] : -1;
             }
+        if (batch) pad_rows(R, B, C - start, 1, tid, blockDim.x);
         __syncthreads();
         if (tid == 0) {
-            R.out_rows[0] = C - start - 1;
-            *R.n_out = 1;
-            *R.M = C - start;
+            R.out_rows[0] = B.row_base + C - start - 1;
+            if (!batch) {
+                *R.n_out = 1;
+                *R.M = C - start;
+            }
             E->Pd = C;
         }
         return;
     }
     const int n_catch = Pd < base ? base - Pd : 0;
+    if (batch && (n_catch + nf > B.rows_cap || nf > B.out_cap)) {
+        if (tid == 0) E->done = -1;
+        pad_rows(R, B, 0, 0, tid, blockDim.x);
+        return;
+    }
     for (int i = tid; i < n_catch; i += blockDim.x) {   // catch-up rows (no outputs)
         const int p = Pd + i;
         R.tok[i] = committed[p];
@@ -120,7 +163,7 @@ __global__ void draft_rows_kernel(card_engine_state* E, const card_cache_state* 
         R.slot[m] = tree_base + f;
         R.plen[m] = base;
         R.n_extra[m] = d;
-        R.out_rows[i] = m;
+        R.out_rows[i] = B.row_base + m;
         if (ctx_tail) {
             // tail of base + path: last `order` tokens (path node = ex[q] - tree_base)
             for (int j = 0; j < order; ++j) {
@@ -135,21 +178,28 @@ __global__ void draft_rows_kernel(card_engine_state* E, const card_cache_state* 
             }
         }
     }
+    if (batch) pad_rows(R, B, n_catch + nf, nf, tid, blockDim.x);
     __syncthreads();
     if (tid == 0) {
-        *R.n_out = nf;
-        *R.M = n_catch + nf;
+        if (!batch) {
+            *R.n_out = nf;
+            *R.M = n_catch + nf;
+        }
         if (Pd < base) E->Pd = base;
     }
 }
 
 __global__ void target_rows_kernel(card_engine_state* E, const card_cache_state* S, const int32_t* __restrict__ q_tok,
                                    const int32_t* __restrict__ committed, CardRows R, int32_t* ctx_tail, int order,
-                                   const int32_t* pt) {
+                                   const int32_t* pt, RowSlot B) {
     if (threadIdx.x != 0) return;
+    const bool batch = B.rows_cap > 0;
     if (E->done) {
-        *R.M = 0;
-        *R.n_out = 0;
+        if (batch) pad_rows(R, B, 0, 0, 0, 1);
+        else {
+            *R.M = 0;
+            *R.n_out = 0;
+        }
         return;
     }
     const int C = E->C;
@@ -163,7 +213,7 @@ __global__ void target_rows_kernel(card_engine_state* E, const card_cache_state*
         R.slot[i] = pslot(pt, p);
         R.plen[i] = p + 1;
         R.n_extra[i] = 0;
-        R.out_rows[i] = i;
+        R.out_rows[i] = B.row_base + i;
         if (ctx_tail)
             for (int j = 0; j < order; ++j) {
                 const int q = i - order + j;   // index into candidate prefix
@@ -176,8 +226,11 @@ __global__ void target_rows_kernel(card_engine_state* E, const card_cache_state*
                 ctx_tail[(int64_t)i * order + j] = t;
             }
     }
-    *R.M = L + 1;
-    *R.n_out = L + 1;
+    if (batch) pad_rows(R, B, L + 1, L + 1, 0, 1);
+    else {
+        *R.M = L + 1;
+        *R.n_out = L + 1;
+    }
 }
 
 // EOS is absorbing (lm.py:148-150): rows whose context ends in EOS become a one-hot.
@@ -565,7 +618,7 @@ int card_draft_rows(card_engine_state* E, card_cache* h, const int32_t* committe
     CardRows R = make_rows(rows, rows + 1, rows + 2, rows + 2 + rm, rows + 2 + 2 * rm, rows + 2 + 3 * rm,
                            rows + 2 + 4 * rm, rows + 2 + 6 * rm, rows + 2 + 5 * rm, rm, extra_max);
     draft_rows_kernel<<<1, 128, 0, (cudaStream_t)stream>>>(E, S, tok, par, lay, fr, committed, R, tree_base, ctx_tail,
-                                                         order, page_table);
+                                                         order, page_table, RowSlot{0, 0, 0, 0});
     CARD_LAUNCH_CHECK();
     return CARD_OK;
 }
@@ -581,7 +634,55 @@ int card_target_rows(card_engine_state* E, card_cache* h, const int32_t* committ
     const int rm = rows_max;
     CardRows R = make_rows(rows, rows + 1, rows + 2, rows + 2 + rm, rows + 2 + 2 * rm, rows + 2 + 3 * rm,
                            rows + 2 + 4 * rm, rows + 2 + 6 * rm, rows + 2 + 5 * rm, rm, extra_max);
-    target_rows_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(E, S, qt, committed, R, ctx_tail, order, page_table);
+    target_rows_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(E, S, qt, committed, R, ctx_tail, order, page_table,
+                                                         RowSlot{0, 0, 0, 0});
+    CARD_LAUNCH_CHECK();
+    return CARD_OK;
+}
+
+// Batched row builders: the request writes its region
+// [row_base, row_base + rows_cap) of a combined block of rows_max rows (and
+// outputs [out_base, out_base + out_cap)); padding fills the rest of the
+// region.  The block header (M, n_out) is the caller's (the region sizes).
+// A request whose rows do not fit its region ends with done = -1.
+int card_draft_rows_at(card_engine_state* E, card_cache* h, const int32_t* committed, int32_t* rows, int rows_max,
+                       int extra_max, int row_base, int rows_cap, int out_base, int out_cap, int dead_slot,
+                       int tree_base, int32_t* ctx_tail, int order, const int32_t* page_table, void* stream) {
+    if (!E || !h || !rows || rows_cap <= 0 || out_cap <= 0 || row_base < 0 || row_base + rows_cap > rows_max ||
+        out_base < 0 || out_base + out_cap > rows_max)
+        return CARD_E_INPUT;
+    card_cache_state* S;
+    int32_t *tok, *par, *lay, *fr;
+    int rc = card_cache_device_ptrs(h, &S, &tok, &par, &lay, &fr, nullptr, nullptr, nullptr);
+    if (rc) return rc;
+    const int rm = rows_max, b = row_base;
+    CardRows R = make_rows(rows, rows + 1, rows + 2 + b, rows + 2 + rm + b, rows + 2 + 2 * rm + b,
+                           rows + 2 + 3 * rm + b, rows + 2 + 4 * rm + b, rows + 2 + 6 * rm + (int64_t)b * extra_max,
+                           rows + 2 + 5 * rm + out_base, rows_cap, extra_max);
+    draft_rows_kernel<<<1, 128, 0, (cudaStream_t)stream>>>(E, S, tok, par, lay, fr, committed, R, tree_base,
+                                                         ctx_tail ? ctx_tail + (int64_t)out_base * order : nullptr,
+                                                         order, page_table, RowSlot{row_base, rows_cap, out_cap, dead_slot});
+    CARD_LAUNCH_CHECK();
+    return CARD_OK;
+}
+
+int card_target_rows_at(card_engine_state* E, card_cache* h, const int32_t* committed, int32_t* rows, int rows_max,
+                        int extra_max, int row_base, int rows_cap, int dead_slot, int32_t* ctx_tail, int order,
+                        const int32_t* page_table, void* stream) {
+    if (!E || !h || !rows || rows_cap <= 0 || row_base < 0 || row_base + rows_cap > rows_max) return CARD_E_INPUT;
+    card_cache_state* S;
+    int rc = card_cache_device_ptrs(h, &S, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr);
+    if (rc) return rc;
+    int32_t *qp, *qt;
+    double* qe;
+    card_cache_query_buffers(h, &qp, &qt, &qe);
+    const int rm = rows_max, b = row_base;
+    CardRows R = make_rows(rows, rows + 1, rows + 2 + b, rows + 2 + rm + b, rows + 2 + 2 * rm + b,
+                           rows + 2 + 3 * rm + b, rows + 2 + 4 * rm + b, rows + 2 + 6 * rm + (int64_t)b * extra_max,
+                           rows + 2 + 5 * rm + b, rows_cap, extra_max);
+    target_rows_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(E, S, qt, committed, R,
+                                                         ctx_tail ? ctx_tail + (int64_t)row_base * order : nullptr,
+                                                         order, page_table, RowSlot{row_base, rows_cap, rows_cap, dead_slot});
     CARD_LAUNCH_CHECK();
     return CARD_OK;
 }

@@ -1101,6 +1101,23 @@ int card_attention_tree(const void* qsw, int qsw_tiles, const int32_t* dM, int m
     return rc;
 }
 
+int card_attention_batch(const float* q, const void* qsw, int qsw_tiles, const int32_t* dM, int m_max,
+                         const int32_t* plen, const int32_t* n_extra, const int32_t* extra, int extra_max,
+                         const void* kc, const void* vc, const int32_t* page_tables, int pt_stride, int seg_rows,
+                         int nh, int nkv, int hd, int max_plen, void* o, void* stream) {
+    if ((!q && !qsw) || !dM || !plen || !kc || !vc || !o || !page_tables || m_max <= 0 || nkv <= 0 || nh % nkv ||
+        seg_rows <= 0 || pt_stride <= 0)
+        return CARD_E_INPUT;
+    const int G = nh / nkv;
+    // segments one tile of 128 query-heads can span
+    if (!attn_tc_fits(m_max, nh, nkv, hd, extra_max) || (128 / G + 2 + seg_rows - 1) / seg_rows + 1 > attn_tc_max_segments())
+        return CARD_E_CONFIG;
+    const int rc = launch_attn_tc(q, dM, m_max, plen, n_extra, extra, extra_max, kc, vc, page_tables, nh, nkv, hd,
+                                  max_plen, o, (cudaStream_t)stream, qsw, qsw_tiles, seg_rows, pt_stride);
+    if (rc == CARD_OK) CARD_LAUNCH_CHECK();
+    return rc;
+}
+
 // vocab splits of the lm_head readers: about six CTAs per SM (the logits are
 // L2-warm right after the lm_head; more parallel reads win in-graph, +0.6 %
 // bench tokens/s against two per SM, same-box A/B)

@@ -21,7 +21,8 @@ int attn_tc_set_trace(unsigned long long* buf);
 int launch_attn_tc(const float* q, const int32_t* dM, int m_max, const int32_t* plen, const int32_t* n_extra,
                    const int32_t* extra, int extra_max, const void* kc, const void* vc, const int32_t* page_table,
                    int nh, int nkv, int hd, int max_plen, void* o, cudaStream_t s, const void* qsw = nullptr,
-                   int qsw_tiles = 0);
+                   int qsw_tiles = 0, int seg_rows = 0, int pt_stride = 0);
+int attn_tc_max_segments();
 }  // namespace card
 
 // GEMM epilogues (card_gemm.cu)

@@ -39,6 +39,7 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <math.h>
+#include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -713,8 +714,15 @@ int card_pfwd_create(int n_layers, int H, int F, int nh, int nkv, int hd, int m_
     if (a.WS > 8) a.WS = 8;
     h->smem = fixed + a.WS * pf::kWBytes + a.XS * xbytes;
     if (e == cudaSuccess && ws_floats) e = cudaMalloc(&h->ws, ws_floats * sizeof(float));
-    if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(pf::pfwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, h->smem);
+    // one attribute for every instance (the largest any plan can ask for):
+    // a per-instance value would be overwritten by the last plan created
+    int optin = 0;
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaFuncAttributes fa;
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, pf::pfwd_kernel);
+    const int dyn_max = optin - (int)fa.sharedSizeBytes;
+    if (e == cudaSuccess && h->smem > dyn_max) e = cudaErrorInvalidValue;
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(pf::pfwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_max);
     if (e != cudaSuccess) {
         set_cuda_error(e);
         if (h->d_layers) cudaFree(h->d_layers);
@@ -784,6 +792,10 @@ int card_pfwd_run(card_pfwd* h, const int32_t* dM, int step_begin, int step_end,
     cudaError_t e = cudaLaunchKernelEx(&cfg, pf::pfwd_kernel, h->tmXb, h->tmO, h->tmG, a);
     if (e != cudaSuccess) {
         set_cuda_error(e);
+        int nb = -1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, pf::pfwd_kernel, pf::kThreads, h->smem);
+        fprintf(stderr, "card_pfwd_run: %s (grid %d, smem %d, blocks/SM %d)\n", cudaGetErrorString(e), h->grid,
+                h->smem, nb);
         return CARD_E_CUDA;
     }
     return CARD_OK;

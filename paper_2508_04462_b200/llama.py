@@ -574,7 +574,8 @@ class DeviceLlama:
             return None
         return PageTable(self.page_pool, self.prefix_slots // PAGE, device or self.dev)
 
-    def forward(self, rows: "RowBlock", m_max: int, topk: bool = False, pages: "PageTable | None" = None):
+    def forward(self, rows: "RowBlock", m_max: int, topk: bool = False, pages: "PageTable | None" = None,
+                batch: "BatchPages | None" = None):
         """Run the forward over the device rows; logits for the output rows
         land in self.logits[:n_out] (topk=True: the lm_head_topk records
         instead, see lm_topk_head).  pages: the request's page table (the
@@ -585,9 +586,11 @@ class DeviceLlama:
         s = stream_ptr()
         plan = self.plans[m_max]
         if self.fused:
-            return self._forward_fused(rows, plan, topk, pages)
+            return self._forward_fused(rows, plan, topk, pages, batch)
         if topk:
             raise ConfigError("the fused top-k lm_head needs the bf16 path")
+        if batch is not None:
+            raise ConfigError("batched forwards run the bf16 paged path")
         dM, dOut = rows.M, rows.n_out
         hd = c.head_dim
         mm = plan["m_max"]   # grids sized for this plan's rows (rows >= M exit at once)
@@ -631,7 +634,30 @@ class DeviceLlama:
             plan["bound_rows"] = None   # rebind the row offset of the new head
         return lin
 
-    def _forward_fused(self, rows: "RowBlock", plan: dict, topk: bool = False, pages: "PageTable | None" = None):
+    def _attend(self, li: int, rows: "RowBlock", mm: int, pages, batch, qsw=None, qsw_tiles: int = 0):
+        """Attention of layer li over the row block: one request's paged KV
+        (pages), or several requests' (batch: each row region its own table)."""
+        c = self.cfg
+        L_ = lib()
+        if batch is not None:
+            return raise_for_status(L_.card_attention_batch(
+                None if qsw is not None else ptr(self.q), ptr(qsw), qsw_tiles, ptr(rows.M), mm, ptr(rows.plen),
+                ptr(rows.n_extra), ptr(rows.extra), rows.extra_max, ptr(self.k_cache[li]), ptr(self.v_cache[li]),
+                ptr(batch.tables), batch.stride, batch.seg_rows, c.n_heads, c.n_kv_heads, c.head_dim,
+                self.prefix_slots, ptr(self.o), stream_ptr()), "attention (batch)")
+        pt = ptr(pages.dev) if pages is not None else None
+        if qsw is not None:
+            return raise_for_status(L_.card_attention_tree(
+                ptr(qsw), qsw_tiles, ptr(rows.M), mm, ptr(rows.plen), ptr(rows.n_extra), ptr(rows.extra),
+                rows.extra_max, ptr(self.k_cache[li]), ptr(self.v_cache[li]), pt, c.n_heads, c.n_kv_heads,
+                c.head_dim, self.prefix_slots, ptr(self.o), stream_ptr()), "attention")
+        return raise_for_status(L_.card_attention_paged(
+            ptr(self.q), ptr(rows.M), mm, ptr(rows.plen), ptr(rows.n_extra), ptr(rows.extra), rows.extra_max,
+            ptr(self.k_cache[li]), ptr(self.v_cache[li]), pt, c.n_heads, c.n_kv_heads, c.head_dim,
+            self.prefix_slots, ptr(self.o), stream_ptr()), "attention")
+
+    def _forward_fused(self, rows: "RowBlock", plan: dict, topk: bool = False, pages: "PageTable | None" = None,
+                       batch: "BatchPages | None" = None):
         c = self.cfg
         L_ = lib()
         s = stream_ptr()
@@ -646,28 +672,15 @@ class DeviceLlama:
             n5 = _PFwd.PHASES
             tree_q = pf.use_qsw(rows.extra_max)
             pf.run(dM, 0, 1)   # layer 0 qkv
-            pt = ptr(pages.dev) if pages is not None else None
             for li in range(c.n_layers):
-                if tree_q:
-                    chk(L_.card_attention_tree(ptr(pf.qsw), pf.qsw_tiles, ptr(dM), mm, ptr(rows.plen),
-                                               ptr(rows.n_extra), ptr(rows.extra), rows.extra_max,
-                                               ptr(self.k_cache[li]), ptr(self.v_cache[li]), pt, c.n_heads,
-                                               c.n_kv_heads, c.head_dim, self.prefix_slots, ptr(self.o), s), "attention")
-                else:
-                    chk(L_.card_attention_paged(ptr(self.q), ptr(dM), mm, ptr(rows.plen), ptr(rows.n_extra),
-                                                ptr(rows.extra), rows.extra_max, ptr(self.k_cache[li]),
-                                                ptr(self.v_cache[li]), pt, c.n_heads, c.n_kv_heads, c.head_dim,
-                                                self.prefix_slots, ptr(self.o), s), "attention")
+                self._attend(li, rows, mm, pages, batch, pf.qsw if tree_q else None, pf.qsw_tiles if tree_q else 0)
                 # o, gate/up, down of layer li, then the qkv of layer li + 1
                 pf.run(dM, n5 * li + 2, min(n5 * (li + 1) + 1, n5 * c.n_layers))
             plan["lm_head_topk" if topk else "lm_head"].run(rows.n_out)
             return
         for li, P in enumerate(plan["layers"]):
             P["qkv"].run(dM)
-            chk(L_.card_attention_paged(ptr(self.q), ptr(dM), mm, ptr(rows.plen), ptr(rows.n_extra), ptr(rows.extra),
-                                        rows.extra_max, ptr(self.k_cache[li]), ptr(self.v_cache[li]),
-                                        ptr(pages.dev) if pages is not None else None, c.n_heads, c.n_kv_heads,
-                                        c.head_dim, self.prefix_slots, ptr(self.o), s), "attention")
+            self._attend(li, rows, mm, pages, batch)
             P["o"].run(dM)
             if self.tp is not None:
                 self._tp_reduce(dM, mm)
@@ -684,6 +697,16 @@ class DeviceLlama:
     def launches_per_forward(self) -> int:
         gu_extra = 0
         return 2 + self.cfg.n_layers * (2 + 1 + 1 + 3 + 1 + 1 + 1 + gu_extra) + 2
+
+
+@dataclass
+class BatchPages:
+    """Page tables of the requests of a batched forward: request i owns rows
+    [i * seg_rows, (i + 1) * seg_rows) and its prefix page table is
+    tables[i] (int32 [B, stride] on the device)."""
+    tables: torch.Tensor
+    stride: int
+    seg_rows: int
 
 
 class RowBlock:
