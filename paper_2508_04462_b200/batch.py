@@ -10,10 +10,14 @@ reference schedule of engine.py:290-317 (serial_sim, correction on):
 
 * its own candidate tree (device arena + hash, cache.py), engine state,
   committed tokens, prefix KV pages and tree-KV slots, and uniforms;
-* its own region of the combined row blocks: ``rows_d = K + ratio + 2``
+* its own region of the combined row blocks: ``rows_d = K + CATCH_UP``
   draft rows (frontier + catch-up), ``K`` draft outputs and
   ``query_depth + 1`` verify rows, padded when shorter
-  (card_draft_rows_at / card_target_rows_at);
+  (card_draft_rows_at / card_target_rows_at).  Catch-up rows are the
+  committed tokens without draft KV: the correction token and at most one
+  accepted frontier node (the accepted chain's other KV is promoted from
+  tree slots, card_draft_promote), so CATCH_UP = 4 leaves margin; a request
+  that overflows its region stops with a ProtocolError;
 * per cycle its own number of draft expansions, min(ratio, max_depth -
   depth) (engine.py:303-310): a request whose budget or frontier runs out
   stops expanding while the others go on.
@@ -25,6 +29,9 @@ parallel branches of the captured graphs.
 
 ``K`` is per request: a batch shares the lm_head/top-k rows of one forward,
 so callers scale K down with B (``batch_config``).
+A forward holds at most MAX_ROWS rows (the tcgen05 GEMM's TMEM tile);
+``run_speculative_batched`` splits larger batches into sub-batches whose
+cycles interleave on separate streams.
 """
 
 from __future__ import annotations
@@ -46,6 +53,13 @@ from .errors import ConfigError, ProtocolError, raise_for_status
 from .metrics import finalize
 
 _SPARE0 = EngineState.spare.offset // 4   # per-cycle draft budget (card_draft_rows_at)
+CATCH_UP = 4      # draft catch-up rows per request region
+MAX_ROWS = 256    # rows of one forward (tc_gemm: Mpad <= 256)
+
+
+def max_batch(config: EngineConfig) -> int:
+    """Requests one BatchRun can hold (draft and verify regions <= MAX_ROWS)."""
+    return max(1, min(MAX_ROWS // (config.K + CATCH_UP), MAX_ROWS // (config.query_depth + 1)))
 
 
 def batch_config(config: EngineConfig, n_requests: int) -> EngineConfig:
@@ -81,9 +95,12 @@ class BatchRun:
         self.cap = 6 * cfg.K * (cfg.max_depth + 1) + 256
         self.K = cfg.K
         self.k = cfg.k
-        self.rd = cfg.K + cfg.ratio + 2            # draft rows per request (frontier + catch-up)
+        self.rd = cfg.K + CATCH_UP                 # draft rows per request (frontier + catch-up)
         self.rt_rows = cfg.query_depth + 1        # verify rows per request
         self.Md, self.Mt = B * self.rd, B * self.rt_rows
+        if max(self.Md, self.Mt) > MAX_ROWS:
+            raise ConfigError(f"{B} requests need {self.Md} draft / {self.Mt} verify rows per forward "
+                              f"(at most {MAX_ROWS}); use run_speculative_batched, which splits the batch")
         self.XM = cfg.max_depth + 1
         order = max(1, draft.bias.order, target.bias.order)
         self.order = order
@@ -325,8 +342,14 @@ class BatchRun:
         self.E[:, _SPARE0].copy_(self._budget, non_blocking=True)
         self.io["h2d"] += 4 * self.B
 
+    @staticmethod
+    def _event():
+        ev = torch.cuda.Event()
+        ev.record()
+        return ev
+
     def _read(self) -> list[EngineState]:
-        torch.cuda.current_stream().synchronize()
+        """The states copied at the end of the last cycle (its event completed)."""
         self.io["d2h"] += self.E.numel() * 4
         raw = self._host.numpy()
         out = [EngineState.from_buffer_copy(raw[i].tobytes()) for i in range(self.B)]
@@ -338,6 +361,12 @@ class BatchRun:
     def run(self):
         """The serial_sim schedule of every request (engine.py:290-317), the
         requests' steps sharing each forward; one host round trip per cycle."""
+        for ev in self.cycles():
+            ev.synchronize()
+
+    def cycles(self):
+        """run() as a generator: each cycle launches its graphs on the current
+        stream, records an event and yields it; resume once it completed."""
         cfg = self.cfg
         d_lat = self.draft_model.spec.forward_latency
         t_lat = self.target_model.spec.forward_latency
@@ -350,6 +379,7 @@ class BatchRun:
             g_d.replay()
             self.replays[0] += 1
         self._host.copy_(self.E, non_blocking=True)
+        yield self._event()
         for i, E in enumerate(self._read()):
             for w in list(E.widths)[:min(E.n_widths, 64)]:
                 if w == 0:
@@ -368,6 +398,7 @@ class BatchRun:
             g_t.replay()
             self.replays[0] += max(budgets)
             self.replays[1] += 1
+            yield self._event()
             for i, E in enumerate(self._read()):
                 if not live[i]:
                     continue
@@ -393,25 +424,53 @@ class BatchRun:
 def run_speculative_batched(draft, target, prompts: Sequence[Sequence[int]], config: EngineConfig,
                             ) -> tuple[list[RunResult], dict]:
     """Decode every prompt with shared draft / verify forwards (BatchRun).
-    ``config`` is per request (see batch_config).  Returns (results, timing):
-    timing["decode_ms"] is the device time of the batched decode,
-    timing["tokens"] the tokens all requests emitted."""
-    run = BatchRun(draft, target, prompts, config)
-    run.prefill()
-    run.capture()
+    ``config`` is per request (see batch_config).  Batches larger than
+    max_batch(config) run as sub-batches whose cycles interleave on their
+    own streams.  Returns (results, timing): timing["decode_ms"] is the
+    device time of the whole decode, timing["tokens"] the tokens all
+    requests emitted."""
+    per = max_batch(config)
+    groups = [list(prompts[j:j + per]) for j in range(0, len(prompts), per)]
+    runs = [BatchRun(draft, target, g, config) for g in groups]
+    streams = [torch.cuda.Stream() for _ in runs]
+    for run in runs:
+        run.prefill()
+        run.capture()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record()
-    run.run()
+    pending = []
+    for run, st in zip(runs, streams):
+        st.wait_event(ev0)
+        with torch.cuda.stream(st):
+            gen = run.cycles()
+            pending.append((gen, next(gen), st))
+    while pending:
+        nxt = []
+        for gen, ev, st in pending:
+            if not ev.query():
+                nxt.append((gen, ev, st))
+                continue
+            with torch.cuda.stream(st):
+                try:
+                    nxt.append((gen, next(gen), st))
+                except StopIteration:
+                    pass
+        pending = nxt
+    for st in streams:
+        torch.cuda.current_stream().wait_stream(st)
     ev1.record()
     ev1.synchronize()
     wall = time.perf_counter() - t0
-    timing = {"decode_ms": ev0.elapsed_time(ev1), "wall_s": wall, "requests": run.B,
-              "tokens": sum(len(o) for o in run.outputs), "draft_steps": run.replays[0],
-              "target_steps": run.replays[1], "launches_per_graph": run.launches_per_graph,
-              "gpu_launches": run.replays[0] * run.launches_per_graph[0] + run.replays[1] * run.launches_per_graph[1],
-              "h2d_bytes": run.io["h2d"], "d2h_bytes": run.io["d2h"], "K_per_request": run.K}
+    lpg = runs[0].launches_per_graph
+    timing = {"decode_ms": ev0.elapsed_time(ev1), "wall_s": wall, "requests": len(prompts), "sub_batches": len(runs),
+              "tokens": sum(len(o) for r in runs for o in r.outputs),
+              "draft_steps": sum(r.replays[0] for r in runs), "target_steps": sum(r.replays[1] for r in runs),
+              "gpu_launches": sum(r.replays[0] * r.launches_per_graph[0] + r.replays[1] * r.launches_per_graph[1]
+                                  for r in runs),
+              "launches_per_graph": lpg, "h2d_bytes": sum(r.io["h2d"] for r in runs),
+              "d2h_bytes": sum(r.io["d2h"] for r in runs), "K_per_request": config.K}
     results = [RunResult(output=o, metrics=finalize(t, target.spec, draft.spec), trace=t, wall=timing)
-               for o, t in zip(run.outputs, run.traces)]
+               for r in runs for o, t in zip(r.outputs, r.traces)]
     return results, timing

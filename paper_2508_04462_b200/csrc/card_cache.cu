@@ -593,7 +593,16 @@ __global__ void __launch_bounds__(kThreads) correct_kernel(Bufs b, const int32_t
         S.root = new_root;
         S.epoch += 1;
         S.dead += sh_dead;
-        sh_flag = (n >= kCompactMinArena && (double)S.dead > 0.75 * (double)n) ? 1 : 0;  // cache.py:471-474
+        // cache.py:471-474; and, unlike the reference's unbounded arena, when
+        // the next cycle's expansions (<= max_depth layers of <= K nodes) could
+        // overflow the fixed device arena.  At small K the reference's
+        // condition can stay false for a whole decode (the committed chain
+        // stays alive as ancestors).  Compaction is order-preserving, so every
+        // decision (sort / query tie-breaks on node ids) is unchanged; only
+        // absolute ids differ from the reference's arena from then on.
+        const bool ref_rule = n >= kCompactMinArena && (double)S.dead > 0.75 * (double)n;
+        const bool pressure = n + S.K * (S.max_depth + 1) + 2 > S.capacity;
+        sh_flag = (ref_rule || pressure) ? 1 : 0;
         S.n_precompact = n;
     }
     __syncthreads();
