@@ -647,7 +647,7 @@ int card_pfwd_create(int n_layers, int H, int F, int nh, int nkv, int hd, int m_
     if (!out || !layer_w || !kv || !x || !xb || !ssq || !q || !o || !g || !pos || !slot || !cos_t || !sin_t)
         return CARD_E_INPUT;
     *out = nullptr;
-    if (n_layers <= 0 || n_layers > pf::kMaxLayers || m_max <= 16 || m_max > pf::kMaxMpad || act_rows < m_max)
+    if (n_layers <= 0 || n_layers > pf::kMaxLayers || m_max < 1 || m_max > pf::kMaxMpad || act_rows < m_max)
         return CARD_E_CONFIG;
     if ((hd != 64 && hd != 128) || H % pf::kTileN || F % 64 || ((nh + 2 * nkv) * hd) % pf::kTileN ||
         (nh * hd) % pf::kBK || H % pf::kBK)

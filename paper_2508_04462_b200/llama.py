@@ -524,6 +524,8 @@ class DeviceLlama:
             plan["layers"].append({"qkv": qkv, "o": o, "gu": gu, "d": d})
         plan["lm_head"] = _Linear(self.lm_head, self.xb, m_max, EPI_STORE_F32,
                                   self.logits if self.tp is None else self.logits_local, c.vocab_size)
+        # (narrow plans — verify, AR — keep the per-GEMM kernels: a persistent
+        # M = 8 verify of Llama-3.1-8B measured 4.03 vs 3.31 ms, tools/pfwd_target_probe.py)
         if self.persistent and self.tp is None and 16 < m_max <= 128:
             plan["pfwd"] = _PFwd(self, m_max)
         return plan
@@ -670,7 +672,9 @@ class DeviceLlama:
         pf = plan.get("pfwd")
         if pf is not None:
             n5 = _PFwd.PHASES
-            tree_q = pf.use_qsw(rows.extra_max)
+            # wide row blocks read Q pre-swizzled by the tcgen05 attention; narrow
+            # ones (verify, AR) keep fp32 q for the register-resident kernel
+            tree_q = pf.use_qsw(rows.extra_max if mm * (c.n_heads // c.n_kv_heads) >= 256 else 1 << 30)
             pf.run(dM, 0, 1)   # layer 0 qkv
             for li in range(c.n_layers):
                 self._attend(li, rows, mm, pages, batch, pf.qsw if tree_q else None, pf.qsw_tiles if tree_q else 0)

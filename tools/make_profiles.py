@@ -84,13 +84,15 @@ if os.path.exists(p):
 KEYS = ["Duration", "DRAM Throughput", "Memory Throughput", "Compute (SM) Throughput", "Elapsed Cycles",
         "Registers Per Thread", "Grid Size", "Cluster Size", "Dynamic Shared Memory Per Block", "Achieved Occupancy",
         "L2 Hit Rate", "Max Active Clusters"]
-for rep in ("gemm_gu_t8", "gemm_qkv_d116"):
+for rep in ("gemm_gu_t8", "gemm_qkv_d116", "pfwd_d116", "attn_tc_d116", "lmhead_topk"):
     p = os.path.join(SRC, rep + ".ncu-rep")
     if not os.path.exists(p):
         continue
     det = subprocess.run(["ncu", "-i", p, "--page", "details", "--csv"], capture_output=True, text=True).stdout
     raw = subprocess.run(["ncu", "-i", p, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     lines = [f"# ncu --set full --clock-control none capture: {rep} (tools/profile_round.sh)"]
+    if os.path.exists(os.path.join(SRC, rep + ".log")):
+        lines.append("# " + open(os.path.join(SRC, rep + ".log")).read().strip().splitlines()[-1][:200])
     drows = list(csv.reader(det.splitlines()))
     dh = drows[0]
     si, ni, ui, vi = (dh.index(c) for c in ("Section Name", "Metric Name", "Metric Unit", "Metric Value"))
