@@ -53,6 +53,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--ar-steps", type=int, default=2)
+    ap.add_argument("--batch", type=int, default=1,
+                    help="requests decoded together per step (BatchRun, K // batch each; BASELINE configs[4]); "
+                         "value = aggregate tokens/s")
     ap.add_argument("--tp", action="store_true",
                     help="under torchrun: one request, target tensor-parallel over all ranks (NCCL), draft "
                          "replicated (BASELINE configs[3] with --target llama-3.1-70b)")
@@ -427,8 +430,18 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
+    if args.batch > 1:
+        bcfg = card.batch_config(cfg, args.batch)
+        P = prompts((args.warmup + args.steps) * args.batch, tcfg.vocab_size, args.prompt_len, rank)
+
+        def one_step(j):
+            res, tm = card.run_speculative_batched(draft, target, P[j * args.batch:(j + 1) * args.batch], bcfg)
+            return res, tm
     for i in range(args.warmup):
-        card.run_speculative(draft, target, P[i], cfg)
+        if args.batch > 1:
+            one_step(i)
+        else:
+            card.run_speculative(draft, target, P[i], cfg)
     barrier()
     clocks = ClockSampler(local)
     clocks.start()
@@ -440,9 +453,22 @@ def main():
     hits = []
     t_steps = 0
     outs = []
+    h2d = d2h = 0
     for i in range(args.steps):
         barrier()
         t0 = time.perf_counter()
+        if args.batch > 1:
+            results, tm = one_step(args.warmup + i)
+            e2e_s += time.perf_counter() - t0
+            dec_ms += tm["decode_ms"]
+            tokens += tm["tokens"]
+            launches += tm["gpu_launches"]
+            acc += [r.metrics.mean_acceptance_length for r in results]
+            hits += [r.metrics.cache_hit_rate for r in results]
+            t_steps += tm["target_steps"]
+            h2d += tm["h2d_bytes"]
+            d2h += tm["d2h_bytes"]
+            continue
         res = card.run_speculative(draft, target, P[args.warmup + i], cfg)
         e2e_s += time.perf_counter() - t0
         dec_ms += res.wall["decode_ms"]
@@ -451,6 +477,8 @@ def main():
         acc.append(res.metrics.mean_acceptance_length)
         hits.append(res.metrics.cache_hit_rate)
         t_steps += res.wall.get("target_steps", 0)
+        h2d += res.wall.get("h2d_bytes", 0)
+        d2h += res.wall.get("d2h_bytes", 0)
         outs.append(res.output)
     barrier()
     clk = clocks.stop()
@@ -472,6 +500,9 @@ def main():
     if args.temperature > 0.0:
         lossless = None   # sampled tokens differ by design; losslessness is distributional (tests)
     ar_value = ar_tok / (ar_ms / 1000.0)
+    if args.batch > 1:   # the single-request runtimes the roofline probes measure (outside the timed region)
+        card.run_speculative(draft, target, P[0], card.EngineConfig(K=args.K, k=args.k, ratio=args.ratio,
+                                                                     max_new_tokens=8))
     roof = measure_roofline(target, args.ratio + 1, args.prompt_len + args.new_tokens // 2, peak)
     roof.update(measure_draft(draft, args.K + 2 * args.ratio + 2, args.prompt_len + args.new_tokens // 2, peak))
     tr = traffic_from_profiles()
@@ -483,7 +514,10 @@ def main():
         "warmup": args.warmup, "ms_per_step": round(max_ms / args.steps, 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (random-init weights, uniform random prompt tokens)",
-        "config": {"workload": f"CARD {args.draft} draft + {args.target} target, 1 request/GPU (time-shared)",
+        "config": {"workload": f"CARD {args.draft} draft + {args.target} target, "
+                               + (f"{args.batch} requests/GPU batched (K={args.K // args.batch} each)" if args.batch > 1
+                                  else "1 request/GPU (time-shared)"),
+                   "batch": args.batch,
                    "model": f"{args.draft}+{args.target}", "global_batch": world, "seq_len": args.prompt_len,
                    "new_tokens": args.new_tokens, "K": args.K, "k": args.k, "ratio": args.ratio,
                    "temperature": args.temperature, "mode": args.mode, "parallelism": f"tp{world} target + replicated draft" if tp else f"dp{world} replicas",
@@ -494,9 +528,11 @@ def main():
         "mean_acceptance_length": round(sum(acc) / len(acc), 4),
         "cache_hit_rate": round(sum(hits) / len(hits), 4),
         "lossless_vs_ar": lossless,
+        # copy bytes counted by the run itself (DeviceRun.io / BatchRun.io):
+        # prompt, engine state, uniforms, per-cycle budgets up; state records down
         "e2e": {"value": round(all_tokens / max_e2e, 3), "unit": UNIT,
-                "h2d_bytes_per_step": args.prompt_len * 4 + 1400,
-                "d2h_bytes_per_step": int(1400 * (t_steps / max(1, args.steps) + 2))},
+                "h2d_bytes_per_step": int(h2d / max(1, args.steps)),
+                "d2h_bytes_per_step": int(d2h / max(1, args.steps))},
         "gpu_launches": launches,
         "roofline": roof,
         "peak_source": peak_src,

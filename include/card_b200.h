@@ -127,6 +127,9 @@ int card_cache_pool(card_cache* h, const double* dists, int n_rows, int vocab,
 /* query(depth) (cache.py:277-318).  Result in the state block (q_hit, q_len)
  * and in the cache's query buffers (card_cache_query_buffers). */
 int card_cache_query(card_cache* h, int depth, void* stream);
+/* card_cache_query unless *skip != 0 (device flag; the mailbox driver's
+ * "no correction arrived" flag) */
+int card_cache_query_if(card_cache* h, int depth, const int32_t* skip, void* stream);
 int card_cache_query_buffers(card_cache* h, int32_t** path, int32_t** tok, double** edge);
 
 /* correct(accepted, correction) (cache.py:355-413).  All inputs on the
@@ -345,6 +348,32 @@ int card_draft_rows(card_engine_state* E, card_cache* h, const int32_t* committe
 int card_target_rows(card_engine_state* E, card_cache* h, const int32_t* committed, int32_t* rows,
                      int rows_max, int extra_max, int32_t* ctx_tail, int order, const int32_t* page_table,
                      void* stream);
+/* Draft <-> target mailboxes of mode="concurrent" across two GPUs
+ * (engine.py:320-389 lock + epoch).  Each direction is
+ * a box in the receiver's memory written by the sender's kernel with P2P
+ * stores and published by a system-scope release of a sequence number:
+ * the query box (target GPU) carries the path queried after a correction
+ * and the tree epoch; the commit box (draft GPU) the verify outcome.
+ *   draft stream, every draft step: poll_commit (a new commit -> the draft
+ *     state, skip flag 0; else 1), card_cache_correct / card_cache_query_if
+ *     gated by the skip flag, publish_query (force = 0: only after a
+ *     correction), then the expansion;
+ *   target stream, every verify: wait_query (blocks on an acquire poll),
+ *     card_target_rows_view on the delivered query, forward, verify,
+ *     commit, publish_commit.
+ * Devices may be equal (then the boxes are local). */
+typedef struct card_mailbox card_mailbox;
+int card_mailbox_create(int draft_dev, int target_dev, card_mailbox** out);
+int card_mailbox_destroy(card_mailbox* m);
+/* boxes and sequence numbers to zero between requests (both devices idle) */
+int card_mailbox_reset(card_mailbox* m);
+int card_mailbox_skip_flag(card_mailbox* m, int32_t** skip);
+int card_mailbox_query_view(card_mailbox* m, card_cache_state** view, int32_t** q_tok);
+int card_mailbox_poll_commit(card_mailbox* m, card_engine_state* draft_state, void* stream);
+int card_mailbox_publish_query(card_mailbox* m, card_cache* h, int force, void* stream);
+int card_mailbox_wait_query(card_mailbox* m, void* stream);
+int card_mailbox_publish_commit(card_mailbox* m, const card_engine_state* target_state, void* stream);
+
 /* Batched decode (the reference runs one request at a time,
  * engine.py:275-287): each request builds its rows into its own region
  * [row_base, row_base + rows_cap) of one combined row block of rows_max rows
@@ -359,6 +388,12 @@ int card_draft_rows_at(card_engine_state* E, card_cache* h, const int32_t* commi
 int card_target_rows_at(card_engine_state* E, card_cache* h, const int32_t* committed, int32_t* rows, int rows_max,
                         int extra_max, int row_base, int rows_cap, int dead_slot, int32_t* ctx_tail, int order,
                         const int32_t* page_table, void* stream);
+/* card_target_rows with the queried path taken from an explicit view (the
+ * q_hit / q_len fields of a card_cache_state and the path tokens), e.g. the
+ * copy a card_mailbox delivered into the target GPU's memory. */
+int card_target_rows_view(card_engine_state* E, const card_cache_state* view, const int32_t* q_tok,
+                          const int32_t* committed, int32_t* rows, int rows_max, int extra_max, int32_t* ctx_tail,
+                          int order, const int32_t* page_table, void* stream);
 int card_eos_fix(const int32_t* n_rows, int m_max, const int32_t* ctx_tail, int order, int eos, int V,
                  double* probs, void* stream);
 int card_record_width(card_engine_state* E, card_cache* h, const int32_t* n_out, void* stream);

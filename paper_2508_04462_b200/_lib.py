@@ -44,6 +44,17 @@ SIGNATURES = {
     "card_cache_expand_topk": (c_int, [_P, _P, _P, _P, c_int, c_int, _P, _P]),
     "card_cache_pool": (c_int, [_P, _P, c_int, c_int, _P, _P, _P, _P, _P]),
     "card_cache_query": (c_int, [_P, c_int, _P]),
+    "card_cache_query_if": (c_int, [_P, c_int, _P, _P]),
+    "card_mailbox_create": (c_int, [c_int, c_int, POINTER(c_void_p)]),
+    "card_mailbox_destroy": (c_int, [_P]),
+    "card_mailbox_reset": (c_int, [_P]),
+    "card_mailbox_skip_flag": (c_int, [_P, POINTER(c_void_p)]),
+    "card_mailbox_query_view": (c_int, [_P, POINTER(c_void_p), POINTER(c_void_p)]),
+    "card_mailbox_poll_commit": (c_int, [_P, _P, _P]),
+    "card_mailbox_publish_query": (c_int, [_P, _P, c_int, _P]),
+    "card_mailbox_wait_query": (c_int, [_P, _P]),
+    "card_mailbox_publish_commit": (c_int, [_P, _P, _P]),
+    "card_target_rows_view": (c_int, [_P, _P, _P, _P, _P, c_int, c_int, _P, c_int, _P, _P]),
     "card_cache_query_buffers": (c_int, [_P, POINTER(c_void_p), POINTER(c_void_p), POINTER(c_void_p)]),
     "card_cache_correct": (c_int, [_P, _P, _P, _P, _P, _P]),
     "card_cache_advance_root": (c_int, [_P, _P, _P, _P, _P]),
@@ -138,7 +149,9 @@ LAUNCHES = {
     "card_draft_rows": 1, "card_target_rows": 1, "card_draft_rows_at": 1, "card_target_rows_at": 1, "card_eos_fix": 1, "card_record_width": 1,
     "card_attention_paged": 1, "card_verify_argmax": 1, "card_verify_probs": 1, "card_commit": 1, "card_verify_result": 1, "card_draft_promote": 2,
     "card_kv_compact": 2, "card_cycle_end": 1, "card_engine_handoff": 1, "card_pfwd_run": 1, "card_attention_tree": 1,
-    "card_attention_batch": 1,
+    "card_attention_batch": 1, "card_cache_query_if": 1, "card_mailbox_poll_commit": 1,
+    "card_mailbox_publish_query": 1, "card_mailbox_wait_query": 1, "card_mailbox_publish_commit": 1,
+    "card_target_rows_view": 1,
 }
 launch_count = [0]
 

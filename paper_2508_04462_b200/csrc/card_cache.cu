@@ -361,7 +361,8 @@ __global__ void pool_kernel(Bufs b, int32_t* o_tok, double* o_w, int32_t* o_pidx
 }
 
 // ---------------------------------------------------------------- query
-__global__ void __launch_bounds__(kThreads) query_kernel(Bufs b, int depth) {
+__global__ void __launch_bounds__(kThreads) query_kernel(Bufs b, int depth, const int32_t* skip) {
+    if (skip && *skip) return;   // (mailbox driver: no correction arrived, nothing to query)
     card_cache_state& S = *b.st;
     __shared__ double bs[32];
     __shared__ int bt[32], bi[32];
@@ -898,7 +899,15 @@ int card_cache_pool(card_cache* h, const double* dists, int n_rows, int vocab, i
 int card_cache_query(card_cache* h, int depth, void* stream) {
     if (!h) return CARD_E_INPUT;
     if (depth < 1) return CARD_E_INPUT;
-    query_kernel<<<1, 256, 0, (cudaStream_t)stream>>>(h->b, depth);
+    query_kernel<<<1, 256, 0, (cudaStream_t)stream>>>(h->b, depth, nullptr);
+    CARD_LAUNCH_CHECK();
+    return CARD_OK;
+}
+
+// card_cache_query unless *skip (device flag)
+int card_cache_query_if(card_cache* h, int depth, const int32_t* skip, void* stream) {
+    if (!h || depth < 1) return CARD_E_INPUT;
+    query_kernel<<<1, 256, 0, (cudaStream_t)stream>>>(h->b, depth, skip);
     CARD_LAUNCH_CHECK();
     return CARD_OK;
 }

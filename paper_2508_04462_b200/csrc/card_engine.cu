@@ -640,6 +640,21 @@ int card_target_rows(card_engine_state* E, card_cache* h, const int32_t* committ
     return CARD_OK;
 }
 
+// target rows from an explicit query view (the mailbox driver: the query
+// arrived in the target GPU's memory, card_mailbox_query_view)
+int card_target_rows_view(card_engine_state* E, const card_cache_state* view, const int32_t* q_tok,
+                          const int32_t* committed, int32_t* rows, int rows_max, int extra_max, int32_t* ctx_tail,
+                          int order, const int32_t* page_table, void* stream) {
+    if (!E || !view || !q_tok || !rows) return CARD_E_INPUT;
+    const int rm = rows_max;
+    CardRows R = make_rows(rows, rows + 1, rows + 2, rows + 2 + rm, rows + 2 + 2 * rm, rows + 2 + 3 * rm,
+                           rows + 2 + 4 * rm, rows + 2 + 6 * rm, rows + 2 + 5 * rm, rm, extra_max);
+    target_rows_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(E, view, q_tok, committed, R, ctx_tail, order, page_table,
+                                                         RowSlot{0, 0, 0, 0});
+    CARD_LAUNCH_CHECK();
+    return CARD_OK;
+}
+
 // Batched row builders: the request writes its region
 // [row_base, row_base + rows_cap) of a combined block of rows_max rows (and
 // outputs [out_base, out_base + out_cap)); padding fills the rest of the

@@ -777,6 +777,7 @@ class _ConcurrentDriver:
 
         self.run = run
         dd, td = run.dev_d, run.dev_t
+        run.q_tok_ptr = ctypes.c_void_p(run.cache._qbufs[1])   # the verify reads the cache's query buffer
         # the draft stream gets the higher priority: with the target verifying
         # concurrently, accepted tokens per second track draft layers per
         # second (each layer adds about one token of depth the next verify can
@@ -900,6 +901,161 @@ class _ConcurrentDriver:
         return sum(r * n for r, n in zip(self.replays, self.per_graph))
 
 
+class _MailboxDriver(_ConcurrentDriver):
+    """mode="concurrent" with the exchange in device mailboxes
+    (csrc/card_mailbox.cu): the default when the draft and
+    the target live on two GPUs.  Neither side waits on the host or on the
+    other's stream: the target's verify graph opens with a kernel that
+    blocks on the query box (an acquire poll on memory the draft GPU writes
+    with P2P stores and a system-scope release), and every draft step opens
+    with a non-blocking poll of the commit box, then corrects the tree,
+    queries it and publishes the query before it expands.  The tree is
+    mutated only by the draft stream, so an expansion always follows the
+    latest correction it has seen (the reference's epoch check,
+    engine.py:359-360, can never fire); the epoch rides along with each
+    query.  The host only keeps one draft step in flight, relaunches the
+    verify graph and reads the records for the trace."""
+
+    def __init__(self, run: "DeviceRun"):
+        from . import _lib
+
+        self.run = run
+        dd, td = run.dev_d, run.dev_t
+        rt = getattr(run.da, "rt", None)
+        if dd == td and rt is not None and any("pfwd" in p for p in rt.plans.values()):
+            # the target's verify graph blocks on the query box while the draft's
+            # persistent forward needs every SM (cooperative launch): on one GPU
+            # the two would wait for each other
+            raise ConfigError("exchange='mailbox' on one GPU needs a draft without the persistent forward "
+                              "(LlamaModel(persistent=False)); use exchange='events' or two GPUs")
+        L_ = lib()
+        h = ctypes.c_void_p()
+        raise_for_status(L_.card_mailbox_create(dd.index, td.index, ctypes.byref(h)), "card_mailbox_create")
+        self.mb = h
+        skip = ctypes.c_void_p()
+        L_.card_mailbox_skip_flag(h, ctypes.byref(skip))
+        view, q_tok = ctypes.c_void_p(), ctypes.c_void_p()
+        L_.card_mailbox_query_view(h, ctypes.byref(view), ctypes.byref(q_tok))
+        self.skip, self.view = skip, view
+        run.q_tok_ptr = q_tok   # the verify reads the delivered candidate tokens
+        self.D = torch.cuda.Stream(device=dd, priority=-8)
+        self.T = torch.cuda.Stream(device=td, priority=0)
+        self.g_d, self.g_q, self.g_t, self.g_c = (torch.cuda.CUDAGraph() for _ in range(4))
+        c = [_lib.launch_count[0]]
+
+        def capture(g, dev, fn):
+            with torch.cuda.device(dev):
+                cap = torch.cuda.Stream(device=dev)
+                cap.wait_stream(torch.cuda.current_stream(dev))
+                with torch.cuda.stream(cap), torch.cuda.graph(g, stream=cap):
+                    fn()
+                torch.cuda.current_stream(dev).wait_stream(cap)
+            c.append(_lib.launch_count[0])
+
+        cache = run.cache.handle
+
+        def exchange():   # the draft side of one exchange: poll, correct, query, publish (all gated)
+            s = stream_ptr()
+            raise_for_status(L_.card_mailbox_poll_commit(h, run.Ed_ptr, s), "poll_commit")
+            raise_for_status(L_.card_cache_correct(cache, run._fptr("acc", True), run._fptr("n_acc", True),
+                                                   run._fptr("corr", True), skip, s), "correct")
+            run.da.post_correct(run)
+            raise_for_status(L_.card_cache_query_if(cache, run.cfg.query_depth, skip, s), "query_if")
+            raise_for_status(L_.card_mailbox_publish_query(h, cache, 0, s), "publish_query")
+
+        def draft_step():
+            exchange()
+            run.launch_draft_step()
+            run._host_d.copy_(run.Ed, non_blocking=True)
+
+        def exchange_only():
+            exchange()
+            run._host_d.copy_(run.Ed, non_blocking=True)
+
+        def first_query():
+            s = stream_ptr()
+            raise_for_status(L_.card_cache_query(cache, run.cfg.query_depth, s), "query")
+            raise_for_status(L_.card_mailbox_publish_query(h, cache, 1, s), "publish_query")
+
+        def target_step():
+            s = stream_ptr()
+            raise_for_status(L_.card_mailbox_wait_query(h, s), "wait_query")
+            raise_for_status(L_.card_target_rows_view(run.E_ptr, view, q_tok, ptr(run.committed),
+                                                      ptr(run.trt.rows.block), run.t_rows_max, 1, ptr(run.trt.tail),
+                                                      run.trt.order, _pt(run.ta), s), "target_rows_view")
+            run.ta.target(run)
+            raise_for_status(L_.card_commit(run.E_ptr, ptr(run.committed), s), "commit")
+            raise_for_status(L_.card_mailbox_publish_commit(h, run.E_ptr, s), "publish_commit")
+            raise_for_status(L_.card_cycle_end(run.E_ptr, None, s), "cycle_end")
+            run._host.copy_(run.E, non_blocking=True)
+
+        capture(self.g_d, dd, draft_step)
+        capture(self.g_q, dd, first_query)
+        capture(self.g_t, td, target_step)
+        capture(self.g_c, dd, exchange_only)
+        self.per_graph = [c[i + 1] - c[i] for i in range(4)]
+        self.replays = [0, 0, 0, 0]
+
+    def __del__(self):
+        try:
+            lib().card_mailbox_destroy(self.mb)
+        except Exception:
+            pass
+
+    def _exchange(self):
+        with torch.cuda.stream(self.D):
+            self.g_c.replay()
+            ev = torch.cuda.Event()
+            ev.record(self.D)
+        self.replays[3] += 1
+        self.run.io["d2h"] += self.run.Ed.numel() * 4
+        return ev
+
+    def run_loop(self):
+        run, cfg = self.run, self.run.cfg
+        t0 = time.perf_counter()
+        for dev, st in ((run.dev_d, self.D), (run.dev_t, self.T)):
+            torch.cuda.current_stream(dev).synchronize()
+            st.wait_stream(torch.cuda.current_stream(dev))
+        # a previous request may have left a commit / query unread
+        raise_for_status(lib().card_mailbox_reset(self.mb), "card_mailbox_reset")
+        paused = False
+        for _ in range(min(cfg.query_depth, cfg.max_depth)):   # warm-up (engine.py:377)
+            ev = self._draft()
+            ev.synchronize()
+            if self._draft_done(t0):
+                paused = True
+                break
+        with torch.cuda.stream(self.D):
+            self.g_q.replay()
+        self.replays[1] += 1
+        d_ev = None
+        while True:
+            with torch.cuda.stream(self.T):
+                self.g_t.replay()   # blocks on the device until the next query arrives
+                v_ev = torch.cuda.Event()
+                v_ev.record(self.T)
+            self.replays[2] += 1
+            run.io["d2h"] += run.E.numel() * 4
+            while not v_ev.query():
+                if d_ev is not None and d_ev.query():
+                    paused = self._draft_done(t0)
+                    d_ev = None
+                if d_ev is None:   # a paused draft still polls, corrects and publishes
+                    d_ev = self._exchange() if paused else self._draft()
+            E = EngineState.from_buffer_copy(run._host.numpy().tobytes())
+            hit = bool(E.rec_hit)
+            run.output.extend(E.committed_now[i] for i in range(E.n_commit))
+            run._emit_target(self._now(t0), hit, E)
+            if E.rec_done:
+                break
+            run._emit(self._now(t0), hit, 0, 0, 0, "correct")
+        if d_ev is not None:
+            d_ev.synchronize()
+        for dev in {run.dev_d, run.dev_t}:
+            torch.cuda.synchronize(dev)
+
+
 def _validate_run_config(draft, target, config):
     """Limits of the device engine only (host-table pairs run the reference
     algorithm on the host and take any depth): the engine state keeps 64
@@ -952,8 +1108,13 @@ def _session_run(draft, target, prompt, config: EngineConfig, trace_alive: bool,
 
 def run_speculative(draft, target, prompt: Sequence[TokenId], config: EngineConfig, *,
                     use_graphs: bool | None = None, trace_alive: bool | None = None,
-                    devices: tuple[int, int] | None = None) -> RunResult:
+                    devices: tuple[int, int] | None = None, exchange: str | None = None) -> RunResult:
     """The generate() entry point (engine.py:275-287), on the device.
+
+    mode="concurrent": ``exchange`` picks how draft and target hand over
+    queries and corrections — "mailbox" (device mailboxes, the default when
+    ``devices`` puts them on two GPUs) or "events" (stream events and a host
+    hand-off, the default on one GPU).
 
     ``use_graphs`` (default: True for transformer pairs with correction on)
     selects the CUDA-graph driver; the stepwise driver reproduces the
@@ -978,9 +1139,14 @@ def run_speculative(draft, target, prompt: Sequence[TokenId], config: EngineConf
         run = _session_run(draft, target, prompt, config, False, devices=devices)
         t0 = time.perf_counter()
         run.prefill()
+        if exchange is None:
+            exchange = "mailbox" if run.dev_d != run.dev_t else "events"
+        if exchange not in ("mailbox", "events"):
+            raise ConfigError(f"exchange must be 'mailbox' or 'events', got {exchange!r}")
         drv = getattr(run, "_cdriver", None)
-        if drv is None:   # the four graphs are captured once per session
-            drv = run._cdriver = _ConcurrentDriver(run)
+        kind = _MailboxDriver if exchange == "mailbox" else _ConcurrentDriver
+        if type(drv) is not kind:   # the four graphs are captured once per session and exchange
+            drv = run._cdriver = kind(run)
         drv.replays = [0, 0, 0, 0]
         for dev in {run.dev_d, run.dev_t}:
             torch.cuda.synchronize(dev)

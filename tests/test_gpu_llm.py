@@ -188,28 +188,41 @@ def test_card_greedy_lossless_high_acceptance_bf16(card):
     assert res.output == van.output
 
 
+@pytest.mark.parametrize("exchange", ["events", "mailbox"])
 @pytest.mark.parametrize("dtype", ["fp32", "bf16"])
-def test_concurrent_mode_is_lossless(card, dtype):
-    """mode="concurrent" (engine.py:320-389): draft and target on two streams
-    with the device hand-off; greedy tokens equal autoregressive decoding."""
+def test_concurrent_mode_is_lossless(card, dtype, exchange):
+    """mode="concurrent" (engine.py:320-389): draft and target on two streams,
+    exchanging queries and corrections through stream events + a device
+    hand-off, or through the device mailboxes (csrc/card_mailbox.cu: the
+    target's verify graph blocks on the query box, each draft step polls
+    the commit box); greedy tokens equal autoregressive decoding, also for a
+    second request on the same session (the mailboxes are reset)."""
     from paper_2508_04462_b200.lm import LogitBias
 
     preset = ("tiny-target", "tiny-draft") if dtype == "fp32" else ("small-target", "small-draft")
     sharp = 30.0 if dtype == "fp32" else 4000.0
     bias = LogitBias(seed=11, order=2, sharpness=sharp, mix_seed=131, mix_weight=0.0)
     d, t, *_ = _tiny_pair(card, dtype, *preset, bias=bias)
+    if exchange == "mailbox":
+        # one GPU: the verify graph's mailbox wait and the draft's cooperative
+        # persistent forward cannot share the SMs (the driver refuses the mix)
+        d.persistent = False
     prompt = [int(x) for x in np.random.default_rng(7).integers(0, t.vocab.size, 48)]
     cfg = card.EngineConfig(K=16, k=3, ratio=5, max_new_tokens=160, mode="concurrent")
     van = card.run_vanilla(t, prompt, cfg)
-    res = card.run_speculative(d, t, prompt, cfg, use_graphs=True)
+    res = card.run_speculative(d, t, prompt, cfg, use_graphs=True, exchange=exchange)
     assert res.output == van.output
     assert res.wall["target_steps"] < len(res.output)   # more than one token per verify on average
     events = {e.event for e in res.trace}
     assert {"verify", "correct"} <= events
+    prompt2 = [int(x) for x in np.random.default_rng(17).integers(0, t.vocab.size, 48)]
+    again = card.run_speculative(d, t, prompt2, cfg, use_graphs=True, exchange=exchange)
+    assert again.output == card.run_vanilla(t, prompt2, cfg).output
 
 
+@pytest.mark.parametrize("exchange", ["events", "mailbox"])
 @pytest.mark.parametrize("devices", [(0, 0), (0, 1)])
-def test_concurrent_device_placement(card, devices):
+def test_concurrent_device_placement(card, devices, exchange):
     """Draft||target placement of mode="concurrent": the tree and draft state
     on the draft device, committed tokens and target state on the target
     device, each side reading the other's small buffers directly (P2P over
@@ -221,6 +234,8 @@ def test_concurrent_device_placement(card, devices):
 
     if max(devices) >= torch.cuda.device_count():
         pytest.skip("needs two GPUs")
+    if exchange == "mailbox" and devices[0] == devices[1]:
+        pytest.skip("one-GPU mailbox runs are covered by test_concurrent_mode_is_lossless")
     bias = LogitBias(seed=11, order=2, sharpness=4000.0)
     ct, cd = PRESETS["small-target"], PRESETS["small-draft"]
     with torch.cuda.device(devices[1]):
@@ -231,9 +246,21 @@ def test_concurrent_device_placement(card, devices):
     cfg = card.EngineConfig(K=16, k=3, ratio=5, max_new_tokens=128, mode="concurrent")
     with torch.cuda.device(devices[1]):
         van = card.run_vanilla(t, prompt, cfg)
-    res = card.run_speculative(d, t, prompt, cfg, use_graphs=True, devices=devices)
+    res = card.run_speculative(d, t, prompt, cfg, use_graphs=True, devices=devices, exchange=exchange)
     assert res.output == van.output
     assert res.wall["target_steps"] < len(res.output)
+
+
+def test_mailbox_refused_next_to_the_persistent_draft(card):
+    from paper_2508_04462_b200.errors import ConfigError
+    from paper_2508_04462_b200.lm import LogitBias
+
+    d, t, *_ = _tiny_pair(card, "bf16", "small-target", "small-draft", bias=LogitBias(seed=11, order=2,
+                                                                                       sharpness=4000.0))
+    prompt = [int(x) for x in np.random.default_rng(7).integers(0, t.vocab.size, 48)]
+    cfg = card.EngineConfig(K=16, k=3, ratio=5, max_new_tokens=16, mode="concurrent")
+    with pytest.raises(ConfigError):
+        card.run_speculative(d, t, prompt, cfg, use_graphs=True, exchange="mailbox")
 
 
 @pytest.mark.parametrize("mode", ["serial_sim", "concurrent"])
