@@ -709,6 +709,8 @@ int card_pfwd_create(int n_layers, int H, int F, int nh, int nkv, int hd, int m_
     const int xbytes = Mpad * pf::kBK * 2;
     const int fixed = 1024 + pf::kMaxMpad * 4 + 64 * 8 + 64;
     const int budget = 226 * 1024;   // + the kernel's static shared memory
+    // (activation stages: fewer measured slower; weight stages beyond 8 no
+    // faster — the gate/up stream is not ring-bound, tools/ab_so.sh)
     a.XS = 6;
     a.WS = (budget - fixed - a.XS * xbytes) / pf::kWBytes;
     if (a.WS > 8) a.WS = 8;
