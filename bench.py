@@ -53,6 +53,11 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--ar-steps", type=int, default=2)
+    ap.add_argument("--draft-sms", type=int, default=0,
+                    help="mode=concurrent on one GPU: SMs of the draft's partition (0: no partition)")
+    ap.add_argument("--exchange", default=None, choices=[None, "events", "mailbox"])
+    ap.add_argument("--draft-per-gemm", action="store_true",
+                    help="draft forward as per-GEMM kernels instead of the persistent cooperative kernel")
     ap.add_argument("--batch", type=int, default=1,
                     help="requests decoded together per step (BatchRun, K // batch each; BASELINE configs[4]); "
                          "value = aggregate tokens/s")
@@ -416,7 +421,7 @@ def main():
     target = card.LlamaModel(tcfg, seed=2, dtype="bf16", bias=bias,
                              spec=card.ModelSpec(tcfg.total_params() / 1e9, 7.0), tp=tp)
     draft = card.LlamaModel(dcfg, seed=1, dtype="bf16", bias=bias,
-                            spec=card.ModelSpec(dcfg.total_params() / 1e9, 1.0))
+                            spec=card.ModelSpec(dcfg.total_params() / 1e9, 1.0), persistent=not args.draft_per_gemm)
     torch.cuda.synchronize()
     init_s = time.perf_counter() - t_init
     cfg = card.EngineConfig(K=args.K, k=args.k, ratio=args.ratio, temperature=args.temperature,
@@ -437,11 +442,14 @@ def main():
         def one_step(j):
             res, tm = card.run_speculative_batched(draft, target, P[j * args.batch:(j + 1) * args.batch], bcfg)
             return res, tm
+    ckw = {}
+    if args.mode == "concurrent":
+        ckw = {"draft_sms": args.draft_sms or None, "exchange": args.exchange}
     for i in range(args.warmup):
         if args.batch > 1:
             one_step(i)
         else:
-            card.run_speculative(draft, target, P[i], cfg)
+            card.run_speculative(draft, target, P[i], cfg, **ckw)
     barrier()
     clocks = ClockSampler(local)
     clocks.start()
@@ -469,7 +477,7 @@ def main():
             h2d += tm["h2d_bytes"]
             d2h += tm["d2h_bytes"]
             continue
-        res = card.run_speculative(draft, target, P[args.warmup + i], cfg)
+        res = card.run_speculative(draft, target, P[args.warmup + i], cfg, **ckw)
         e2e_s += time.perf_counter() - t0
         dec_ms += res.wall["decode_ms"]
         tokens += len(res.output)
@@ -520,7 +528,9 @@ def main():
                    "batch": args.batch,
                    "model": f"{args.draft}+{args.target}", "global_batch": world, "seq_len": args.prompt_len,
                    "new_tokens": args.new_tokens, "K": args.K, "k": args.k, "ratio": args.ratio,
-                   "temperature": args.temperature, "mode": args.mode, "parallelism": f"tp{world} target + replicated draft" if tp else f"dp{world} replicas",
+                   "temperature": args.temperature, "mode": args.mode,
+                   **({"draft_sms": args.draft_sms, "exchange": args.exchange or "events"}
+                      if args.mode == "concurrent" else {}), "parallelism": f"tp{world} target + replicated draft" if tp else f"dp{world} replicas",
                    "agreement_knob": {"kgram_logit_bias_sharpness": args.bias_sharpness, "mix_weight": args.bias_mix},
                    "l2": "weights 17.5 GB >> 126 MB L2: streamed from HBM every step (no flush needed)"},
         "speedup_vs_ar": round(value / ar_value, 3),

@@ -241,6 +241,10 @@ int card_pfwd_create(int n_layers, int H, int F, int nh, int nkv, int hd, int m_
                      void* o, void* g, int act_rows, const int32_t* pos, const int32_t* slot, const float* cos_t,
                      const float* sin_t, float eps, card_pfwd** out);
 int card_pfwd_run(card_pfwd* h, const int32_t* dM, int step_begin, int step_end, void* stream);
+/* grid (CTAs, one per SM) of the next launches, with the split-K ways
+ * re-derived for it: the SM count of the partition the forward runs on
+ * (card_green); 0 = the whole device */
+int card_pfwd_set_grid(card_pfwd* h, int grid);
 /* qkv epilogue writes Q as pre-swizzled bf16 tiles for card_attention_tree
  * ([nkv][tiles][hd/64][128 x 64] SWIZZLE_128B; tiles >= ceil(Mpad*nh/nkv/128))
  * instead of fp32 q; NULL restores fp32 q */
@@ -348,6 +352,16 @@ int card_draft_rows(card_engine_state* E, card_cache* h, const int32_t* committe
 int card_target_rows(card_engine_state* E, card_cache* h, const int32_t* committed, int32_t* rows,
                      int rows_max, int extra_max, int32_t* ctx_tail, int order, const int32_t* page_table,
                      void* stream);
+/* SM partitions of one GPU for mode="concurrent" (engine.py:320-389): two
+ * green contexts, draft_sms SMs (rounded up to the partition granularity)
+ * for the draft and the rest for the target, each with a stream.  Kernels
+ * and CUDA graphs captured on a partition's stream run on its SMs only;
+ * memory is shared with the primary context. */
+typedef struct card_green card_green;
+int card_green_create(int device, int draft_sms, card_green** out);
+int card_green_stream(card_green* g, int part, void** stream, int* sms);
+int card_green_destroy(card_green* g);
+
 /* Draft <-> target mailboxes of mode="concurrent" across two GPUs
  * (engine.py:320-389 lock + epoch).  Each direction is
  * a box in the receiver's memory written by the sender's kernel with P2P

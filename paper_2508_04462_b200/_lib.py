@@ -82,6 +82,10 @@ SIGNATURES = {
     "card_pfwd_info": (c_int, [_P, _P]),
     "card_pfwd_bind": (c_int, [_P, _P, _P]),
     "card_pfwd_set_qsw": (c_int, [_P, _P, c_int]),
+    "card_pfwd_set_grid": (c_int, [_P, c_int]),
+    "card_green_create": (c_int, [c_int, c_int, POINTER(c_void_p)]),
+    "card_green_stream": (c_int, [_P, c_int, POINTER(c_void_p), POINTER(c_int)]),
+    "card_green_destroy": (c_int, [_P]),
     "card_pfwd_trace": (c_int, [_P, _P]),
     "card_pfwd_tune": (c_int, [_P, c_int, c_int]),
     "card_pfwd_destroy": (c_int, [_P]),

@@ -823,6 +823,27 @@ int card_pfwd_bind(card_pfwd* h, const int32_t* pos, const int32_t* slot) {
     return CARD_OK;
 }
 
+// grid of the next launches: G CTAs (one per SM of the partition the forward
+// runs on, card_green); split-K ways re-derived for G.  G = 0: the device.
+int card_pfwd_set_grid(card_pfwd* h, int G) {
+    if (!h || G < 0) return CARD_E_INPUT;
+    if (G == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&G, cudaDevAttrMultiProcessorCount, dev);
+    }
+    pf::Args& a = h->args;
+    for (int p = 0; p < pf::kPhases; ++p) {
+        if (p == pf::PH_ATTN) continue;
+        pf::Gemm& gm = a.gm[p];
+        gm.splits = (p == pf::PH_GU) ? 1 : pf_splits(gm.n_tiles, gm.kb_total, G);
+        if (gm.splits > 1 && gm.n_tiles > pf::kTileCtrs) gm.splits = 1;
+        gm.units = gm.n_tiles * gm.splits;
+    }
+    h->grid = G;
+    return CARD_OK;
+}
+
 // tuning: split-K ways of one GEMM phase (0 qkv, 2 o, 3 gate/up, 4 down)
 int card_pfwd_tune(card_pfwd* h, int phase, int splits) {
     if (!h || phase < 0 || phase >= pf::kPhases || phase == pf::PH_ATTN || splits < 1 || splits > pf::kMaxSplits)

@@ -756,6 +756,29 @@ class DeviceRun:
         return self.cycles
 
 
+_GREEN: dict = {}
+_DRAFT_PRIORITY = -8   # concurrent mode, shared SMs: the draft stream first (clamped to the highest priority)
+
+
+def _green_partition(device: int, draft_sms: int):
+    """The (draft, target) SM partitions of one GPU (card_green) as stream
+    pointers and SM counts, created once per process and split: graphs
+    captured on the streams keep referring to them, so they live as long
+    as the process."""
+    key = (device, draft_sms)
+    if key not in _GREEN:
+        g = ctypes.c_void_p()
+        raise_for_status(lib().card_green_create(device, draft_sms, ctypes.byref(g)), "card_green_create")
+        ptrs, sms = [], []
+        for part in (0, 1):
+            sp, n = ctypes.c_void_p(), ctypes.c_int()
+            raise_for_status(lib().card_green_stream(g, part, ctypes.byref(sp), ctypes.byref(n)), "card_green_stream")
+            ptrs.append(sp.value)
+            sms.append(n.value)
+        _GREEN[key] = (g, ptrs, sms)
+    return _GREEN[key][1], _GREEN[key][2]
+
+
 class _ConcurrentDriver:
     """mode="concurrent" (engine.py:320-389) on one GPU: the draft expands the
     tree on its own stream while the target verifies on another.  The
@@ -772,29 +795,63 @@ class _ConcurrentDriver:
     flight so a correction waits for at most one.  Greedy output is
     schedule-invariant (lossless); the trace carries wall-clock times."""
 
-    def __init__(self, run: "DeviceRun"):
+    def _streams(self, run: "DeviceRun", draft_sms: int | None):
+        """The draft and target streams.  draft_sms (one GPU): two SM
+        partitions (card_green), the draft's persistent forward sized to its
+        share; otherwise two streams sharing every SM, the draft's at the
+        higher priority (with the target verifying concurrently, accepted
+        tokens per second track draft layers per second)."""
+        dd, td = run.dev_d, run.dev_t
+        self.green = None
+        self.draft_sms = None
+        if draft_sms:
+            if dd != td:
+                raise ConfigError("draft_sms partitions one GPU; the draft and target are on two")
+            ptrs, sms = _green_partition(dd.index, int(draft_sms))
+            self.draft_sms, self.target_sms = sms
+            self.D = torch.cuda.ExternalStream(ptrs[0], device=dd)
+            self.T = torch.cuda.ExternalStream(ptrs[1], device=td)
+        else:
+            self.D = torch.cuda.Stream(device=dd, priority=_DRAFT_PRIORITY)
+            self.T = torch.cuda.Stream(device=td, priority=0)
+
+    def _capture_fn(self, counter):
+        """capture(graph, device, fn): on the side's own stream (a graph keeps
+        the SM partition of the stream it was captured on); the draft's
+        persistent forward sized to the partition while capturing."""
+        from . import _lib
+
+        def capture(g, dev, fn):
+            side = self.D if dev == self.run.dev_d else self.T
+            pf = [p["pfwd"] for p in getattr(getattr(self.run.da, "rt", None), "plans", {}).values() if "pfwd" in p] \
+                if (self.draft_sms and side is self.D) else []
+            for f in pf:
+                raise_for_status(lib().card_pfwd_set_grid(f.h, self.draft_sms), "card_pfwd_set_grid")
+            try:
+                with torch.cuda.device(dev):
+                    side.wait_stream(torch.cuda.current_stream(dev))
+                    with torch.cuda.stream(side), torch.cuda.graph(g, stream=side):
+                        fn()
+                    torch.cuda.current_stream(dev).wait_stream(side)
+            finally:
+                for f in pf:   # the serial drivers keep the whole device
+                    lib().card_pfwd_set_grid(f.h, 0)
+            counter.append(_lib.launch_count[0])
+        return capture
+
+    def __del__(self):
+        pass
+
+    def __init__(self, run: "DeviceRun", draft_sms: int | None = None):
         from . import _lib
 
         self.run = run
         dd, td = run.dev_d, run.dev_t
         run.q_tok_ptr = ctypes.c_void_p(run.cache._qbufs[1])   # the verify reads the cache's query buffer
-        # the draft stream gets the higher priority: with the target verifying
-        # concurrently, accepted tokens per second track draft layers per
-        # second (each layer adds about one token of depth the next verify can
-        # accept), so the draft's kernels are scheduled first
-        self.D = torch.cuda.Stream(device=dd, priority=-8)   # clamped to the highest priority
-        self.T = torch.cuda.Stream(device=td, priority=0)
+        self._streams(run, draft_sms)
         self.g_d, self.g_q, self.g_t, self.g_c = (torch.cuda.CUDAGraph() for _ in range(4))
         c = [_lib.launch_count[0]]
-
-        def capture(g, dev, fn):
-            with torch.cuda.device(dev):
-                cap = torch.cuda.Stream(device=dev)
-                cap.wait_stream(torch.cuda.current_stream(dev))
-                with torch.cuda.stream(cap), torch.cuda.graph(g, stream=cap):
-                    fn()
-                torch.cuda.current_stream(dev).wait_stream(cap)
-            c.append(_lib.launch_count[0])
+        capture = self._capture_fn(c)
 
         def draft_step():
             run.launch_draft_step()
@@ -916,18 +973,22 @@ class _MailboxDriver(_ConcurrentDriver):
     query.  The host only keeps one draft step in flight, relaunches the
     verify graph and reads the records for the trace."""
 
-    def __init__(self, run: "DeviceRun"):
+    def __init__(self, run: "DeviceRun", draft_sms: int | None = None):
         from . import _lib
 
         self.run = run
         dd, td = run.dev_d, run.dev_t
         rt = getattr(run.da, "rt", None)
+        if dd == td and draft_sms:
+            # measured: graphs on the two green-context streams did not run
+            # side by side, so the verify graph's blocking wait starved the draft
+            raise ConfigError("exchange='mailbox' does not run on SM partitions of one GPU; use exchange='events'")
         if dd == td and rt is not None and any("pfwd" in p for p in rt.plans.values()):
             # the target's verify graph blocks on the query box while the draft's
             # persistent forward needs every SM (cooperative launch): on one GPU
             # the two would wait for each other
             raise ConfigError("exchange='mailbox' on one GPU needs a draft without the persistent forward "
-                              "(LlamaModel(persistent=False)); use exchange='events' or two GPUs")
+                              "(LlamaModel(persistent=False)); or exchange='events' or two GPUs")
         L_ = lib()
         h = ctypes.c_void_p()
         raise_for_status(L_.card_mailbox_create(dd.index, td.index, ctypes.byref(h)), "card_mailbox_create")
@@ -938,19 +999,10 @@ class _MailboxDriver(_ConcurrentDriver):
         L_.card_mailbox_query_view(h, ctypes.byref(view), ctypes.byref(q_tok))
         self.skip, self.view = skip, view
         run.q_tok_ptr = q_tok   # the verify reads the delivered candidate tokens
-        self.D = torch.cuda.Stream(device=dd, priority=-8)
-        self.T = torch.cuda.Stream(device=td, priority=0)
+        self._streams(run, draft_sms)
         self.g_d, self.g_q, self.g_t, self.g_c = (torch.cuda.CUDAGraph() for _ in range(4))
         c = [_lib.launch_count[0]]
-
-        def capture(g, dev, fn):
-            with torch.cuda.device(dev):
-                cap = torch.cuda.Stream(device=dev)
-                cap.wait_stream(torch.cuda.current_stream(dev))
-                with torch.cuda.stream(cap), torch.cuda.graph(g, stream=cap):
-                    fn()
-                torch.cuda.current_stream(dev).wait_stream(cap)
-            c.append(_lib.launch_count[0])
+        capture = self._capture_fn(c)
 
         cache = run.cache.handle
 
@@ -1108,13 +1160,16 @@ def _session_run(draft, target, prompt, config: EngineConfig, trace_alive: bool,
 
 def run_speculative(draft, target, prompt: Sequence[TokenId], config: EngineConfig, *,
                     use_graphs: bool | None = None, trace_alive: bool | None = None,
-                    devices: tuple[int, int] | None = None, exchange: str | None = None) -> RunResult:
+                    devices: tuple[int, int] | None = None, exchange: str | None = None,
+                    draft_sms: int | None = None) -> RunResult:
     """The generate() entry point (engine.py:275-287), on the device.
 
     mode="concurrent": ``exchange`` picks how draft and target hand over
     queries and corrections — "mailbox" (device mailboxes, the default when
     ``devices`` puts them on two GPUs) or "events" (stream events and a host
-    hand-off, the default on one GPU).
+    hand-off, the default on one GPU).  ``draft_sms`` (one GPU) splits the
+    SMs into a draft partition of that many SMs and a target partition, so
+    the latency-bound draft steps and the bandwidth-bound verify overlap.
 
     ``use_graphs`` (default: True for transformer pairs with correction on)
     selects the CUDA-graph driver; the stepwise driver reproduces the
@@ -1145,8 +1200,10 @@ def run_speculative(draft, target, prompt: Sequence[TokenId], config: EngineConf
             raise ConfigError(f"exchange must be 'mailbox' or 'events', got {exchange!r}")
         drv = getattr(run, "_cdriver", None)
         kind = _MailboxDriver if exchange == "mailbox" else _ConcurrentDriver
-        if type(drv) is not kind:   # the four graphs are captured once per session and exchange
-            drv = run._cdriver = kind(run)
+        if type(drv) is not kind or drv.draft_sms_req != draft_sms:   # captured once per session and setup
+            run._cdriver = None
+            drv = run._cdriver = kind(run, draft_sms)
+            drv.draft_sms_req = draft_sms
         drv.replays = [0, 0, 0, 0]
         for dev in {run.dev_d, run.dev_t}:
             torch.cuda.synchronize(dev)

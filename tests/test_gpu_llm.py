@@ -251,6 +251,22 @@ def test_concurrent_device_placement(card, devices, exchange):
     assert res.wall["target_steps"] < len(res.output)
 
 
+@pytest.mark.parametrize("exchange", ["events"])
+def test_concurrent_sm_partitions_are_lossless(card, exchange):
+    """mode="concurrent" with the GPU split into a draft and a target SM
+    partition (card_green; draft_sms): graphs captured on the partition
+    streams, the draft's persistent forward sized to its share; greedy
+    tokens still equal autoregressive decoding."""
+    from paper_2508_04462_b200.lm import LogitBias
+
+    bias = LogitBias(seed=11, order=2, sharpness=4000.0)
+    d, t, *_ = _tiny_pair(card, "bf16", "small-target", "small-draft", bias=bias)
+    prompt = [int(x) for x in np.random.default_rng(9).integers(0, t.vocab.size, 48)]
+    cfg = card.EngineConfig(K=16, k=3, ratio=5, max_new_tokens=96, mode="concurrent")
+    res = card.run_speculative(d, t, prompt, cfg, use_graphs=True, exchange=exchange, draft_sms=48)
+    assert res.output == card.run_vanilla(t, prompt, cfg).output
+
+
 def test_mailbox_refused_next_to_the_persistent_draft(card):
     from paper_2508_04462_b200.errors import ConfigError
     from paper_2508_04462_b200.lm import LogitBias
@@ -261,6 +277,8 @@ def test_mailbox_refused_next_to_the_persistent_draft(card):
     cfg = card.EngineConfig(K=16, k=3, ratio=5, max_new_tokens=16, mode="concurrent")
     with pytest.raises(ConfigError):
         card.run_speculative(d, t, prompt, cfg, use_graphs=True, exchange="mailbox")
+    with pytest.raises(ConfigError):   # nor on SM partitions of one GPU
+        card.run_speculative(d, t, prompt, cfg, use_graphs=True, exchange="mailbox", draft_sms=48)
 
 
 @pytest.mark.parametrize("mode", ["serial_sim", "concurrent"])
