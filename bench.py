@@ -510,7 +510,7 @@ def main():
     ar_value = ar_tok / (ar_ms / 1000.0)
     if args.batch > 1:   # the single-request runtimes the roofline probes measure (outside the timed region)
         card.run_speculative(draft, target, P[0], card.EngineConfig(K=args.K, k=args.k, ratio=args.ratio,
-                                                                     max_new_tokens=8))
+                                                                     max_new_tokens=args.new_tokens))
     roof = measure_roofline(target, args.ratio + 1, args.prompt_len + args.new_tokens // 2, peak)
     roof.update(measure_draft(draft, args.K + 2 * args.ratio + 2, args.prompt_len + args.new_tokens // 2, peak))
     tr = traffic_from_profiles()
