@@ -142,6 +142,7 @@ class BatchRun:
             st.n_uni = rng_n
             states.append(bytes(st))
         self.E = torch.frombuffer(bytearray(b"".join(states)), dtype=torch.int32).view(B, -1).to(dev)
+        self._E0 = self.E.clone()   # initial states, for rebind()
         self.nE = self.E.shape[1]
         self.committed = torch.zeros((B, self.max_ctx + 8), dtype=torch.int32, device=dev)
         for i, p in enumerate(self.prompts):
@@ -181,6 +182,32 @@ class BatchRun:
         self.traces: list[list[StepTrace]] = [[] for _ in range(B)]
         self.graphs = None
         self.timing: dict = {}
+
+    def rebind(self, prompts: Sequence[Sequence[int]]):
+        """A new batch of prompts (same count and lengths) on this run's
+        buffers and captured graphs: every buffer a step could read goes back
+        to its constructor contents (trees cleared, states, committed tokens,
+        tails, reader outputs); call prefill() next."""
+        prompts = [_check_prompt(p, self.target_model.vocab.size) for p in prompts]
+        if [len(p) for p in prompts] != [len(p) for p in self.prompts]:
+            raise ConfigError("rebind needs prompts of the run's lengths")
+        self.prompts = prompts
+        for c, p in zip(self.caches, prompts):
+            c.clear(p[-1])
+        self.E.copy_(self._E0)
+        self.committed.zero_()
+        for i, p in enumerate(prompts):
+            self.committed[i, :len(p)] = torch.tensor(p, dtype=torch.int32)
+        self.tail_d.fill_(-1)
+        self.tail_t.fill_(-1)
+        for t in (self.tok, self.logp, self.cnt, self.amax, self.lm_work_d, self.lm_work_t, self.probs):
+            if t is not None:
+                t.zero_()
+        self.io = {"h2d": sum(4 * len(p) for p in prompts) + self.E.numel() * 4, "d2h": 0}
+        self.outputs = [[] for _ in range(self.B)]
+        self.traces = [[] for _ in range(self.B)]
+        if self.graphs is not None:
+            self.replays = [0, 0]
 
     # ------------------------------------------------------------ helpers
     def _Ep(self, i: int, field: str | None = None) -> ctypes.c_void_p:
@@ -421,6 +448,30 @@ class BatchRun:
                 depth[i] = E.rec_depth
 
 
+_SESSIONS_PER_TARGET = 4
+
+
+def _session(draft, target, prompts, config: EngineConfig, slot: int) -> BatchRun:
+    """A serving session per (pair, prompt lengths, config, sub-batch slot):
+    the BatchRun's buffers and captured graphs are built by the first batch
+    and rebound to the next ones, as a server captures its graphs once per
+    shape (engine._session_run does the same for single requests)."""
+    from .engine import _model_sig
+
+    key = (_model_sig(draft), _model_sig(target), tuple(len(p) for p in prompts),
+           tuple(sorted(config.to_dict().items())), slot)
+    store = target.__dict__.setdefault("_card_batch_sessions", {})
+    run = store.pop(key, None)
+    if run is not None and run.draft_model is draft:
+        run.rebind(prompts)
+    else:
+        run = BatchRun(draft, target, prompts, config)
+    store[key] = run
+    while len(store) > _SESSIONS_PER_TARGET:
+        store.pop(next(iter(store)))
+    return run
+
+
 def run_speculative_batched(draft, target, prompts: Sequence[Sequence[int]], config: EngineConfig,
                             ) -> tuple[list[RunResult], dict]:
     """Decode every prompt with shared draft / verify forwards (BatchRun).
@@ -431,11 +482,12 @@ def run_speculative_batched(draft, target, prompts: Sequence[Sequence[int]], con
     requests emitted."""
     per = max_batch(config)
     groups = [list(prompts[j:j + per]) for j in range(0, len(prompts), per)]
-    runs = [BatchRun(draft, target, g, config) for g in groups]
+    runs = [_session(draft, target, g, config, j) for j, g in enumerate(groups)]
     streams = [torch.cuda.Stream() for _ in runs]
     for run in runs:
         run.prefill()
-        run.capture()
+        if run.graphs is None:
+            run.capture()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

@@ -94,3 +94,19 @@ def test_batch_config_scales_frontier(pair):
     cfg = card.EngineConfig(K=100, k=3, ratio=7)
     assert card.batch_config(cfg, 8).K == 12
     assert card.batch_config(cfg, 200).K == 1
+
+
+def test_batch_session_reuse_equals_fresh_runs(pair):
+    """A second batch of the same shape reuses the first's buffers and
+    graphs (rebind): identical results to a run on fresh buffers."""
+    card, d, t = pair
+    cfg = card.EngineConfig(K=8, k=3, ratio=4, max_new_tokens=32)
+    first = _prompts(3, t.vocab.size, [40])
+    second = [[int(x) for x in np.random.default_rng(900 + i).integers(0, t.vocab.size, 40)] for i in range(3)]
+    card.run_speculative_batched(d, t, first, cfg)
+    reused, tm = card.run_speculative_batched(d, t, second, cfg)
+    t.__dict__.pop("_card_batch_sessions", None)
+    fresh, _ = card.run_speculative_batched(d, t, second, cfg)
+    for x, y in zip(reused, fresh):
+        assert x.output == y.output
+        assert [ev.to_dict() for ev in x.trace] == [ev.to_dict() for ev in y.trace]
