@@ -260,6 +260,12 @@ int card_pfwd_trace(card_pfwd* h, unsigned long long* trace);
 int card_pfwd_tune(card_pfwd* h, int phase, int splits);
 int card_pfwd_destroy(card_pfwd* h);
 
+/* The lm_head reads its n_out input rows as one contiguous block; for a
+ * batched draft step (whose output rows are spread over the requests'
+ * regions) copy row out_rows[o] of the bf16 residual and of its
+ * per-16-column sums of squares to row o of xb_out / ssq_out first. */
+int card_gather_rows(const int32_t* out_rows, const int32_t* n_out, int m_max, int H, const void* xb, const float* ssq,
+                     int ssq_ld, void* xb_out, float* ssq_out, int ssq_out_ld, void* stream);
 /* x[r] = E[tok[r]] (fp32 residual); if xb != NULL also its bf16 copy and the
  * per-16-column sums of squares ssq[(col/16)*ssq_ld + r] (fused-norm input) */
 /* Tensor-parallel target: after the NCCL all-reduce of a

@@ -90,6 +90,7 @@ SIGNATURES = {
     "card_pfwd_tune": (c_int, [_P, c_int, c_int]),
     "card_pfwd_destroy": (c_int, [_P]),
     "card_embed": (c_int, [_P, _P, c_int, _P, c_int, c_int, _P, _P, _P, c_int, _P]),
+    "card_gather_rows": (c_int, [_P, _P, c_int, c_int, _P, _P, c_int, _P, _P, c_int, _P]),
     "card_resid_add": (c_int, [_P, c_int, c_int, _P, _P, _P, _P, c_int, _P]),
     "card_rmsnorm": (c_int, [_P, _P, c_int, ctypes.c_float, _P, c_int, _P, _P, c_int, _P]),
     "card_rope_kv": (c_int, [_P, _P, c_int, _P, _P, _P, _P, c_int, c_int, c_int, _P, _P, _P, c_int, _P]),
@@ -153,7 +154,7 @@ LAUNCHES = {
     "card_draft_rows": 1, "card_target_rows": 1, "card_draft_rows_at": 1, "card_target_rows_at": 1, "card_eos_fix": 1, "card_record_width": 1,
     "card_attention_paged": 1, "card_verify_argmax": 1, "card_verify_probs": 1, "card_commit": 1, "card_verify_result": 1, "card_draft_promote": 2,
     "card_kv_compact": 2, "card_cycle_end": 1, "card_engine_handoff": 1, "card_pfwd_run": 1, "card_attention_tree": 1,
-    "card_attention_batch": 1, "card_cache_query_if": 1, "card_mailbox_poll_commit": 1,
+    "card_attention_batch": 1, "card_gather_rows": 1, "card_cache_query_if": 1, "card_mailbox_poll_commit": 1,
     "card_mailbox_publish_query": 1, "card_mailbox_wait_query": 1, "card_mailbox_publish_commit": 1,
     "card_target_rows_view": 1,
 }

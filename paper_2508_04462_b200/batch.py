@@ -109,9 +109,10 @@ class BatchRun:
         dev = self.dev
         self.rt_d = DeviceLlama(draft.shard_cfg, draft.packed, max_ctx=self.max_ctx, tree_slots=B * self.cap + 1,
                                 row_budgets=sorted({self.Md, PREFILL_CHUNK}), pool_requests=B,
-                                extra_max=max(32, self.XM))
+                                extra_max=max(32, self.XM), persistent=getattr(draft, "persistent", True))
         self.rt_t = DeviceLlama(target.shard_cfg, target.packed, max_ctx=self.max_ctx, tree_slots=1,
-                                row_budgets=sorted({self.Mt, PREFILL_CHUNK}), pool_requests=B)
+                                row_budgets=sorted({self.Mt, PREFILL_CHUNK}), pool_requests=B,
+                                persistent=getattr(target, "persistent", True))
         for rt in (self.rt_d, self.rt_t):
             if not rt.fused:
                 raise ConfigError("batched decode needs the fused bf16 path")
@@ -166,7 +167,28 @@ class BatchRun:
         self.lm_work_t = torch.zeros(lib().card_lmhead_work_floats(self.Mt, 1), dtype=torch.float32, device=dev)
         self.probs = torch.zeros((self.Mt, target.vocab.size), dtype=torch.float64, device=dev) \
             if self.sampling else None
-        self.head = self.rt_d.lm_topk_head(self.Md) if (draft.fused_topk and k <= 4) else None
+        # The lm_head reads its input rows as one contiguous block, but the
+        # draft's output rows are spread over the requests' regions: they are
+        # gathered (card_gather_rows) into a staging block the batch's own
+        # lm_head linear reads.
+        from .llama import EPI_STORE_F32, EPI_TOPK, TOPK_REC, _Linear
+
+        Hd = draft.shard_cfg.hidden
+        self.stage_rows = ((self.Md + 15) // 16) * 16
+        self.stage_xb = torch.zeros((self.stage_rows, Hd), dtype=torch.bfloat16, device=dev)
+        self.stage_ssq = torch.zeros((Hd // 16, self.stage_rows), dtype=torch.float32, device=dev)
+        W = self.rt_d.lm_head
+        if draft.fused_topk and k <= 4:
+            n_tiles = W.shape[0] if W.dim() == 4 else W.shape[0] // 128
+            work = torch.zeros(self.Md * n_tiles * TOPK_REC, dtype=torch.float32, device=dev)
+            self.head = _Linear(W, self.stage_xb, self.Md, EPI_TOPK, work, 0)
+            self.head.work, self.head.n_tiles = work, n_tiles
+        else:
+            self.head = None
+            self.lm_logits = _Linear(W, self.stage_xb, self.Md, EPI_STORE_F32, self.rt_d.logits,
+                                     draft.vocab.size)
+        lin = self.head if self.head is not None else self.lm_logits
+        lin.fuse_norm(self.stage_ssq, Hd // 16, self.stage_rows, draft.shard_cfg.rms_eps, Hd, None)
         # draft KV compaction scratch, one per request (compactions run in parallel)
         nL = draft.shard_cfg.n_layers
         row_bytes = self.rt_d.kv_row_elems() * self.rt_d.kv_esize()
@@ -265,17 +287,23 @@ class BatchRun:
         self._fan_out(rows)
         bias = self._bias_args(self.draft_model, self.tail_d)
         n_out = self.rows_d.n_out
+        rt = self.rt_d
+        rt.forward(self.rows_d, self.Md, batch=self.bp_d, head=False)
+        raise_for_status(L_.card_gather_rows(ptr(self.rows_d.out_rows), ptr(n_out), self.Md,
+                                             self.draft_model.shard_cfg.hidden, ptr(rt.xb), ptr(rt.ssq), rt.mpad,
+                                             ptr(self.stage_xb), ptr(self.stage_ssq), self.stage_rows, stream_ptr()),
+                         "gather_rows")
         if self.head is not None:
             head = self.head
             raise_for_status(L_.card_linear_fuse_kgram(head.h, *bias), "fuse_kgram")
             raise_for_status(L_.card_linear_fuse_topk(head.h, self.draft_model.vocab.size, 1.0 / self.t_score),
                              "fuse_topk")
-            self.rt_d.forward(self.rows_d, self.Md, topk=True, batch=self.bp_d)
+            head.run(n_out)
             raise_for_status(L_.card_lmhead_topk_merge(ptr(head.work), ptr(n_out), self.Md, head.n_tiles, k,
                                                        self.draft_model.vocab.size, ptr(self.tok), ptr(self.logp),
                                                        ptr(self.cnt), stream_ptr()), "lmhead_topk_merge")
         else:
-            self.rt_d.forward(self.rows_d, self.Md, batch=self.bp_d)
+            self.lm_logits.run(n_out)
             raise_for_status(L_.card_topk_logits(ptr(self.rt_d.logits), ptr(n_out), self.Md,
                                                  self.draft_model.vocab.size, k, 1.0 / self.t_score, ptr(self.tok),
                                                  ptr(self.logp), ptr(self.cnt), ptr(self.lm_work_d), *bias,

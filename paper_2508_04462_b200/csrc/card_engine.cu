@@ -69,7 +69,9 @@ __device__ void pad_rows(CardRows R, const RowSlot& B, int m0, int o0, int tid, 
         R.plen[m] = 0;
         R.n_extra[m] = 0;
     }
-    for (int o = o0 + tid; o < B.out_cap; o += nt) R.out_rows[o] = B.row_base + B.rows_cap - 1;
+    // padded outputs read the region's own rows in order (a target region's
+    // outputs are then the identity map of its rows)
+    for (int o = o0 + tid; o < B.out_cap; o += nt) R.out_rows[o] = B.row_base + (o < B.rows_cap ? o : B.rows_cap - 1);
 }
 
 __global__ void draft_rows_kernel(card_engine_state* E, const card_cache_state* S, const int32_t* __restrict__ ntoken,
@@ -91,7 +93,9 @@ __global__ void draft_rows_kernel(card_engine_state* E, const card_cache_state* 
             *R.M = 0;
             *R.n_out = 0;
         }
-        if (spent && tid == 0) E->stop = 1;
+        // a spent budget stops this cycle's expansions; a finished request's
+        // too (its padded outputs must not reach card_cache_expand_topk)
+        if ((spent || (batch && E->done)) && tid == 0) E->stop = 1;
         return;
     }
     if (batch && tid == 0) E->spare[0] -= 1;

@@ -102,6 +102,23 @@ __global__ void resid_add_kernel(const int32_t* dM, int H, float* __restrict__ x
     }
 }
 
+// Output rows of a batched forward -> one contiguous block for the lm_head
+// (its activation tile reads rows [0, n_out) contiguously): row out_rows[o]
+// of the bf16 residual and its per-16-column sums of squares -> row o.
+__global__ void gather_rows_kernel(const int32_t* __restrict__ out_rows, const int32_t* n_out, int H,
+                                   const __nv_bfloat16* __restrict__ xb, const float* __restrict__ ssq, int ssq_ld,
+                                   __nv_bfloat16* __restrict__ xb_out, float* __restrict__ ssq_out, int ssq_out_ld) {
+    pdl_wait();
+    pdl_trigger();
+    const int o = blockIdx.x;
+    if (o >= *n_out) return;
+    const int r = out_rows[o];
+    const uint4* src = reinterpret_cast<const uint4*>(xb + (int64_t)r * H);
+    uint4* dst = reinterpret_cast<uint4*>(xb_out + (int64_t)o * H);
+    for (int c = threadIdx.x; c < H / 8; c += blockDim.x) dst[c] = src[c];
+    for (int g = threadIdx.x; g < H / 16; g += blockDim.x) ssq_out[(int64_t)g * ssq_out_ld + o] = ssq[(int64_t)g * ssq_ld + r];
+}
+
 // ---------------------------------------------------------------- rmsnorm
 template <typename Y>
 __global__ void rmsnorm_kernel(const float* __restrict__ x, const float* __restrict__ w, int H, float eps,
@@ -974,6 +991,15 @@ int card_resid_add(const int32_t* dM, int m_max, int H, float* x, const float* p
     if (!dM || !x || !part || !xb || !ssq || H % 16 != 0 || m_max <= 0) return CARD_E_INPUT;
     CARD_PDL(resid_add_kernel, dim3(m_max), dim3(128), 0, (cudaStream_t)stream, dM, H, x, part, (__nv_bfloat16*)xb,
              ssq, ssq_ld);
+    CARD_LAUNCH_CHECK();
+    return CARD_OK;
+}
+
+int card_gather_rows(const int32_t* out_rows, const int32_t* n_out, int m_max, int H, const void* xb, const float* ssq,
+                     int ssq_ld, void* xb_out, float* ssq_out, int ssq_out_ld, void* stream) {
+    if (!out_rows || !n_out || !xb || !ssq || !xb_out || !ssq_out || H % 16 != 0 || m_max <= 0) return CARD_E_INPUT;
+    CARD_PDL(gather_rows_kernel, dim3(m_max), dim3(128), 0, (cudaStream_t)stream, out_rows, n_out, H,
+             (const __nv_bfloat16*)xb, ssq, ssq_ld, (__nv_bfloat16*)xb_out, ssq_out, ssq_out_ld);
     CARD_LAUNCH_CHECK();
     return CARD_OK;
 }

@@ -577,7 +577,7 @@ class DeviceLlama:
         return PageTable(self.page_pool, self.prefix_slots // PAGE, device or self.dev)
 
     def forward(self, rows: "RowBlock", m_max: int, topk: bool = False, pages: "PageTable | None" = None,
-                batch: "BatchPages | None" = None):
+                batch: "BatchPages | None" = None, head: bool = True):
         """Run the forward over the device rows; logits for the output rows
         land in self.logits[:n_out] (topk=True: the lm_head_topk records
         instead, see lm_topk_head).  pages: the request's page table (the
@@ -588,7 +588,7 @@ class DeviceLlama:
         s = stream_ptr()
         plan = self.plans[m_max]
         if self.fused:
-            return self._forward_fused(rows, plan, topk, pages, batch)
+            return self._forward_fused(rows, plan, topk, pages, batch, head)
         if topk:
             raise ConfigError("the fused top-k lm_head needs the bf16 path")
         if batch is not None:
@@ -659,7 +659,9 @@ class DeviceLlama:
             self.prefix_slots, ptr(self.o), stream_ptr()), "attention")
 
     def _forward_fused(self, rows: "RowBlock", plan: dict, topk: bool = False, pages: "PageTable | None" = None,
-                       batch: "BatchPages | None" = None):
+                       batch: "BatchPages | None" = None, head: bool = True):
+        """head=False stops before the lm_head (its input rows: xb / ssq at
+        the rows' out_rows, e.g. for card_gather_rows)."""
         c = self.cfg
         L_ = lib()
         s = stream_ptr()
@@ -680,7 +682,8 @@ class DeviceLlama:
                 self._attend(li, rows, mm, pages, batch, pf.qsw if tree_q else None, pf.qsw_tiles if tree_q else 0)
                 # o, gate/up, down of layer li, then the qkv of layer li + 1
                 pf.run(dM, n5 * li + 2, min(n5 * (li + 1) + 1, n5 * c.n_layers))
-            plan["lm_head_topk" if topk else "lm_head"].run(rows.n_out)
+            if head:
+                plan["lm_head_topk" if topk else "lm_head"].run(rows.n_out)
             return
         for li, P in enumerate(plan["layers"]):
             P["qkv"].run(dM)
@@ -692,6 +695,8 @@ class DeviceLlama:
             P["d"].run(dM)
             if self.tp is not None:
                 self._tp_reduce(dM, mm)
+        if not head:
+            return
         plan["lm_head_topk" if topk else "lm_head"].run(rows.n_out)
         if self.tp is not None:
             if topk:

@@ -329,3 +329,62 @@ def test_attention_tree_preswizzled_q_equals_paged(card, hd, M):
         assert torch.equal(o_sw.view(torch.int16), o_ref.view(torch.int16))
     else:                        # paged ran the mma.sync kernel: same values within bf16 rounding
         assert ((o_sw.float() - o_ref.float()).norm() / o_ref.float().norm()) < 1e-2
+
+
+@pytest.mark.parametrize("hd,nh,nkv,seg_rows,B,dead,P", [(64, 8, 4, 5, 6, (), 700), (128, 32, 8, 8, 9, (), 700),
+                                                          (64, 32, 8, 7, 16, (), 700), (64, 4, 2, 18, 4, (), 700),
+                                                          (64, 8, 4, 5, 2, (0,), 700), (64, 8, 4, 5, 4, (0, 1), 700),
+                                                          (128, 32, 8, 8, 4, (0, 2), 700), (64, 8, 4, 5, 2, (0,), 80)])
+def test_attention_batch_matches_torch(card, hd, nh, nkv, seg_rows, B, dead, P):
+    """card_attention_batch: rows [i*seg_rows, (i+1)*seg_rows) of request i
+    read its prefix through its own page table (tables [B, stride]); tiles
+    span several requests; padding rows (plen 0) and tree extras; fp32
+    torch reference per row over the request's logical sequence."""
+    from paper_2508_04462_b200._device import ptr, stream_ptr
+    from paper_2508_04462_b200._lib import lib
+    from paper_2508_04462_b200.llama import RowBlock
+
+    XM = 8
+    M = B * seg_rows
+    g = torch.Generator(device="cuda").manual_seed(hd + 3 * B + seg_rows)
+    rng = np.random.default_rng(hd * 17 + B)
+    stride = (P + 63) // 64
+    n_pages = B * stride + 3
+    perm = rng.permutation(n_pages)
+    tables = torch.tensor(perm[:B * stride].reshape(B, stride), dtype=torch.int32, device="cuda")
+    slots = n_pages * 64 + 512
+    kc = torch.randn(slots, nkv, hd, device="cuda", generator=g).to(torch.bfloat16)
+    vc = torch.randn(slots, nkv, hd, device="cuda", generator=g).to(torch.bfloat16)
+    q = torch.randn(M, nh, hd, device="cuda", generator=g) / hd ** 0.5
+    plen, extras = [], []
+    for m in range(M):
+        if rng.random() < 0.2 or m // seg_rows in dead:   # padding row (dead: a finished request's region)
+            plen.append(0)
+            extras.append([])
+        else:
+            plen.append(int(rng.integers(1, P + 1)))
+            extras.append(sorted(set(int(x) for x in rng.integers(n_pages * 64, slots, int(rng.integers(0, XM))))))
+    rows = RowBlock(M, XM, "cuda")
+    _fill(rows, [0] * M, [0] * M, [0] * M, plen, extras, [])
+    o = torch.full((M, nh * hd), float("nan"), device="cuda", dtype=torch.bfloat16)
+    rc = lib().card_attention_batch(ptr(q), None, 0, ptr(rows.M), M, ptr(rows.plen), ptr(rows.n_extra),
+                                    ptr(rows.extra), XM, ptr(kc), ptr(vc), ptr(tables), stride, seg_rows, nh, nkv,
+                                    hd, P, ptr(o), stream_ptr())
+    assert rc == 0
+    torch.cuda.synchronize()
+    G = nh // nkv
+    Kf, Vf = kc.float(), vc.float()
+    tab = tables.long().cpu()
+    for r in range(M):
+        if plen[r] == 0 and not extras[r]:
+            assert torch.all(o[r].float() == 0), r
+            continue
+        i = r // seg_rows
+        logical = (tab[i][:, None] * 64 + torch.arange(64)[None]).reshape(-1)
+        vis = logical[:plen[r]].tolist() + extras[r]
+        k = Kf[vis].repeat_interleave(G, dim=1)
+        v = Vf[vis].repeat_interleave(G, dim=1)
+        s = torch.einsum("hd,thd->ht", q[r], k)
+        want = torch.einsum("ht,thd->hd", torch.softmax(s, -1), v).reshape(-1)
+        err = (o[r].float() - want).norm() / want.norm()
+        assert err < 1e-2, (r, i, float(err))
