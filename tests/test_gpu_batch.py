@@ -181,3 +181,24 @@ def test_gather_rows_packs_output_rows():
     idx = rows.long()
     assert torch.equal(out[:n], xb[idx]) and torch.equal(sout[:, :n], ssq[:, idx])
     assert torch.all(out[n:] == 0)
+
+
+def test_batched_drafts_compute_their_own_rows():
+    """The batched draft forward must compute each request's own rows.  With
+    the target as its own draft and no agreement bias the acceptance depends
+    entirely on the draft's logits: a request fed another row's hidden
+    state would fall to ~1 accepted token per verify.  Each request's mean
+    acceptance in a batch of 4 matches the single-request engine's."""
+    import paper_2508_04462_b200 as card
+    from paper_2508_04462_b200.llama import PRESETS, init_weights
+
+    ct = PRESETS["small-target"]
+    t = card.LlamaModel(ct, dtype="bf16", weights=init_weights(ct, 2), spec=card.ModelSpec(8.0, 7.0))
+    cfg = card.EngineConfig(K=8, k=3, ratio=4, max_new_tokens=96)
+    prompts = _prompts(4, t.vocab.size, [40, 56])
+    batch, _ = card.run_speculative_batched(t, t, prompts, cfg)
+    for p, r in zip(prompts, batch):
+        single = card.run_speculative(t, t, p, cfg)   # the single-request engine, per-GEMM draft rows
+        a, b = r.metrics.mean_acceptance_length, single.metrics.mean_acceptance_length
+        assert b > 1.5 and abs(a - b) <= 0.15 * b, (a, b)
+        _lossless_upto_ties(card, t, p, r.output, cfg)
