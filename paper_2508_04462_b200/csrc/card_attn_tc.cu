@@ -28,6 +28,7 @@
 // The S ranks' partials (m, l, O) are pushed into the owner rank's shared
 // memory (st.shared::cluster) and merged in rank order (deterministic); the
 // owner writes o (bf16) for the o-projection GEMM.
+#include <cuda.h>
 #include <cuda_bf16.h>
 #include <math.h>
 
@@ -130,6 +131,14 @@ __device__ __forceinline__ uint32_t sw_off(int r, int c) {
 __device__ __forceinline__ void cp16(uint32_t dst, const void* src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
 }
+// 3D TMA box (KV cache [slots, nkv, hd]: {64 dims, 1 head, 64 slots}) -> SW128 rows
+__device__ __forceinline__ void tma3d(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0, int c1, int c2) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(
+            dst),
+        "l"(map), "r"(bar), "r"(c0), "r"(c1), "r"(c2)
+        : "memory");
+}
 __device__ __forceinline__ void st16_zero(uint32_t dst) {
     asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(dst), "r"(0u) : "memory");
 }
@@ -208,8 +217,12 @@ struct Smem {
     static constexpr int kQ = HD / 64 * kSub;          // Q tile [128 x HD]
     static constexpr int kKV = HD / 64 * kSub;         // one K (or V) round [128 keys x HD]
     static constexpr int kP = 2 * kSub;                // P [128 x 128 keys]
+    // hd 64: P and O double-buffered, so the O accumulation of a round is
+    // deferred behind the next round's softmax (TMEM: S 128 + 2 x O 64)
+    static constexpr bool kDefer = HD == 64;
+    static constexpr int kPB = kDefer ? 2 : 1;
     static constexpr int kRecvLd = HD + 4;             // merge record [m, l, pad, pad, O[HD]]
-    static constexpr int oQ = 0, oK = kQ, oV = oK + kNB * kKV, oP = oV + kNB * kKV, oR = oP + kP;
+    static constexpr int oQ = 0, oK = kQ, oV = oK + kNB * kKV, oP = oV + kNB * kKV, oR = oP + kPB * kP;
     static constexpr int oMeta = oR + kQT * kRecvLd * 4;   // recv: one record per query-head row
     // meta: ext_slot[kMaxX], rplen/rnx/rxo[kMaxRows], xch[2][128], bars, tmem slot,
     // segment table seg_vb[kMaxSeg + 1] / seg_kp[kMaxSeg]
@@ -220,7 +233,9 @@ struct Smem {
 }  // namespace
 
 template <int HD>
-__global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const TcAttnArgs a) {
+__global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_constant__ TcAttnArgs a,
+                                                              const __grid_constant__ CUtensorMap tmK,
+                                                              const __grid_constant__ CUtensorMap tmV) {
     using L = Smem<HD>;
     constexpr int HH = HD / 2;   // O columns per softmax half
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -242,8 +257,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const TcAttnArgs a
     uint64_t* s_full = bars + 4;     // MMA commit -> softmax
     uint64_t* s_empty = bars + 6;    // softmax -> MMA
     uint64_t* p_full = bars + 8;     // softmax -> MMA
-    uint64_t* o_full = bars + 9;     // MMA commit -> softmax
-    uint64_t* o_empty = bars + 10;   // softmax -> MMA
+    // MMA commit -> softmax / softmax -> MMA, per O buffer (bars 9, 10 and 14, 15)
+    auto o_full_b = [&](int ob) { return bars + (ob ? 14 : 9); };
+    auto o_empty_b = [&](int ob) { return bars + (ob ? 15 : 10); };
     uint64_t* recv_bar = bars + 11;  // every rank's partials of my rows landed (st.async complete_tx)
     uint32_t* tmem_slot = (uint32_t*)(bars + 12);
     uint64_t* q_full = bars + 13;    // pre-swizzled Q tile landed (bulk copy)
@@ -278,8 +294,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const TcAttnArgs a
         bar_init(s_full, 1);
         bar_init(s_empty, kSoftWarps * 32);
         bar_init(p_full, kSoftWarps * 32);
-        bar_init(o_full, 1);
-        bar_init(o_empty, kSoftWarps * 32);
+        for (int i = 0; i < 2; ++i) {
+            bar_init(o_full_b(i), 1);
+            bar_init(o_empty_b(i), kSoftWarps * 32);
+        }
         bar_init(recv_bar, 1);
         bar_init(q_full, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -352,22 +370,45 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const TcAttnArgs a
     const int nr = rank < n_tot ? (n_tot - rank + S - 1) / S : 0;
 
     __syncthreads();   // ext_slot / s_old complete
-    if (warp >= kLoadWarp0) {
-        // old prefix keys of the first two rounds stream in under the previous kernel's tail
-        const int lt = threadIdx.x - kLoadWarp0 * 32;
+    // Prefix rounds load by TMA: the round's two 64-key pages of K and V of
+    // this kv head, one box per (page, 64-dim sub-block), straight into the
+    // SW128 layout the UMMA descriptors read.  A page past the segment's
+    // keys reloads its last page (finite values the softmax masks).  The
+    // issuing loader thread's arrival is the expect_tx.
+    auto tma_round = [&](int li) {
+        const int b = li % L::kNB;
+        const int j0 = (rank + li * S) * kKB;
+        int sg = 0;
+        while (j0 >= seg_vb[sg + 1]) ++sg;
+        const int pp0 = j0 - seg_vb[sg];
+        const int last_pg = seg_kp[sg] > 0 ? (seg_kp[sg] - 1) >> 6 : 0;
+        const int32_t* pt = a.page_table ? a.page_table + (int64_t)(s_lo + sg) * a.pt_stride : nullptr;
+        const uint32_t bar = su32(&kv_full[b]);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                     "r"((uint32_t)(2 * 2 * (HD / 64) * 8192))
+                     : "memory");
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+            const int pg = min((pp0 >> 6) + half, last_pg);
+            const int slot0 = (pt ? pt[pg] : pg) * 64;
+#pragma unroll
+            for (int sb = 0; sb < HD / 64; ++sb) {
+                const uint32_t off = (uint32_t)(sb * kSub + half * 8192);
+                tma3d(su32(sK + b * L::kKV) + off, &tmK, bar, sb * 64, g, slot0);
+                tma3d(su32(sV + b * L::kKV) + off, &tmV, bar, sb * 64, g, slot0);
+            }
+        }
+    };
+    int early = 0;   // prefix rounds whose pages all predate this forward, issued before the PDL wait
+    if (warp >= kLoadWarp0 && threadIdx.x == kLoadWarp0 * 32) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tmK) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tmV) : "memory");
         const int old = segm ? 0 : min(*s_old, Kp);
         for (int li = 0; li < min(nr, L::kNB); ++li) {
             const int j0 = (rank + li * S) * kKB;
-            const int k_hi = min(kKB, old - j0);
-            const uint32_t kb = su32(sK + li * L::kKV), vb = su32(sV + li * L::kKV);
-            for (int idx = lt; idx < k_hi * (HD / 8); idx += kLoadWarps * 32) {
-                const int kk = idx / (HD / 8), c = idx % (HD / 8);
-                const int j = j0 + kk;
-                const int slot = a.page_table ? a.page_table[j >> 6] * 64 + (j & 63) : j;
-                const int64_t e = ((int64_t)slot * a.nkv + g) * HD + c * 8;
-                const uint32_t off = (uint32_t)((c >> 3) * kSub) + sw_off(kk, c & 7);
-                cp16(kb + off, a.kc + e);
-                cp16(vb + off, a.vc + e);
+            if (j0 < XB && j0 + kKB <= old) {
+                tma_round(li);
+                early |= 1 << li;
             }
         }
     }
@@ -416,7 +457,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const TcAttnArgs a
     tc_stamp(3);
     const uint32_t tmem = *tmem_slot;
     const uint32_t tS = tmem;          // S of the current round (128 columns)
-    const uint32_t tO = tmem + 128;    // O of the current round (hd columns)
+    const uint32_t tO = tmem + 128;    // O of the current round (hd columns; hd 64: two buffers)
 
     // softmax state: warp w owns TMEM lanes 32 (w % 4) .. and S columns / O
     // columns of half h = w / 4; (m, l) of a row are shared by its two halves
@@ -461,20 +502,22 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const TcAttnArgs a
                 }
             }
         };
-        // rounds 0 and 1: the old prefix keys were issued before the PDL wait
-        const int old = segm ? 0 : min(*s_old, Kp);
         for (int li = 0; li < nr; ++li) {
             const int b = li % L::kNB;
             const int j0 = (rank + li * S) * kKB;
-            if (li >= L::kNB) {
-                bar_wait(&kv_empty[b], ((li / L::kNB) - 1) & 1);
+            if (li >= L::kNB) bar_wait(&kv_empty[b], ((li / L::kNB) - 1) & 1);
+            if (j0 < XB) {   // prefix round: TMA (thread 0's arrival is its expect_tx)
+                if (lt == 0) {
+                    if (!((early >> li) & 1)) tma_round(li);
+                } else {
+                    bar_arrive(&kv_full[b]);
+                }
+            } else {         // tree extras: gathered slot by slot
                 gather(li, j0, j0 + kKB);
-            } else {
-                gather(li, max(j0, old), j0 + kKB);
+                asm volatile("cp.async.wait_all;" ::: "memory");
+                fence_async_smem();
+                bar_arrive(&kv_full[b]);
             }
-            asm volatile("cp.async.wait_all;" ::: "memory");
-            fence_async_smem();
-            bar_arrive(&kv_full[b]);
         }
     } else if (warp == kMmaWarp) {
         // ------------------------------------------------ MMA issuer
@@ -498,15 +541,22 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const TcAttnArgs a
                 }
                 tc_commit(s_full);
                 bar_wait(p_full, li & 1);
-                if (li >= 1) bar_wait(o_empty, (li - 1) & 1);
+                const int ob = L::kDefer ? (li & 1) : 0;
+                if (L::kDefer) {
+                    if (li >= 2) bar_wait(o_empty_b(ob), ((li - 2) >> 1) & 1);   // O of round li-2 accumulated
+                } else if (li >= 1) {
+                    bar_wait(o_empty_b(0), (li - 1) & 1);
+                }
                 tc_after();
                 const uint32_t v_s = su32(sV + b * L::kKV);
+                const uint32_t p_b = p_s + (uint32_t)(ob * L::kP);
+                const uint32_t t_o = tO + (uint32_t)(ob * HD);
 #pragma unroll
                 for (int k = 0; k < kKB / 16; ++k) {
-                    const uint32_t pa = p_s + (uint32_t)((k >> 2) * kSub + (k & 3) * 32);
-                    tc_mma(tO, desc_kmajor(pa), desc_mnmajor(v_s + (uint32_t)(k * 2048)), idO, k > 0 ? 1u : 0u);
+                    const uint32_t pa = p_b + (uint32_t)((k >> 2) * kSub + (k & 3) * 32);
+                    tc_mma(t_o, desc_kmajor(pa), desc_mnmajor(v_s + (uint32_t)(k * 2048)), idO, k > 0 ? 1u : 0u);
                 }
-                tc_commit(o_full);
+                tc_commit(o_full_b(ob));
                 tc_commit(&kv_empty[b]);
             }
         }
@@ -522,6 +572,22 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const TcAttnArgs a
         const int e0 = live ? XB + rxo[ri] : 0, e1 = live ? XB + rxo[ri] + rnx[ri] : 0;
         const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
         const int pair_bar = 1 + (warp & 3);   // named barrier of warps w and w + 4
+        float alpha_prev = 0.f;
+        // O_acc = O_acc * alpha + O of round r (TMEM buffer r & 1 when double-buffered)
+        auto accumulate_o = [&](int r, float alpha) {
+            const int ob = L::kDefer ? (r & 1) : 0;
+            bar_wait(o_full_b(ob), L::kDefer ? ((r >> 1) & 1) : (r & 1));
+            tc_after();
+#pragma unroll
+            for (int c = 0; c < HH / 16; ++c) {
+                float v[16];
+                tmem_ld16(tO + (uint32_t)(ob * HD) + lane_off + (uint32_t)(h * HH + c * 16), v);
+#pragma unroll
+                for (int u = 0; u < 16; ++u) oacc[c * 16 + u] = fmaf(oacc[c * 16 + u], alpha, v[u]);
+            }
+            tc_before();
+            bar_arrive(o_empty_b(ob));
+        };
         for (int li = 0; li < nr; ++li) {
             const int b = li & 1;
             const int j0 = (rank + li * S) * kKB;
@@ -570,7 +636,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const TcAttnArgs a
                         sum += __bfloat162float(pr.x) + __bfloat162float(pr.y);   // l sums what P.V uses
                     }
                 }
-                const uint32_t base = su32(sP + (c >> 2) * kSub);
+                const uint32_t base = su32(sP + (L::kDefer ? (li & 1) * L::kP : 0) + (c >> 2) * kSub);
                 const int ch = (c & 3) * 2;
                 asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(base + sw_off(t, ch)), "r"(w[0]),
                              "r"(w[1]), "r"(w[2]), "r"(w[3])
@@ -586,18 +652,16 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const TcAttnArgs a
             const float alpha = (m_run == -INFINITY) ? 0.f : exp2f((m_run - m_new) * kLog2e);
             l_run = l_run * alpha + sum;   // this half's share of l
             m_run = m_new;
-            bar_wait(o_full, li & 1);
-            tc_after();
-#pragma unroll
-            for (int c = 0; c < HH / 16; ++c) {
-                float v[16];
-                tmem_ld16(tO + lane_off + (uint32_t)(h * HH + c * 16), v);
-#pragma unroll
-                for (int u = 0; u < 16; ++u) oacc[c * 16 + u] = fmaf(oacc[c * 16 + u], alpha, v[u]);
+            if (L::kDefer) {
+                // O of the previous round, now that this round's P is out
+                // (same accumulation order: O = O * alpha_r + O_r, r ascending)
+                if (li >= 1) accumulate_o(li - 1, alpha_prev);
+                alpha_prev = alpha;
+            } else {
+                accumulate_o(li, alpha);
             }
-            tc_before();
-            bar_arrive(o_empty);
         }
+        if (L::kDefer && nr >= 1) accumulate_o(nr - 1, alpha_prev);
         // the row's l = both halves' shares
         named_bar_sync(pair_bar, 64);
         xch[h * kQT + t] = l_run;
@@ -697,6 +761,33 @@ static int attn_tc_ranks(int tiles) {
     return tiles <= 18 ? 8 : tiles <= 37 ? 4 : tiles <= 74 ? 2 : 1;   // portable clusters (<= 8)
 }
 
+typedef CUresult (*PFN_encodeTiled_attn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                          const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                          CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+// KV cache [slots, nkv, hd] bf16 as a 3D tensor map, boxes of {64 dims, 1 head,
+// 64 slots} with the 128-byte swizzle.  The slot extent is nominal (1 << 24):
+// only slots of the caller's pages are ever addressed.
+static int kv_map(CUtensorMap* m, const void* base, int nkv, int hd) {
+    static PFN_encodeTiled_attn enc = nullptr;
+    if (!enc) {
+        cudaDriverEntryPointQueryResult q;
+        void* p = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return CARD_E_CUDA;
+        enc = (PFN_encodeTiled_attn)p;
+    }
+    cuuint64_t dims[3] = {(cuuint64_t)hd, (cuuint64_t)nkv, (cuuint64_t)1 << 24};
+    cuuint64_t strides[2] = {(cuuint64_t)hd * 2, (cuuint64_t)nkv * hd * 2};
+    cuuint32_t box[3] = {64, 1, 64};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? CARD_OK : CARD_E_CUDA;
+}
+
 template <int HD>
 static cudaError_t launch_tc(const TcAttnArgs& a, dim3 grid, int S, cudaStream_t s) {
     static bool attr = false;
@@ -719,7 +810,10 @@ static cudaError_t launch_tc(const TcAttnArgs& a, dim3 grid, int S, cudaStream_t
     at[1].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 2;
-    return cudaLaunchKernelEx(&cfg, attn_tc_kernel<HD>, a);
+    CUtensorMap tmK, tmV;
+    if (kv_map(&tmK, a.kc, a.nkv, HD) != CARD_OK || kv_map(&tmV, a.vc, a.nkv, HD) != CARD_OK)
+        return cudaErrorInvalidValue;
+    return cudaLaunchKernelEx(&cfg, attn_tc_kernel<HD>, a, tmK, tmV);
 }
 
 int launch_attn_tc(const float* q, const int32_t* dM, int m_max, const int32_t* plen, const int32_t* n_extra,
