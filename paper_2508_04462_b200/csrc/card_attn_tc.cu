@@ -43,8 +43,8 @@ constexpr int kKB = 128;        // keys per round = S MMA N = PV MMA K
 constexpr int kMaxX = 1024;     // gathered extra keys per tile
 constexpr int kMaxRows = 136;   // token rows per tile (GQA group >= 1)
 constexpr int kMaxSeg = 64;     // request segments per tile (batched forwards)
-constexpr int kSoftWarps = 8, kMmaWarp = 8, kLoadWarp0 = 9, kLoadWarps = 4;
-constexpr int kThreads = (kLoadWarp0 + kLoadWarps) * 32;   // 416
+constexpr int kSoftWarps = 8, kMmaWarp = 8, kLoadWarp0 = 9, kLoadWarps = 3;   // 12 warps: up to 168 registers
+constexpr int kThreads = (kLoadWarp0 + kLoadWarps) * 32;   // 384
 constexpr int kSub = 128 * 64 * 2;   // one [128 rows x 64 bf16] SW128 sub-block (16 KB)
 constexpr float kLog2e = 1.4426950408889634f;
 
@@ -101,6 +101,14 @@ __device__ __forceinline__ void tc_mma(uint32_t d, uint64_t a, uint64_t b, uint3
         "l"(a), "l"(b), "r"(idesc), "r"(acc)
         : "memory");
 }
+__device__ __forceinline__ void tmem_ld16_issue(uint32_t taddr, uint32_t* r) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
     uint32_t r[16];
     asm volatile(
@@ -578,13 +586,15 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
             const int ob = L::kDefer ? (r & 1) : 0;
             bar_wait(o_full_b(ob), L::kDefer ? ((r >> 1) & 1) : (r & 1));
             tc_after();
+            uint32_t orr[HH / 16][16];
 #pragma unroll
-            for (int c = 0; c < HH / 16; ++c) {
-                float v[16];
-                tmem_ld16(tO + (uint32_t)(ob * HD) + lane_off + (uint32_t)(h * HH + c * 16), v);
+            for (int c = 0; c < HH / 16; ++c)
+                tmem_ld16_issue(tO + (uint32_t)(ob * HD) + lane_off + (uint32_t)(h * HH + c * 16), orr[c]);
+            tmem_wait_ld();
 #pragma unroll
-                for (int u = 0; u < 16; ++u) oacc[c * 16 + u] = fmaf(oacc[c * 16 + u], alpha, v[u]);
-            }
+            for (int c = 0; c < HH / 16; ++c)
+#pragma unroll
+                for (int u = 0; u < 16; ++u) oacc[c * 16 + u] = fmaf(oacc[c * 16 + u], alpha, __uint_as_float(orr[c][u]));
             tc_before();
             bar_arrive(o_empty_b(ob));
         };
@@ -592,6 +602,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
             const int b = li & 1;
             const int j0 = (rank + li * S) * kKB;
             bar_wait(s_full, li & 1);
+            if (li == 0) tc_stamp(5);   // (thread 0: the first S is in TMEM)
             tc_after();
             // 16-column validity masks of my half (c = 4h .. 4h+3)
             uint32_t msk[4];
@@ -606,14 +617,24 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
                 if (x1 > x0) m |= ((1u << x1) - 1u) & ~((1u << x0) - 1u);
                 msk[q] = m;
             }
+            // my half of S in one batch of TMEM loads (one wait), kept in
+            // registers for both passes; S's TMEM is free for the next round
+            uint32_t sr[4][16];
+            bool need[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                need[q] = __any_sync(0xffffffffu, msk[q] != 0u);
+                if (need[q]) tmem_ld16_issue(tS + lane_off + (uint32_t)((4 * h + q) * 16), sr[q]);
+            }
+            tmem_wait_ld();
+            tc_before();
+            bar_arrive(s_empty);
             float mx = -INFINITY;
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-                if (!__any_sync(0xffffffffu, msk[q] != 0u)) continue;
-                float v[16];
-                tmem_ld16(tS + lane_off + (uint32_t)((4 * h + q) * 16), v);
+                if (!need[q]) continue;
 #pragma unroll
-                for (int u = 0; u < 16; ++u) mx = ((msk[q] >> u) & 1u) ? fmaxf(mx, v[u]) : mx;
+                for (int u = 0; u < 16; ++u) mx = ((msk[q] >> u) & 1u) ? fmaxf(mx, __uint_as_float(sr[q][u])) : mx;
             }
             xch[h * kQT + t] = mx;
             named_bar_sync(pair_bar, 64);
@@ -624,13 +645,13 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
             for (int q = 0; q < 4; ++q) {
                 const int c = 4 * h + q;
                 uint32_t w[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
-                if (__any_sync(0xffffffffu, msk[q] != 0u)) {
-                    float v[16];
-                    tmem_ld16(tS + lane_off + (uint32_t)(c * 16), v);
+                if (need[q]) {
+                    const uint32_t* v = sr[q];
 #pragma unroll
                     for (int u = 0; u < 16; u += 2) {
-                        const float p0 = ((msk[q] >> u) & 1u) ? exp2f(fmaf(v[u], kLog2e, -mb)) : 0.f;
-                        const float p1 = ((msk[q] >> (u + 1)) & 1u) ? exp2f(fmaf(v[u + 1], kLog2e, -mb)) : 0.f;
+                        const float p0 = ((msk[q] >> u) & 1u) ? exp2f(fmaf(__uint_as_float(v[u]), kLog2e, -mb)) : 0.f;
+                        const float p1 =
+                            ((msk[q] >> (u + 1)) & 1u) ? exp2f(fmaf(__uint_as_float(v[u + 1]), kLog2e, -mb)) : 0.f;
                         w[u >> 1] = pack_bf2(p0, p1);
                         const __nv_bfloat162 pr = *reinterpret_cast<__nv_bfloat162*>(&w[u >> 1]);
                         sum += __bfloat162float(pr.x) + __bfloat162float(pr.y);   // l sums what P.V uses
@@ -647,7 +668,6 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
             }
             fence_async_smem();
             tc_before();
-            bar_arrive(s_empty);
             bar_arrive(p_full);
             const float alpha = (m_run == -INFINITY) ? 0.f : exp2f((m_run - m_new) * kLog2e);
             l_run = l_run * alpha + sum;   // this half's share of l

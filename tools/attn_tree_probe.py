@@ -94,7 +94,7 @@ t = buf.view(-1, 8).cpu().numpy().astype(np.float64)
 t = t[t[:, 0] > 0]
 t0 = t[:, 0].min()
 print(f"{len(t)} CTAs")
-for k, nm in enumerate(["entry", "setup", "pdl", "q_ready", "loop_end", "-", "merged", "end"]):
+for k, nm in enumerate(["entry", "setup", "pdl", "q_ready", "loop_end", "first_S", "merged", "end"]):
     v = t[:, k][t[:, k] > 0] - t0
     if len(v):
         print(f"  {nm:9s} min {v.min() / 1e3:7.2f} med {np.median(v) / 1e3:7.2f} max {v.max() / 1e3:7.2f} us")
