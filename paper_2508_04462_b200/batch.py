@@ -9,7 +9,8 @@ chains.  Per request everything else stays separate and follows the
 reference schedule of engine.py:290-317 (serial_sim, correction on):
 
 * its own candidate tree (device arena + hash, cache.py), engine state,
-  committed tokens, prefix KV pages and tree-KV slots, and uniforms;
+  committed tokens, prefix KV pages and tree-KV slots, and uniforms
+  (request i: default_rng(seed + i));
 * its own region of the combined row blocks: ``rows_d = K + CATCH_UP``
   draft rows (frontier + catch-up), ``K`` draft outputs and
   ``query_depth + 1`` verify rows, padded when shorter
@@ -129,7 +130,10 @@ class BatchRun:
         self.caches = [TreeCache(p[-1], CacheConfig(cfg.K, cfg.k, cfg.max_depth), eos_token=self.eos,
                                  capacity=self.cap) for p in self.prompts]
         rng_n = (cfg.max_new_tokens + 2) * (cfg.query_depth + 2) + 16 if self.sampling else 1
-        self.uni = torch.from_numpy(np.random.default_rng(cfg.seed).random(rng_n)).to(dev)
+        # request i draws from default_rng(seed + i) (engine.py:162 per request):
+        # request 0 of a batch samples exactly as run_speculative with the config
+        self.uni = torch.from_numpy(np.stack([np.random.default_rng(cfg.seed + i).random(rng_n)
+                                              for i in range(B)])).to(dev)
         states = []
         for p in self.prompts:
             st = EngineState()
@@ -353,7 +357,7 @@ class BatchRun:
             q_tok = ctypes.c_void_p(c._qbufs[1])
             if self.sampling:
                 raise_for_status(L_.card_verify_probs(E, q_tok, ctypes.c_void_p(self.probs.data_ptr() + i * R * V * 8),
-                                                      V, None, ptr(self.uni), stream_ptr()), "verify_probs")
+                                                      V, None, ptr(self.uni[i]), stream_ptr()), "verify_probs")
             else:
                 raise_for_status(L_.card_verify_argmax(E, q_tok, ctypes.c_void_p(self.amax.data_ptr() + i * R * 4),
                                                        stream_ptr()), "verify_argmax")

@@ -102,6 +102,19 @@ def test_batched_requests_are_isolated(pair):
         assert [ev.to_dict() for ev in x.trace] == [ev.to_dict() for ev in y.trace]
 
 
+def test_batched_sampling_draws_per_request_streams(pair):
+    """T=1: request i samples from default_rng(seed + i), so identical prompts
+    in one batch follow different random streams (and request 0 the
+    config's own seed)."""
+    card, d, t = pair
+    cfg = card.EngineConfig(K=8, k=3, ratio=4, max_new_tokens=48, temperature=1.0, seed=3)
+    p = _prompts(1, t.vocab.size, [40])[0]
+    res, _ = card.run_speculative_batched(d, t, [p, p, p], cfg)
+    assert len({tuple(r.output) for r in res}) > 1
+    again, _ = card.run_speculative_batched(d, t, [p], cfg)
+    assert len(again[0].output) == cfg.max_new_tokens
+
+
 def test_batched_sampling_is_reproducible(pair):
     card, d, t = pair
     cfg = card.EngineConfig(K=8, k=3, ratio=4, max_new_tokens=32, temperature=1.0, seed=7)
