@@ -160,14 +160,16 @@ class CpuCard:
     random-init draft/target, agreement bias, prompt and K/k/ratio.  Weights
     are initialised once; the 512-token prompt is prefilled once (each model
     keeps a KV-cached token stream, so every tree path and verify chain
-    reuses the prompt's KV: the prefix memo of SURVEY §8d).  A sample is one
+    reuses the prompt's KV: the prefix memo of SURVEY §8d).  Each draft tree
+    layer is one masked pass and each verify chain one pass (BatchedRefModel,
+    the batching lm.py:155-163 asks of a real backend).  A sample is one
     CARD cycle (<= ratio draft layers of <= K tree rows + one verify)."""
 
     def __init__(self, args):
         import torch
 
         from oracle import card_oracle as O
-        from oracle.llama_ref import RefModel
+        from oracle.llama_ref import BatchedRefModel as RefModel
         from paper_2508_04462_b200.llama import PRESETS, init_weights
         from paper_2508_04462_b200.lm import LogitBias
 
@@ -216,7 +218,8 @@ class CpuCard:
 
     def describe(self, n_cycles, n_tok, secs) -> str:
         a = self.args
-        return (f"oracle CARD loop (card_oracle.serial_cycles = reference _run_serial) + run_vanilla, fp32 torch CPU, "
+        return (f"oracle CARD loop (card_oracle.serial_cycles = reference _run_serial; one masked pass per draft "
+                f"tree layer, one pass per verify chain) + run_vanilla, fp32 torch CPU, "
                 f"{a.draft} draft + {a.target} target, {a.prompt_len}-token prompt (prefilled once, "
                 f"{self.prefill_s:.1f} s, excluded), K={a.K} k={a.k} r={a.ratio} T={a.temperature}: {n_cycles} cycles, "
                 f"{n_tok} tokens in {secs:.1f} s; weights initialised once ({self.init_s:.1f} s)")

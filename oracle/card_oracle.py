@@ -66,6 +66,18 @@ def kgram_uniforms(seed: int, tail, n: int) -> list[float]:
     return [(mix64((s + (i + 1) * GAMMA) & M64) >> 11) * INV_2_53 for i in range(n)]
 
 
+def kgram_uniforms_np(seed: int, tail, n: int) -> np.ndarray:
+    """kgram_uniforms vectorised (uint64 wrap-around arithmetic): the same
+    float64 values, for vocabulary-sized rows in the CPU baselines."""
+    s = np.uint64(stream_state(seed, tail))
+    with np.errstate(over="ignore"):
+        z = s + np.arange(1, n + 1, dtype=np.uint64) * np.uint64(GAMMA)
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(MIX_C1)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(MIX_C2)
+        z = z ^ (z >> np.uint64(31))
+    return (z >> np.uint64(11)).astype(np.float64) * INV_2_53
+
+
 def cr_log(x: float) -> float:
     """Correctly rounded natural log (50-digit decimal, then one rounding).
     glibc's math.log (what the reference calls) is misrounded by 1 ulp on
@@ -576,8 +588,11 @@ def serial_cycles(draft, target, prompt, K=50, k=3, ratio=5, temperature=0.0, ma
     def draft_step():                                  # engine.py:198-221
         if tree.frontier:
             anc = 0 if anchor_origin else tree.root
-            dists = [draft.next_distribution(st["base"] + [tree.token[x] for x in tree.path_to(h, anc)],
-                                             t_score) for h in tree.frontier]
+            paths = [[tree.token[x] for x in tree.path_to(h, anc)] for h in tree.frontier]
+            if hasattr(draft, "tree_distributions") and all(paths):   # one masked pass (lm.py:155-163)
+                dists = draft.tree_distributions(st["base"], paths, t_score)
+            else:
+                dists = [draft.next_distribution(st["base"] + p, t_score) for p in paths]
         else:
             dists = [draft.next_distribution(committed(), t_score)]
         try:
@@ -593,7 +608,10 @@ def serial_cycles(draft, target, prompt, K=50, k=3, ratio=5, temperature=0.0, ma
             tok = sample_index(rng, d) if sampling else argmax_token(d)
             return False, 0, (), tok
         ctx = committed()
-        dists = [target.next_distribution(ctx + toks[:i], t_score) for i in range(len(toks) + 1)]
+        if hasattr(target, "chain_distributions"):   # the chain in one pass
+            dists = target.chain_distributions(ctx, list(toks), t_score)
+        else:
+            dists = [target.next_distribution(ctx + toks[:i], t_score) for i in range(len(toks) + 1)]
         if sampling:
             acc, corr = verify_sampling(dists, [1.0] * len(toks), toks, rng)
         else:

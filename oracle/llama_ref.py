@@ -132,6 +132,86 @@ class RefLlama:
         self.tokens, self.kv = [], []
         return self._extend(list(tokens))
 
+    # ------------------------------------------------------------ batched passes
+    def _sync(self, prefix: list[int]) -> None:
+        """Make the cached stream exactly `prefix` (reuse the common part)."""
+        c, m = 0, min(len(prefix), len(self.tokens))
+        while c < m and prefix[c] == self.tokens[c]:
+            c += 1
+        self.tokens = self.tokens[:c]
+        self.kv = [(k[:c], v[:c]) for k, v in self.kv]
+        if c < len(prefix):
+            self._extend(prefix[c:], "none")
+
+    def chain_logits(self, ctx: list[int], toks: list[int]) -> torch.Tensor:
+        """Logits after ctx + toks[:i] for i = 0..len(toks): one pass over
+        the chain (a verify's rows) instead of len(toks) + 1 extensions."""
+        ctx = [int(t) for t in ctx]
+        self._sync(ctx[:-1])
+        return self._extend([ctx[-1]] + [int(t) for t in toks], "all")
+
+    def tree_logits(self, base: list[int], paths: list[list[int]]) -> torch.Tensor:
+        """Logits after base + path for each path: one masked pass over the
+        newest tree layer (each row's last token), attending to the cached
+        base stream plus its ancestors' keys, which are kept per node (keyed
+        by the node's full context) from the layers that produced them."""
+        base = [int(t) for t in base]
+        self._sync(base)
+        if not hasattr(self, "node_kv") or len(self.node_kv) > 50000:
+            self.node_kv = {}
+        nb = len(base)
+        for key in [k for k in self.node_kv if len(k) <= nb]:   # now part of the stream
+            del self.node_kv[key]
+        bt = tuple(base)
+        ctxs = [bt + tuple(int(t) for t in p) for p in paths]
+        # nodes whose keys are missing (first layers, or after a reset): by depth
+        need = sorted({c[:j] for c in ctxs for j in range(nb + 1, len(c)) if c[:j] not in self.node_kv}, key=len)
+        while need:
+            d = len(need[0])
+            self._tree_rows([c for c in need if len(c) == d], nb)
+            need = [c for c in need if len(c) > d]
+        return self._tree_rows(ctxs, nb)
+
+    def _tree_rows(self, ctxs: list[tuple], nb: int) -> torch.Tensor:
+        c = self.cfg
+        n = len(ctxs)
+        nh, nkv, hd = c.n_heads, c.n_kv_heads, c.head_dim
+        g = nh // nkv
+        pos = torch.tensor([len(x) - 1 for x in ctxs])
+        x = self.w["embed"][torch.tensor([x[-1] for x in ctxs])]
+        own = [[] for _ in range(n)]
+        for i in range(c.n_layers):
+            p = f"l{i}."
+            h = self._rms(x, self.w[p + "attn_norm"])
+            q = h @ self.w[p + "wq"].T
+            k = h @ self.w[p + "wk"].T
+            v = h @ self.w[p + "wv"].T
+            if c.qkv_bias:
+                q, k, v = q + self.w[p + "bq"], k + self.w[p + "bk"], v + self.w[p + "bv"]
+            q = self._rope(q.view(n, nh, hd), pos) / math.sqrt(hd)
+            k = self._rope(k.view(n, nkv, hd), pos)
+            v = v.view(n, nkv, hd)
+            Kb, Vb = self.kv[i]
+            Kb = Kb[:nb].repeat_interleave(g, dim=1)
+            Vb = Vb[:nb].repeat_interleave(g, dim=1)
+            sb = torch.einsum("nhd,thd->nht", q, Kb)          # every row sees the whole base
+            o = torch.empty(n, nh, hd)
+            for r, cx in enumerate(ctxs):
+                anc = [self.node_kv[cx[:j]][i] for j in range(nb + 1, len(cx))]
+                ke = torch.stack([a[0] for a in anc] + [k[r]]).repeat_interleave(g, dim=1)   # [e, nh, hd]
+                ve = torch.stack([a[1] for a in anc] + [v[r]]).repeat_interleave(g, dim=1)
+                se = torch.einsum("hd,ehd->he", q[r], ke)
+                a = torch.softmax(torch.cat([sb[r], se], dim=-1), dim=-1)
+                o[r] = torch.einsum("ht,thd->hd", a[:, :nb], Vb) + torch.einsum("he,ehd->hd", a[:, nb:], ve)
+                own[r].append((k[r], v[r]))
+            x = x + o.reshape(n, nh * hd) @ self.w[p + "wo"].T
+            h = self._rms(x, self.w[p + "mlp_norm"])
+            x = x + (torch.nn.functional.silu(h @ self.w[p + "wg"].T) * (h @ self.w[p + "wu"].T)) @ self.w[p + "wd"].T
+        for r, cx in enumerate(ctxs):
+            self.node_kv[cx] = own[r]
+        x = self._rms(x, self.w["norm"])
+        return x @ self.w["lm_head"].T
+
 
 class RefModel:
     """The reference's model protocol (lm.py:109-196) over RefLlama, with the
@@ -150,18 +230,43 @@ class RefModel:
             out = np.zeros(self.vocab_size)
             out[self.eos_token] = 1.0
             return out
-        lg = self.llama.logits_for(list(ctx)).double()
+        return self._dist(ctx, self.llama.logits_for(list(ctx)), temperature)
+
+    def _dist(self, ctx, lg, temperature):
+        if self.eos_token is not None and ctx[-1] == self.eos_token:
+            out = np.zeros(self.vocab_size)
+            out[self.eos_token] = 1.0
+            return out
+        lg = lg.double()
         if self.bias is not None and self.bias.sharpness != 0.0:
-            from oracle.card_oracle import kgram_uniforms
+            from oracle.card_oracle import kgram_uniforms_np
 
             tail = [int(t) for t in ctx][-self.bias.order:]
-            u = np.array(kgram_uniforms(self.bias.seed, tail, self.vocab_size), dtype=np.float32)
+            u = kgram_uniforms_np(self.bias.seed, tail, self.vocab_size).astype(np.float32)
             if self.bias.mix_weight:
-                u = u + np.float32(self.bias.mix_weight) * np.array(
-                    kgram_uniforms(self.bias.mix_seed, tail, self.vocab_size), dtype=np.float32)
+                u = u + np.float32(self.bias.mix_weight) * kgram_uniforms_np(
+                    self.bias.mix_seed, tail, self.vocab_size).astype(np.float32)
             lg = (lg.float() + torch.from_numpy(np.float32(self.bias.sharpness) * u)).double()
         if temperature == 0.0:
             out = np.zeros(self.vocab_size)
             out[int(torch.argmax(lg))] = 1.0
             return out
         return torch.softmax(lg / temperature, dim=0).numpy()
+
+
+class BatchedRefModel(RefModel):
+    """RefModel with the batched passes a real backend makes (lm.py:155-163:
+    "a real backend would batch this into a single masked pass"): a draft
+    tree layer in one masked forward (`tree_distributions`) and a verify
+    chain in one forward (`chain_distributions`).  card_oracle.serial_cycles
+    uses them when present; same distributions up to fp32 summation order.
+    Used by bench.py's CPU legs, where one-context-at-a-time fp32 forwards
+    would make a CARD cycle take minutes."""
+
+    def tree_distributions(self, base, paths, temperature=1.0):
+        lg = self.llama.tree_logits(list(base), [list(p) for p in paths])
+        return [self._dist(list(base) + list(p), lg[i], temperature) for i, p in enumerate(paths)]
+
+    def chain_distributions(self, ctx, toks, temperature=1.0):
+        lg = self.llama.chain_logits(list(ctx), list(toks))
+        return [self._dist(list(ctx) + list(toks[:i]), lg[i], temperature) for i in range(len(toks) + 1)]

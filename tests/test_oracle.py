@@ -100,3 +100,14 @@ def test_reference_fixture_goldens():
                            t.params_billions, t.forward_latency, d.params_billions)
                 for p in g["corpus"]]
         assert O.aggregate(runs) == g["ablation"][variant]
+
+
+def test_kgram_uniforms_vectorised_equals_scalar():
+    """The numpy k-gram uniforms (CPU baselines' logit bias) are the scalar
+    restatement's values bit for bit (_kernels_py.py:27-45)."""
+    import numpy as np
+
+    from oracle.card_oracle import kgram_uniforms, kgram_uniforms_np
+
+    for seed, tail in [(11, [3, 5]), (131, [0]), (7, [123456, 99]), (0, [])]:
+        assert np.array_equal(np.array(kgram_uniforms(seed, tail, 3000)), kgram_uniforms_np(seed, tail, 3000))

@@ -100,3 +100,45 @@ def test_safetensors_checkpoint_round_trip_and_hf(tmp_path):
     bad.write_bytes(b"\x01\x00")
     with pytest.raises(ConfigError):
         load_llama_safetensors(str(bad), _cfgs()[0])
+
+
+def test_batched_passes_equal_per_context():
+    """The batched CPU passes bench.py's CPU legs use (one masked pass per
+    draft tree layer, one pass per verify chain) give the per-context
+    distributions, and the oracle CARD loop driven by them emits the same
+    tokens and trace as the per-context protocol (lm.py:155-163)."""
+    import numpy as np
+
+    from oracle import card_oracle as O
+    from oracle.llama_ref import BatchedRefModel, RefModel
+    from paper_2508_04462_b200.llama import PRESETS, init_weights
+    from paper_2508_04462_b200.lm import LogitBias
+
+    cfg = _cfgs()[1]
+    w = init_weights(cfg, seed=5)
+    ref, bat = RefLlama(cfg, w), RefLlama(cfg, w)
+    base = list(range(3, 40))
+    paths = [[5], [6], [5, 9], [5, 10], [6, 11, 12], [5, 9, 13, 14]]
+    got = bat.tree_logits(base, paths)
+    for i, p in enumerate(paths):
+        assert torch.allclose(got[i], ref.logits_for(base + p), atol=2e-5), i
+    got = bat.tree_logits(base + [5], [[9, 13], [10, 2]])   # base grew: memo entries reused / pruned
+    assert torch.allclose(got[0], ref.logits_for(base + [5, 9, 13]), atol=2e-5)
+    assert torch.allclose(got[1], ref.logits_for(base + [5, 10, 2]), atol=2e-5)
+    ch = bat.chain_logits(base, [4, 8, 1])
+    for i in range(4):
+        assert torch.allclose(ch[i], ref.logits_for(base + [4, 8, 1][:i]), atol=2e-5)
+
+    cd, ct = PRESETS["tiny-draft"], PRESETS["tiny-target"]
+    wd, wt = init_weights(cd, seed=1), init_weights(ct, seed=2)
+    bias = LogitBias(seed=11, order=2, sharpness=3e3, mix_seed=131, mix_weight=0.5)
+    prompt = [int(x) for x in np.random.default_rng(4).integers(0, ct.vocab_size, 16)]
+    cfg_run = dict(K=12, k=3, ratio=3, max_new_tokens=40)
+    runs = []
+    for M in (RefModel, BatchedRefModel):
+        runs.append(O.run_serial(M(cd, wd, forward_latency=1.0, bias=bias),
+                                 M(ct, wt, forward_latency=7.0, bias=bias), prompt, **cfg_run))
+    assert runs[0][0] == runs[1][0]
+    assert [(e.event, e.hit, e.candidate_len, e.accepted_len) for e in runs[0][1]] == \
+           [(e.event, e.hit, e.candidate_len, e.accepted_len) for e in runs[1][1]]
+    assert any(e.accepted_len > 0 for e in runs[0][1])
