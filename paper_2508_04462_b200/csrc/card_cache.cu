@@ -183,6 +183,8 @@ __global__ void init_root_kernel(Bufs b, const int32_t* d_tok, int tok, int bump
 struct PoolSmem {
     double* w;
     double* e;
+    ulonglong2* key;   // (-w, token, parent) as two u64 compared lexicographically
+    uint32_t* k32;     // key.x >> 32, padded to a multiple of 4 (first-pass compare)
     int32_t* tok;
     int32_t* pid;
     int32_t* rank;
@@ -192,10 +194,23 @@ __device__ __forceinline__ PoolSmem carve_pool(char* smem, int P) {
     PoolSmem p;
     p.w = (double*)smem;
     p.e = p.w + P;
-    p.tok = (int32_t*)(p.e + P);
+    p.key = (ulonglong2*)(p.e + P);
+    p.k32 = (uint32_t*)(p.key + P);
+    p.tok = (int32_t*)(p.k32 + ((P + 3) & ~3));
     p.pid = p.tok + P;
     p.rank = p.pid + P;
     return p;
+}
+
+// order key (-weight, token, parent node id) of cache.py:237-239 for pool
+// slot s, compared as (hi, lo) pairs: weight descending by its bit pattern
+// (-0.0 folds into +0.0 as the double compare does), then token, then parent
+// ascending; invalid slots sort last
+__device__ __forceinline__ ulonglong2 pool_key(const PoolSmem& p, int s) {
+    if (p.tok[s] < 0) return make_ulonglong2(~0ull, ~0ull);
+    const unsigned long long b = (unsigned long long)__double_as_longlong(p.w[s] + 0.0);
+    const unsigned long long asc = (b >> 63) ? ~b : (b | (1ull << 63));   // ascending in w
+    return make_ulonglong2(~asc, ((unsigned long long)(uint32_t)p.tok[s] << 32) | (uint32_t)p.pid[s]);
 }
 
 // Builds the extension pool (cache.py:190-222) into smem; returns P.
@@ -221,18 +236,12 @@ __device__ int build_pool(const Bufs& b, const int32_t* c_tok, const double* c_v
     return P;
 }
 
-// key (-weight, token, parent node id) of cache.py:237-239
-__device__ __forceinline__ bool pool_before(const PoolSmem& p, int a, int c) {
-    if (p.w[a] != p.w[c]) return p.w[a] > p.w[c];
-    if (p.tok[a] != p.tok[c]) return p.tok[a] < p.tok[c];
-    return p.pid[a] < p.pid[c];
-}
 
 __global__ void __launch_bounds__(kThreads) expand_kernel(Bufs b, const int32_t* c_tok, const double* c_val,
                                                           const int32_t* c_cnt, int n_rows_host, int vals_are_logp,
                                                           const int32_t* skip) {
     extern __shared__ __align__(16) char smem[];
-    __shared__ int sh_flag, sh_npar, sh_valid, sh_m, sh_m2, sh_dead;
+    __shared__ int sh_flag, sh_npar, sh_valid, sh_m, sh_cnt[3], sh_dead;
     __shared__ int lvl[2][kMaxK];
     card_cache_state& S = *b.st;
     const int tid = threadIdx.x;
@@ -256,7 +265,7 @@ __global__ void __launch_bounds__(kThreads) expand_kernel(Bufs b, const int32_t*
         sh_npar = npar;
         sh_valid = 0;
         sh_dead = 0;
-        sh_m2 = 0;
+        sh_cnt[0] = 0;
         sh_m = S.n_frontier;
     }
     __syncthreads();
@@ -270,14 +279,47 @@ __global__ void __launch_bounds__(kThreads) expand_kernel(Bufs b, const int32_t*
     PoolSmem p = carve_pool(smem, npar * k);
     const int P = build_pool(b, c_tok, c_val, c_cnt, vals_are_logp, p, npar, k);
     __syncthreads();
-    // parallel rank sort; (token, parent) pairs are unique so ranks are distinct
-    for (int s = tid; s < P; s += blockDim.x) {
-        if (p.tok[s] < 0) continue;
-        int r = 0;
-        for (int t = 0; t < P; ++t)
-            if (p.tok[t] >= 0 && pool_before(p, t, s)) ++r;
-        p.rank[s] = r;
-        atomicAdd(&sh_valid, 1);
+    // parallel rank sort; (token, parent) pairs are unique so ranks are
+    // distinct.  Keys packed once; each slot's count is split over `parts`
+    // threads (all warps busy instead of P / 32)
+    const int P4 = (P + 3) & ~3;
+    for (int s = tid; s < P4; s += blockDim.x) {
+        const ulonglong2 ks = s < P ? pool_key(p, s) : make_ulonglong2(~0ull, ~0ull);
+        if (s < P) {
+            p.key[s] = ks;
+            p.rank[s] = 0;
+        }
+        p.k32[s] = (uint32_t)(ks.x >> 32);
+        // valid slots, one shared atomic per warp (same-address atomics serialise)
+        const unsigned am = __activemask();
+        const unsigned v = __ballot_sync(am, s < P && p.tok[s] >= 0);
+        if ((tid & 31) == __ffs(am) - 1) atomicAdd(&sh_valid, __popc(v));
+    }
+    __syncthreads();
+    {   // count the slots before s: the top 32 key bits decide all but near-ties
+        const int parts = P <= (int)blockDim.x ? min(8, (int)blockDim.x / P) : 1;
+        for (int i = tid; i < P * parts; i += blockDim.x) {
+            const int s = i % P, part = i / P;
+            if (p.tok[s] < 0) continue;
+            const ulonglong2 ks = p.key[s];
+            const uint32_t h = (uint32_t)(ks.x >> 32);
+            int r = 0;
+            const int t0 = (P4 / 4 * part / parts) * 4, t1 = (P4 / 4 * (part + 1) / parts) * 4;
+            for (int t = t0; t < t1; t += 4) {
+                const uint4 q = *reinterpret_cast<const uint4*>(p.k32 + t);
+                r += (q.x < h) + (q.y < h) + (q.z < h) + (q.w < h);
+                if (q.x == h || q.y == h || q.z == h || q.w == h) {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const ulonglong2 kt = p.key[t + j];
+                        if (t + j < P && (uint32_t)(kt.x >> 32) == h && (kt.x < ks.x || (kt.x == ks.x && kt.y < ks.y)))
+                            ++r;
+                    }
+                }
+            }
+            if (parts == 1) p.rank[s] = r;
+            else atomicAdd(&p.rank[s], r);
+        }
     }
     __syncthreads();
     const int nnew = sh_valid < K ? sh_valid : K;
@@ -304,36 +346,33 @@ __global__ void __launch_bounds__(kThreads) expand_kernel(Bufs b, const int32_t*
         for (int i = tid; i < npar; i += blockDim.x) b.has_kv[b.frontier_old[i]] = 1;
     __syncthreads();
     const int stamp = S.stamp + 1;
-    // keep = every ancestor of the new frontier (cache.py:255-260)
-    for (int i = tid; i < nnew; i += blockDim.x) {
-        int cur = b.parent[n0 + i];
-        while (cur >= 0 && b.mark[cur] != stamp) {
-            b.mark[cur] = stamp;
-            cur = b.parent[cur];
-        }
-    }
-    __syncthreads();
-    // level-synchronous dead-end pruning from the old frontier (cache.py:261-271)
+    // Level-synchronous dead-end pruning from the old frontier
+    // (cache.py:261-271).  The reference's `keep` set (ancestors of the new
+    // frontier, cache.py:255-260) needs no pass of its own here: nkids counts
+    // a node's alive children, and every ancestor of a new frontier node has
+    // one (its child on that path), so `nkids != 0` already stops the climb
+    // wherever `keep` would.
+    // A parent joins the next level when this pass takes its last alive
+    // child (the thread whose decrement reaches 0 pushes it, once): the
+    // nodes the reference's per-branch climb would reach next.  Next-level
+    // counts rotate over three slots so each level needs one barrier (slot
+    // (i + 1) % 3 was last read before the previous barrier).
     int m = sh_m, cur_l = 0;
     const int root = S.root;
-    while (m > 0) {
+    for (int lv = 0; m > 0; ++lv) {
+        if (tid == 0) sh_cnt[(lv + 1) % 3] = 0;
         for (int i = tid; i < m; i += blockDim.x) {
             const int x = lvl[cur_l][i];
-            if (x == root || b.mark[x] == stamp || !b.alive[x] || b.nkids[x] != 0) continue;
-            b.alive[x] = 0;
-            atomicAdd(&sh_dead, 1);
             const int par = b.parent[x];
-            if (par >= 0) {
-                atomicSub(&b.nkids[par], 1);
-                if (atomicExch(&b.mark2[par], stamp) != stamp) lvl[cur_l ^ 1][atomicAdd(&sh_m2, 1)] = par;
-            }
+            if (x == root || (lv == 0 && (!b.alive[x] || b.nkids[x] != 0))) continue;
+            b.alive[x] = 0;
+            const unsigned am = __activemask();   // the lanes killing a node here
+            if ((tid & 31) == __ffs(am) - 1) atomicAdd(&sh_dead, __popc(am));
+            if (par >= 0 && atomicSub(&b.nkids[par], 1) == 1) lvl[cur_l ^ 1][atomicAdd(&sh_cnt[lv % 3], 1)] = par;
         }
         __syncthreads();
-        m = sh_m2;
+        m = sh_cnt[lv % 3];
         cur_l ^= 1;
-        __syncthreads();
-        if (tid == 0) sh_m2 = 0;
-        __syncthreads();
     }
     if (tid == 0) {
         S.stamp = stamp;
@@ -717,7 +756,8 @@ __global__ void clear_status_kernel(Bufs b) {
 
 static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
-static int pool_smem_bytes(int P) { return P * (8 + 8 + 4 + 4 + 4); }
+// w, e, key, k32 (padded to 4), tok, pid, rank
+static int pool_smem_bytes(int P) { return P * (8 + 8 + 16 + 4 + 4 + 4 + 4) + 16; }
 
 }  // namespace card
 
