@@ -64,6 +64,31 @@ __global__ void embed_kernel(const int32_t* __restrict__ tok, const int32_t* dM,
         for (int i = threadIdx.x; i < H; i += blockDim.x) x[(int64_t)r * H + i] = ldf(E, t * H + i);
         return;
     }
+    if constexpr (sizeof(W) == 2) {   // bf16 table: 32-byte loads, the bf16 copy is the row itself
+        for (int g16 = threadIdx.x; g16 < H / 16; g16 += blockDim.x) {
+            const uint4* src = reinterpret_cast<const uint4*>(E + t * H + g16 * 16);
+            const uint4 a[2] = {src[0], src[1]};
+            const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(a);
+            float v[16];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const float2 f = __bfloat1622float2(h2[i]);
+                v[2 * i] = f.x;
+                v[2 * i + 1] = f.y;
+            }
+            float acc = 0.f;
+#pragma unroll
+            for (int i = 0; i < 16; ++i) acc = fmaf(v[i], v[i], acc);
+            float4* xd = reinterpret_cast<float4*>(x + (int64_t)r * H + g16 * 16);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) xd[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+            uint4* bd = reinterpret_cast<uint4*>(xb + (int64_t)r * H + g16 * 16);
+            bd[0] = a[0];
+            bd[1] = a[1];
+            ssq[(int64_t)g16 * ssq_ld + r] = acc;
+        }
+        return;
+    }
     for (int g16 = threadIdx.x; g16 < H / 16; g16 += blockDim.x) {
         float acc = 0.f;
 #pragma unroll
@@ -1178,9 +1203,20 @@ __global__ void __launch_bounds__(256) tiles_merge_kernel(const int32_t* dM, int
         tt[q] = 0x7fffffff;
     }
     float lm = -INFINITY;
-    for (int s = threadIdx.x; s < S; s += blockDim.x) {
+    constexpr int kKeep = 8;   // records' (max, sum) kept in registers for the second pass
+    float rm[kKeep], rs[kKeep];
+    int j = 0;
+    for (int s = threadIdx.x; s < S; s += blockDim.x, ++j) {
         const float* p = base + (int64_t)s * kTopkRec;
         lm = fmaxf(lm, p[0]);
+        if (j < kKeep) {
+#pragma unroll
+            for (int q = 0; q < kKeep; ++q)
+                if (q == j) {
+                    rm[q] = p[0];
+                    rs[q] = p[1];
+                }
+        }
 #pragma unroll
         for (int c = 0; c < kTopkKT; ++c) {
             float cv = p[2 + 2 * c];
@@ -1205,9 +1241,22 @@ __global__ void __launch_bounds__(256) tiles_merge_kernel(const int32_t* dM, int
     for (int w = 1; w < (int)(blockDim.x >> 5); ++w) gmf = fmaxf(gmf, sh_v[w]);
     const double gm = (double)gmf;
     double tot = 0.0;
-    for (int s = threadIdx.x; s < S; s += blockDim.x) {
-        const float* p = base + (int64_t)s * kTopkRec;
-        if (p[1] > 0.f) tot += (double)p[1] * exp((double)p[0] - gm);
+    j = 0;
+    for (int s = threadIdx.x; s < S; s += blockDim.x, ++j) {
+        float m0, s0;
+        if (j < kKeep) {
+#pragma unroll
+            for (int q = 0; q < kKeep; ++q)
+                if (q == j) {
+                    m0 = rm[q];
+                    s0 = rs[q];
+                }
+        } else {
+            const float* p = base + (int64_t)s * kTopkRec;
+            m0 = p[0];
+            s0 = p[1];
+        }
+        if (s0 > 0.f) tot += (double)s0 * exp((double)m0 - gm);
     }
     for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
     if (lane_id() == 0) sh_d[warp_id()] = tot;
