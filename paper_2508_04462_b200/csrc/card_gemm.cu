@@ -309,7 +309,8 @@ __device__ __forceinline__ void epi_chunk(const TcArgs& a, int tile, int n_glob,
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
             float x = v[j] + b;
-            if (a.kg.sharp != 0.f && j < mc) x = kg_apply_step(a.kg, x, step, kgs[2 * (m0 + j)], kgs[2 * (m0 + j) + 1]);
+            if (a.kg.sharp != 0.f && j < mc)   // (the second stream's state only when it is mixed in)
+                x = kg_apply_step(a.kg, x, step, kgs[2 * (m0 + j)], a.kg.mixw != 0.f ? kgs[2 * (m0 + j) + 1] : 0ull);
             sts_f32(xch + (uint32_t)((j * 128 + n_local) * 4), (live && j < mc) ? x * a.inv_temp : -INFINITY);
         }
         named_bar(gbar, kGroupThreads);
@@ -370,17 +371,41 @@ __device__ __forceinline__ void epi_chunk(const TcArgs& a, int tile, int n_glob,
 #pragma unroll
         for (int q = 0; q < 16; ++q)
             if (xs[q] >= T && xs[q] != -INFINITY) insert(xs[q], tile * kTileN + sub + 8 * ((q + rot) & 15));
+        // merge the 8 lanes' sorted top-4 lists: per butterfly round a
+        // bitonic merge (best of mine[q] vs partner[3-q], then two
+        // compare-exchange layers) instead of four insertions
+        static_assert(kTopkKT == 4, "bitonic top-4 merge");
+        auto better = [](float av, int ai, float bv, int bi) { return av > bv || (av == bv && ai < bi); };
+        auto cx = [&](int i, int j) {   // order (i, j) best first
+            const bool sw = better(tv[j], tt[j], tv[i], tt[i]);
+            const float fi = tv[i], fj = tv[j];
+            const int ii = tt[i], ij = tt[j];
+            tv[i] = sw ? fj : fi;
+            tt[i] = sw ? ij : ii;
+            tv[j] = sw ? fi : fj;
+            tt[j] = sw ? ii : ij;
+        };
 #pragma unroll
         for (int o = 1; o < 8; o <<= 1) {
-            float ov[kTopkKT];
-            int ot[kTopkKT];
+            // (q, 3 - q) pairs: both partner values are read before either
+            // slot changes (fewer live registers than four at once)
 #pragma unroll
-            for (int q = 0; q < kTopkKT; ++q) {
-                ov[q] = __shfl_xor_sync(0xffffffffu, tv[q], o);
-                ot[q] = __shfl_xor_sync(0xffffffffu, tt[q], o);
+            for (int q = 0; q < 2; ++q) {
+                const float pa = __shfl_xor_sync(0xffffffffu, tv[3 - q], o), pb = __shfl_xor_sync(0xffffffffu, tv[q], o);
+                const int ia = __shfl_xor_sync(0xffffffffu, tt[3 - q], o), ib = __shfl_xor_sync(0xffffffffu, tt[q], o);
+                if (better(pa, ia, tv[q], tt[q])) {
+                    tv[q] = pa;
+                    tt[q] = ia;
+                }
+                if (better(pb, ib, tv[3 - q], tt[3 - q])) {
+                    tv[3 - q] = pb;
+                    tt[3 - q] = ib;
+                }
             }
-#pragma unroll
-            for (int q = 0; q < kTopkKT; ++q) insert(ov[q], ot[q]);
+            cx(0, 2);
+            cx(1, 3);
+            cx(0, 1);
+            cx(2, 3);
         }
         if (sub == 0 && jt < mc) {
             float* rec = a.out_f32 + ((int64_t)(m0 + jt) * a.n_tiles + tile) * kTopkRec;
