@@ -164,6 +164,7 @@ constexpr int kBK = 64;       // bf16 K per stage = one 128-byte swizzle atom
 // their epilogues are bound by the math of 4 warps; narrow ones NG = 1 (two
 // CTAs per SM must fit the register file).
 constexpr int kGroupThreads = 128;
+constexpr int kXchLd = 136;   // row stride (floats) of an epilogue group's [16][128] exchange buffer
 template <int NG>
 struct Roles {
     static constexpr int kEpiThreads = NG * kGroupThreads;
@@ -311,10 +312,10 @@ __device__ __forceinline__ void epi_chunk(const TcArgs& a, int tile, int n_glob,
             float x = v[j] + b;
             if (a.kg.sharp != 0.f && j < mc)   // (the second stream's state only when it is mixed in)
                 x = kg_apply_step(a.kg, x, step, kgs[2 * (m0 + j)], a.kg.mixw != 0.f ? kgs[2 * (m0 + j) + 1] : 0ull);
-            sts_f32(xch + (uint32_t)((j * 128 + n_local) * 4), (live && j < mc) ? x * a.inv_temp : -INFINITY);
+            sts_f32(xch + (uint32_t)((j * kXchLd + n_local) * 4), (live && j < mc) ? x * a.inv_temp : -INFINITY);
         }
         named_bar(gbar, kGroupThreads);
-        const int jt = n_local >> 3, sub = n_local & 7, rot = (n_local >> 3) & 3;
+        const int jt = n_local >> 3, sub = n_local & 7;
         float mx = -INFINITY, sum = 0.f;
         float tv[kTopkKT];
         int tt[kTopkKT];
@@ -339,10 +340,12 @@ __device__ __forceinline__ void epi_chunk(const TcArgs& a, int tile, int n_glob,
         // maxima (those are 4 distinct elements), so each lane inserts only
         // its elements >= T (a handful per tile).  The sum-exp is taken
         // against the tile max directly (no rescaling chain).
+        // element q of this lane: vocab row sub + 8 q of token jt (rows of
+        // kXchLd = 136 floats: the warp's 4 tokens x 8 lanes hit 32 banks)
+        const uint32_t rbase = xch + (uint32_t)((jt * kXchLd + sub) * 4);
         float xs[16];
 #pragma unroll
-        for (int q = 0; q < 16; ++q)   // rotated rows: the 32 lanes hit 32 banks
-            xs[q] = lds_f32(xch + (uint32_t)((jt * 128 + sub + 8 * ((q + rot) & 15)) * 4));
+        for (int q = 0; q < 16; ++q) xs[q] = lds_f32(rbase + (uint32_t)(q * 32));
         float lm = xs[0];
 #pragma unroll
         for (int q = 1; q < 16; ++q) lm = fmaxf(lm, xs[q]);
@@ -368,9 +371,16 @@ __device__ __forceinline__ void epi_chunk(const TcArgs& a, int tile, int n_glob,
         const unsigned grpmask = 0xffu << (lane_id_ & 24);
         const int src = __ffs(hit & grpmask) - 1;
         const float T = __shfl_sync(0xffffffffu, lm, src);
+        // a handful of candidates: walk their mask (a predicated insertion
+        // per element would execute all 16)
+        unsigned cand = 0;
 #pragma unroll
-        for (int q = 0; q < 16; ++q)
-            if (xs[q] >= T && xs[q] != -INFINITY) insert(xs[q], tile * kTileN + sub + 8 * ((q + rot) & 15));
+        for (int q = 0; q < 16; ++q) cand |= (xs[q] >= T && xs[q] != -INFINITY) ? (1u << q) : 0u;
+        while (cand) {
+            const int q = __ffs(cand) - 1;
+            cand &= cand - 1;
+            insert(lds_f32(rbase + (uint32_t)(q * 32)), tile * kTileN + sub + 8 * q);
+        }
         // merge the 8 lanes' sorted top-4 lists: per butterfly round a
         // bitonic merge (best of mine[q] vs partner[3-q], then two
         // compare-exchange layers) instead of four insertions
@@ -478,8 +488,8 @@ __global__ void __launch_bounds__(Roles<NG>::kThreads, 1) tc_gemm_kernel(const _
     uint64_t* tempty = tfull + 2;   // [2]
     uint64_t* rbar = tempty + 2;    // split-K: every rank's slice of my rows landed (bulk DSMEM copies)
     uint32_t* tmem_slot = (uint32_t*)(rbar + 2);
-    float* xch = (float*)(tmem_slot + 4);   // [groups][16][128] (group 1's only when Mpad > 16)
-    float* invs = xch + NG * 16 * 128;   // [256] per-token rsqrt(mean x^2 + eps)
+    float* xch = (float*)(tmem_slot + 4);   // [groups][16][kXchLd] (group 1's only when Mpad > 16)
+    float* invs = xch + NG * 16 * kXchLd;   // [256] per-token rsqrt(mean x^2 + eps)
     int* tpos = (int*)(invs + 256);          // [256] QKV: RoPE position of each token row
     int* tslot = tpos + 256;                 // [256] QKV: KV-cache slot of each token row
     uint64_t* kgs = (uint64_t*)(tslot + 256);   // [256][2] lm_head: k-gram stream state of each output row
@@ -692,7 +702,7 @@ __global__ void __launch_bounds__(Roles<NG>::kThreads, 1) tc_gemm_kernel(const _
             const uint32_t trow = tmem_base + ((uint32_t)(wq * 32) << 16) + (uint32_t)(acc * a.Mpad);
             // cluster mode (splits > 1): the accumulator stays in TMEM until
             // every rank of the cluster has finished its main loop (below)
-            float* gx = xch + grp * 16 * 128;
+            float* gx = xch + grp * 16 * kXchLd;
             for (int m0 = grp * 16; m0 < M && !CL; m0 += NG * 16) {
                 float v[16];
                 tmem_ld16(trow + (uint32_t)m0, v);
@@ -1319,7 +1329,7 @@ int card_linear_create(const void* W, int N, int K, int wdtype, const void* X, i
     int ctas_per_sm = (cols <= 256 && Mpad < 64) ? 2 : 1;
     const int stage_bytes = kTileN * kBK * 2 + Mpad * kBK * 2;
     int budget = (ctas_per_sm == 2 ? 110 : 220) * 1024;
-    const int extra = 1024 + 64 * 8 + epi_groups(epi, Mpad) * 16 * 128 * 4 + 3 * 256 * 4 + 2 * 256 * 8 + 64;
+    const int extra = 1024 + 64 * 8 + epi_groups(epi, Mpad) * 16 * kXchLd * 4 + 3 * 256 * 4 + 2 * 256 * 8 + 64;
     int stages = (budget - extra) / stage_bytes;
     if (stages > 8) stages = 8;
     if (stages < 2) stages = 2;
