@@ -352,9 +352,12 @@ __device__ __forceinline__ void epi_chunk(const TcArgs& a, int tile, int n_glob,
         float tmx = lm;
 #pragma unroll
         for (int o = 1; o < 8; o <<= 1) tmx = fmaxf(tmx, __shfl_xor_sync(0xffffffffu, tmx, o));
+        // exp(-inf - m) = +0 adds nothing; a chunk of padding rows only (tmx
+        // = -inf) subtracts 0 instead, so no element needs the -inf test
+        const float tsub = tmx == -INFINITY ? 0.f : tmx;
         float s = 0.f;
 #pragma unroll
-        for (int q = 0; q < 16; ++q) s += xs[q] == -INFINITY ? 0.f : __expf(xs[q] - tmx);
+        for (int q = 0; q < 16; ++q) s += __expf(xs[q] - tsub);
 #pragma unroll
         for (int o = 1; o < 8; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
         mx = tmx;
