@@ -1206,32 +1206,45 @@ __global__ void __launch_bounds__(256) tiles_merge_kernel(const int32_t* dM, int
     constexpr int kKeep = 8;   // records' (max, sum) kept in registers for the second pass
     float rm[kKeep], rs[kKeep];
     int j = 0;
+    static_assert(kTopkKT == 4 && kTopkRec % 2 == 0, "bitonic top-4 merge of 8-byte aligned records");
+    auto cx = [&](int i, int k) {   // order slots (i, k) best first
+        const bool sw = lbefore(tv[k], tt[k], tv[i], tt[i]);
+        const float fi = tv[i], fk = tv[k];
+        const int ii = tt[i], ik = tt[k];
+        tv[i] = sw ? fk : fi;
+        tt[i] = sw ? ik : ii;
+        tv[k] = sw ? fi : fk;
+        tt[k] = sw ? ii : ik;
+    };
     for (int s = threadIdx.x; s < S; s += blockDim.x, ++j) {
-        const float* p = base + (int64_t)s * kTopkRec;
-        lm = fmaxf(lm, p[0]);
+        const float2* p2 = reinterpret_cast<const float2*>(base + (int64_t)s * kTopkRec);
+        const float2 h = p2[0];   // (max, sum-exp)
+        float2 c[kTopkKT];        // the record's sorted top-4 (value, token bits)
+#pragma unroll
+        for (int q = 0; q < kTopkKT; ++q) c[q] = p2[1 + q];
+        lm = fmaxf(lm, h.x);
         if (j < kKeep) {
 #pragma unroll
             for (int q = 0; q < kKeep; ++q)
                 if (q == j) {
-                    rm[q] = p[0];
-                    rs[q] = p[1];
+                    rm[q] = h.x;
+                    rs[q] = h.y;
                 }
         }
+        // both lists sorted: best of mine[q] / theirs[3 - q], then a bitonic
+        // sort of the four (8 compare-selects instead of 4 insertions)
 #pragma unroll
-        for (int c = 0; c < kTopkKT; ++c) {
-            float cv = p[2 + 2 * c];
-            int ci = __float_as_int(p[3 + 2 * c]);
-#pragma unroll
-            for (int q = 0; q < kTopkKT; ++q) {
-                const bool bt = lbefore(cv, ci, tv[q], tt[q]);
-                const float ov = tv[q];
-                const int oi = tt[q];
-                tv[q] = bt ? cv : ov;
-                tt[q] = bt ? ci : oi;
-                cv = bt ? ov : cv;
-                ci = bt ? oi : ci;
-            }
+        for (int q = 0; q < kTopkKT; ++q) {
+            const float ov = c[3 - q].x;
+            const int oi = __float_as_int(c[3 - q].y);
+            const bool tk = lbefore(ov, oi, tv[q], tt[q]);
+            tv[q] = tk ? ov : tv[q];
+            tt[q] = tk ? oi : tt[q];
         }
+        cx(0, 2);
+        cx(1, 3);
+        cx(0, 1);
+        cx(2, 3);
     }
     // block max of the record maxima
     for (int o = 16; o > 0; o >>= 1) lm = fmaxf(lm, __shfl_xor_sync(0xffffffffu, lm, o));
